@@ -1,0 +1,180 @@
+/*
+ * spingp_c.h — the C ABI of the B200-native SpInGP sparse-precision inference path.
+ *
+ * This is the drop-in boundary: plain pointers, sizes and
+ * status codes, no C++ or torch types.  The C++ header API in include/spingp/
+ * (the reference's `spingp` namespace) is implemented on top of it, and any
+ * FFI (ctypes, cgo, JNI) binds these symbols directly.
+ *
+ * Which reference interface each entry point replaces (file:line under the
+ * read-only reference tree):
+ *   spingp_state_space        state_space_of            proj/include/spingp/kernels.hpp:326-381
+ *   spingp_discretize         discretize(_with_grad)    proj/include/spingp/kernels.hpp:392-443
+ *   spingp_eval[_device]      log_marginal_likelihood + mll_gradient + predict (training grid)
+ *                                                       SPEC.md:280-306 (assemble :262-279)
+ *   spingp_eval_batched[...]  the same over many independent series (BASELINE cfg3)
+ *   spingp_assemble[_device]  assemble_prior_precision + add_observation_term
+ *   spingp_btd_cr_solve[...]  cr_solve (+ solve/logdet)
+ *   spingp_btd_selinv[...]    selective_inverse
+ *   spingp_btd_matvec[...]    matvec
+ * Error convention: every function returns a spingp_status; NOT_PD carries the
+ * failing block index through `fail_block` (errors.hpp:12-20 NotPositiveDefinite),
+ * SINGULAR_Q likewise (errors.hpp:23-27 SingularProcessNoise).  The C++ layer
+ * rethrows the reference exception types.
+ *
+ * Memory: the caller owns every buffer.  Functions without a `_device` suffix
+ * take HOST pointers and are synchronous (host->device copies, kernels,
+ * device->host copies inside the call).  `_device` variants take DEVICE
+ * pointers, enqueue on the context's stream and return immediately; device-side
+ * failures are then reported by spingp_ctx_status().
+ *
+ * Layouts: all matrices are row-major; a block-tridiagonal (BTD) matrix of n
+ * blocks of size b is stored as diag[n][b][b] and upper[n-1][b][b] (upper[i] is
+ * the (i, i+1) block; the (i+1, i) block is its transpose) — SPEC.md:129-134,220.
+ * Vectors over blocks are x[n][b] (times k right-hand sides: x[n*b][k]).
+ */
+#ifndef SPINGP_C_H
+#define SPINGP_C_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPINGP_ABI_VERSION 1
+
+typedef enum {
+    SPINGP_OK = 0,
+    SPINGP_NOT_PD = 1,          /* a Cholesky pivot failed (NotPositiveDefinite)            */
+    SPINGP_SINGULAR_Q = 2,      /* a process-noise block stayed singular after jitter       */
+    SPINGP_BAD_ARG = 3,         /* invalid argument (std::invalid_argument)                 */
+    SPINGP_CUDA_ERR = 4,        /* CUDA runtime failure                                     */
+    SPINGP_NCCL_ERR = 5,        /* NCCL failure                                             */
+    SPINGP_DUPLICATE_TIME = 6,  /* two training times coincide (DuplicateTimestamp)         */
+    SPINGP_UNSUPPORTED = 7,     /* configuration not implemented by this build              */
+    SPINGP_NEG_VARIANCE = 8     /* a posterior variance fell below -1e-10     */
+} spingp_status;
+
+/* Kernel leaves.  Matérn-ν and EQ follow kernels.hpp:17-49; QP (quasi-periodic:
+ * periodic with J harmonics x Matérn-1/2 envelope, Solin & Särkkä 2014) is the
+ * extension BASELINE cfg5 needs and the reference lacks. */
+typedef enum {
+    SPINGP_MATERN12 = 0,
+    SPINGP_MATERN32 = 1,
+    SPINGP_MATERN52 = 2,
+    SPINGP_EQ = 3,
+    SPINGP_QP = 4
+} spingp_leaf_type;
+
+/* One leaf of a sum kernel.  `order`: EQ approximation order (even, 2..16);
+ * QP number of harmonics J (state dimension 2(J+1)); ignored for Matérn.
+ * Hyperparameters, in the reference's traversal order (kernels.hpp:84-107):
+ *   Matérn, EQ : (var, len)
+ *   QP         : (var, len, period, env)   len = periodic smoothness ℓ_p,
+ *                                          env = envelope lengthscale ℓ_e      */
+typedef struct {
+    int32_t type;
+    int32_t order;
+} spingp_leaf;
+
+/* flags for the evaluation entry points */
+#define SPINGP_WANT_LOGLIK 0u      /* always computed                                   */
+#define SPINGP_WANT_GRAD 1u        /* d loglik / d(theta..., sigma), raw parameters     */
+#define SPINGP_WANT_MEAN 2u        /* posterior mean H mu_i at the training times       */
+#define SPINGP_WANT_VAR 4u         /* posterior latent variance H C_ii H^T              */
+#define SPINGP_INCLUDE_NOISE 8u    /* add sigma^2 to the variances                      */
+
+typedef struct spingp_ctx spingp_ctx;
+
+int spingp_abi_version(void);
+const char* spingp_status_string(int status);
+
+/* ---- host-side model setup (no GPU needed) ------------------------------------ */
+
+/* b (state dimension) and n_theta (kernel hyperparameters, excluding sigma). */
+int spingp_kernel_dims(const spingp_leaf* leaves, int32_t n_leaves, int32_t* b, int32_t* n_theta);
+
+/* state_space_of (kernels.hpp:326-381): F[b*b], H[b], Pinf[b*b], dF[n_theta*b*b],
+ * dPinf[n_theta*b*b], f_constant[n_theta]; any output may be NULL. */
+int spingp_state_space(const spingp_leaf* leaves, int32_t n_leaves, const double* theta,
+                       int32_t n_theta, double* F, double* H, double* Pinf, double* dF,
+                       double* dPinf, int32_t* f_constant);
+
+/* ---- context ------------------------------------------------------------------- */
+
+int spingp_ctx_create(int32_t device, spingp_ctx** out);
+int spingp_ctx_destroy(spingp_ctx* ctx);
+/* Use an external CUDA stream (cudaStream_t passed as void*); NULL = own stream. */
+int spingp_ctx_set_stream(spingp_ctx* ctx, void* stream);
+void* spingp_ctx_get_stream(spingp_ctx* ctx);
+/* Synchronise the context's stream and return the first device-side failure of
+ * the work enqueued since the previous call (and its block index). */
+int spingp_ctx_status(spingp_ctx* ctx, int64_t* fail_block);
+/* Number of kernel launches this context has issued so far. */
+int64_t spingp_ctx_launch_count(spingp_ctx* ctx);
+
+/* ---- the hot path: discretise -> assemble -> partitioned BTD factor/solve/selinv
+ *      -> loglik, gradient, posterior mean/var, fused on the device ------------- */
+
+int spingp_eval(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
+                const double* theta, int32_t n_theta, const double* t, const double* y,
+                int64_t n, double sigma, uint32_t flags, double* out_loglik,
+                double* out_grad /* n_theta+1 */, double* out_mean /* n */,
+                double* out_var /* n */, int64_t* fail_block);
+
+int spingp_eval_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
+                       const double* theta, int32_t n_theta, const double* d_t,
+                       const double* d_y, int64_t n, double sigma, uint32_t flags,
+                       double* d_loglik /* 1 */, double* d_grad, double* d_mean, double* d_var);
+
+/* S independent series of n points each, series-major t[S][n], y[S][n];
+ * per-series hyperparameters theta[S][n_theta] and noise sigma[S];
+ * outputs loglik[S], grad[S][n_theta+1], mean[S][n], var[S][n]. */
+int spingp_eval_batched(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
+                        const double* theta, int32_t n_theta, int64_t S, int64_t n,
+                        const double* t, const double* y, const double* sigma, uint32_t flags,
+                        double* out_loglik, double* out_grad, double* out_mean, double* out_var,
+                        int64_t* fail_block);
+
+int spingp_eval_batched_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
+                               const double* d_theta, int32_t n_theta, int64_t S, int64_t n,
+                               const double* d_t, const double* d_y, const double* d_sigma,
+                               uint32_t flags, double* d_loglik, double* d_grad, double* d_mean,
+                               double* d_var);
+
+/* assemble_prior_precision + add_observation_term with the jitter
+ * of SPEC.md:328 and Q_0 := Pinf: diag[n*b*b], upper[(n-1)*b*b], rhs[n*b]
+ * (rhs_i = H^T y_i / sigma^2). */
+int spingp_assemble(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
+                    const double* theta, int32_t n_theta, const double* t, const double* y,
+                    int64_t n, double sigma, double* diag, double* upper, double* rhs,
+                    int64_t* fail_block);
+
+/* ---- btd_core on a materialised symmetric BTD --------------- */
+
+/* cr_solve: x = M^{-1} rhs for k right-hand sides, plus log det M. */
+int spingp_btd_cr_solve(spingp_ctx* ctx, int64_t n, int32_t b, const double* diag,
+                        const double* upper, const double* rhs, int32_t k, double* x,
+                        double* logdet, int64_t* fail_block);
+int spingp_btd_cr_solve_device(spingp_ctx* ctx, int64_t n, int32_t b, const double* d_diag,
+                               const double* d_upper, const double* d_rhs, int32_t k,
+                               double* d_x, double* d_logdet);
+
+/* selective_inverse: the BTD-pattern blocks of M^{-1}: cdiag[n*b*b], cupper[(n-1)*b*b]. */
+int spingp_btd_selinv(spingp_ctx* ctx, int64_t n, int32_t b, const double* diag,
+                      const double* upper, double* cdiag, double* cupper, double* logdet,
+                      int64_t* fail_block);
+int spingp_btd_selinv_device(spingp_ctx* ctx, int64_t n, int32_t b, const double* d_diag,
+                             const double* d_upper, double* d_cdiag, double* d_cupper,
+                             double* d_logdet);
+
+/* matvec: y = M v (one vector). */
+int spingp_btd_matvec(spingp_ctx* ctx, int64_t n, int32_t b, const double* diag,
+                      const double* upper, const double* v, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPINGP_C_H */
