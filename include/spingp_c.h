@@ -89,6 +89,8 @@ typedef struct spingp_ctx spingp_ctx;
 
 int spingp_abi_version(void);
 const char* spingp_status_string(int status);
+/* Message of the last failure on the calling thread. */
+const char* spingp_last_error(void);
 
 /* ---- host-side model setup (no GPU needed) ------------------------------------ */
 
@@ -113,6 +115,8 @@ void* spingp_ctx_get_stream(spingp_ctx* ctx);
 int spingp_ctx_status(spingp_ctx* ctx, int64_t* fail_block);
 /* Number of kernel launches this context has issued so far. */
 int64_t spingp_ctx_launch_count(spingp_ctx* ctx);
+/* Tuning/testing knob: force the level-0 chunk length (0 = automatic). */
+int spingp_ctx_set_chunk(spingp_ctx* ctx, int64_t m0);
 
 /* ---- the hot path: discretise -> assemble -> partitioned BTD factor/solve/selinv
  *      -> loglik, gradient, posterior mean/var, fused on the device ------------- */
@@ -137,9 +141,12 @@ int spingp_eval_batched(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_le
                         double* out_loglik, double* out_grad, double* out_mean, double* out_var,
                         int64_t* fail_block);
 
+/* Device variant: t, y and every output are device pointers; the per-series
+ * hyperparameters theta[S][n_theta] and sigma[S] stay HOST arrays (control data,
+ * turned into per-series device records by the library). */
 int spingp_eval_batched_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
-                               const double* d_theta, int32_t n_theta, int64_t S, int64_t n,
-                               const double* d_t, const double* d_y, const double* d_sigma,
+                               const double* theta, int32_t n_theta, int64_t S, int64_t n,
+                               const double* d_t, const double* d_y, const double* sigma,
                                uint32_t flags, double* d_loglik, double* d_grad, double* d_mean,
                                double* d_var);
 

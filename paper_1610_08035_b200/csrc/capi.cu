@@ -1,0 +1,437 @@
+// capi.cu — the C ABI of include/spingp_c.h: context lifetime, planning,
+// host<->device staging and dispatch to the kernel instantiations
+// (inst_*.cu, btd_*.cu).  Every per-point computation runs in the sm_100a
+// kernels of engine.cuh; there is no CPU fallback — without a CUDA device the
+// computing entry points return SPINGP_CUDA_ERR.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "ctx.hpp"
+
+using namespace spingp_dev;
+using namespace spingp_host;
+
+namespace spingp_host {
+
+std::string& last_error() {
+    thread_local std::string s;
+    return s;
+}
+
+
+int take_status(spingp_ctx* ctx, int64_t* fail_block) {
+    unsigned long long h = 0;
+    CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    CUDA_OK(cudaMemcpy(&h, ctx->d_status, sizeof h, cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemset(ctx->d_status, 0xFF, sizeof(unsigned long long)));
+    if (h == ~0ULL) return SPINGP_OK;
+    if (fail_block) *fail_block = static_cast<int64_t>(h >> 4);
+    const int code = static_cast<int>(h & 15ULL);
+    static const char* what[] = {"", "pivot block is not positive definite",
+                                 "process noise block singular after jitter", "invalid input value",
+                                 "", "", "duplicate training timestamp", "", "negative posterior variance"};
+    last_error() = what[code < 9 ? code : 0];
+    return code;
+}
+
+void upload(spingp_ctx* ctx, double* dst, const double* src, size_t count) {
+    double* st = ctx->stage(count);
+    std::memcpy(st, src, count * sizeof(double));
+    CUDA_OK(cudaMemcpyAsync(dst, st, count * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    ctx->stage_done();
+}
+
+}  // namespace spingp_host
+
+namespace {
+
+// device scratch for the host-pointer entry points
+struct DeviceVec {
+    double* p = nullptr;
+    size_t n = 0;
+    double* get(size_t count) {
+        if (count > n) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            n = 0;
+            CUDA_OK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double)));
+            n = count;
+        }
+        return p;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+void dispatch_eval(spingp_ctx* ctx, const EvalArgs& a) {
+    const HostModel& hm = *a.hm;
+    if (hm.single_matern) {
+        switch (hm.b) {
+            case 1: return eval_matern_1(ctx, a);
+            case 2: return eval_matern_2(ctx, a);
+            case 3: return eval_matern_3(ctx, a);
+        }
+    }
+    switch (pad_b(hm.b)) {
+        case 1: case 2: case 3: return eval_generic_3(ctx, a);
+        case 4: return eval_generic_4(ctx, a);
+        case 6: return eval_generic_6(ctx, a);
+        case 8: return eval_generic_8(ctx, a);
+        case 12: return eval_generic_12(ctx, a);
+        case 16: return eval_generic_16(ctx, a);
+    }
+    throw ApiError{SPINGP_UNSUPPORTED, -1, "no kernel instantiation for this state dimension"};
+}
+
+int plan_bsize(const HostModel& hm) { return hm.single_matern ? hm.b : std::max(3, pad_b(hm.b)); }
+
+void btd_dispatch(spingp_ctx* ctx, int64_t n, int b, const double* diag, const double* upper,
+                  const double* rhs, int k, int col, double* x, double* cdiag, double* cupper,
+                  double* logdet, bool needC) {
+    if (n < 1 || b < 1) throw std::invalid_argument("empty block-tridiagonal matrix");
+#define R(B) btd_run_##B(ctx, n, b, diag, upper, rhs, k, col, x, cdiag, cupper, logdet, needC)
+    switch (pad_b(b)) {
+        case 1: R(1); break;
+        case 2: R(2); break;
+        case 3: R(3); break;
+        case 4: R(4); break;
+        case 6: R(6); break;
+        case 8: R(8); break;
+        case 12: R(12); break;
+        case 16: R(16); break;
+    }
+#undef R
+}
+
+spingp_ctx* checked(spingp_ctx* ctx) {
+    if (!ctx) throw std::invalid_argument("null context");
+    CUDA_OK(cudaSetDevice(ctx->device));
+    return ctx;
+}
+
+}  // namespace
+
+extern "C" {
+
+int spingp_abi_version(void) { return SPINGP_ABI_VERSION; }
+
+const char* spingp_status_string(int status) {
+    switch (status) {
+        case SPINGP_OK: return "ok";
+        case SPINGP_NOT_PD: return "not positive definite";
+        case SPINGP_SINGULAR_Q: return "singular process noise";
+        case SPINGP_BAD_ARG: return "bad argument";
+        case SPINGP_CUDA_ERR: return "cuda error";
+        case SPINGP_NCCL_ERR: return "nccl error";
+        case SPINGP_DUPLICATE_TIME: return "duplicate timestamp";
+        case SPINGP_UNSUPPORTED: return "unsupported";
+        case SPINGP_NEG_VARIANCE: return "negative variance";
+    }
+    return "unknown status";
+}
+
+const char* spingp_last_error(void) { return last_error().c_str(); }
+
+int spingp_ctx_create(int32_t device, spingp_ctx** out) {
+    return guarded(nullptr, [&] {
+        if (!out) throw std::invalid_argument("null output");
+        *out = nullptr;
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+            throw ApiError{SPINGP_CUDA_ERR, -1, "no CUDA device available (this build has no CPU fallback)"};
+        if (device < 0 || device >= count) throw std::invalid_argument("device index out of range");
+        CUDA_OK(cudaSetDevice(device));
+        auto* c = new spingp_ctx();
+        c->device = device;
+        CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+        CUDA_OK(cudaMalloc(&c->d_status, sizeof(unsigned long long)));
+        CUDA_OK(cudaMemset(c->d_status, 0xFF, sizeof(unsigned long long)));
+        CUDA_OK(cudaEventCreateWithFlags(&c->stage_ev[0], cudaEventDisableTiming));
+        CUDA_OK(cudaEventCreateWithFlags(&c->stage_ev[1], cudaEventDisableTiming));
+        *out = c;
+        return SPINGP_OK;
+    });
+}
+
+int spingp_ctx_destroy(spingp_ctx* ctx) {
+    if (!ctx) return SPINGP_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->ws.base) cudaFree(ctx->ws.base);
+    if (ctx->d_status) cudaFree(ctx->d_status);
+    for (int k = 0; k < 2; ++k) {
+        if (ctx->h_stage[k]) cudaFreeHost(ctx->h_stage[k]);
+        if (ctx->stage_ev[k]) cudaEventDestroy(ctx->stage_ev[k]);
+    }
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return SPINGP_OK;
+}
+
+int spingp_ctx_set_stream(spingp_ctx* ctx, void* stream) {
+    return guarded(nullptr, [&] {
+        checked(ctx);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CUDA_OK(cudaStreamSynchronize(ctx->stream));
+        if (ctx->own_stream) CUDA_OK(cudaStreamDestroy(ctx->stream));
+        if (stream) {
+            ctx->stream = static_cast<cudaStream_t>(stream);
+            ctx->own_stream = false;
+        } else {
+            CUDA_OK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+            ctx->own_stream = true;
+        }
+        return SPINGP_OK;
+    });
+}
+
+void* spingp_ctx_get_stream(spingp_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int spingp_ctx_set_chunk(spingp_ctx* ctx, int64_t m0) {
+    if (!ctx || m0 < 0) return SPINGP_BAD_ARG;
+    ctx->m0_override = m0;
+    return SPINGP_OK;
+}
+
+int spingp_ctx_status(spingp_ctx* ctx, int64_t* fail_block) {
+    return guarded(fail_block, [&] {
+        checked(ctx);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        return take_status(ctx, fail_block);
+    });
+}
+
+int64_t spingp_ctx_launch_count(spingp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int spingp_eval_batched_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
+                               const double* theta, int32_t n_theta, int64_t S, int64_t n,
+                               const double* d_t, const double* d_y, const double* sigma,
+                               uint32_t flags, double* d_loglik, double* d_grad, double* d_mean,
+                               double* d_var) {
+    return guarded(nullptr, [&] {
+        checked(ctx);
+        if (!theta || !sigma || !d_t || !d_y || !d_loglik) throw std::invalid_argument("null argument");
+        if ((flags & SPINGP_WANT_GRAD) && !d_grad) throw std::invalid_argument("gradient output is null");
+        if ((flags & SPINGP_WANT_MEAN) && !d_mean) throw std::invalid_argument("mean output is null");
+        if ((flags & SPINGP_WANT_VAR) && !d_var) throw std::invalid_argument("variance output is null");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        const HostModel hm = build_model(leaves, n_leaves, n_theta);
+        const Plan plan = make_plan(n, S, plan_bsize(hm), ctx->m0_override);
+        std::vector<double> params(static_cast<size_t>(S) * hm.rec_stride, 0.0);
+        for (int64_t s = 0; s < S; ++s)
+            fill_record(hm, theta + s * n_theta, sigma[s], params.data() + s * hm.rec_stride);
+        EvalArgs a{&hm, &plan, params.data(), params.size(), d_t, d_y, flags, d_loglik, d_grad, d_mean, d_var,
+                   0, nullptr, nullptr, nullptr};
+        dispatch_eval(ctx, a);
+        return SPINGP_OK;
+    });
+}
+
+int spingp_eval_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
+                       const double* theta, int32_t n_theta, const double* d_t, const double* d_y,
+                       int64_t n, double sigma, uint32_t flags, double* d_loglik, double* d_grad,
+                       double* d_mean, double* d_var) {
+    return spingp_eval_batched_device(ctx, leaves, n_leaves, theta, n_theta, 1, n, d_t, d_y, &sigma,
+                                      flags, d_loglik, d_grad, d_mean, d_var);
+}
+
+int spingp_eval_batched(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
+                        const double* theta, int32_t n_theta, int64_t S, int64_t n, const double* t,
+                        const double* y, const double* sigma, uint32_t flags, double* out_loglik,
+                        double* out_grad, double* out_mean, double* out_var, int64_t* fail_block) {
+    return guarded(fail_block, [&] {
+        checked(ctx);
+        if (!t || !y || !out_loglik || S < 1 || n < 1) throw std::invalid_argument("bad argument");
+        if ((flags & SPINGP_WANT_GRAD) && !out_grad) throw std::invalid_argument("gradient output is null");
+        if ((flags & SPINGP_WANT_MEAN) && !out_mean) throw std::invalid_argument("mean output is null");
+        if ((flags & SPINGP_WANT_VAR) && !out_var) throw std::invalid_argument("variance output is null");
+        static thread_local DeviceVec dbuf;
+        const size_t N = static_cast<size_t>(S) * n;
+        const size_t nt1 = static_cast<size_t>(n_theta) + 1;
+        const size_t ng = (flags & SPINGP_WANT_GRAD) ? S * nt1 : 0;
+        const size_t nm = (flags & SPINGP_WANT_MEAN) ? N : 0;
+        const size_t nv = (flags & SPINGP_WANT_VAR) ? N : 0;
+        double* base = dbuf.get(2 * N + S + ng + nm + nv);
+        double* d_t = base;
+        double* d_y = d_t + N;
+        double* d_ll = d_y + N;
+        double* d_g = d_ll + S;
+        double* d_m = d_g + ng;
+        double* d_v = d_m + nm;
+        {
+            std::lock_guard<std::mutex> lk(ctx->mu);
+            CUDA_OK(cudaMemcpyAsync(d_t, t, N * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+            CUDA_OK(cudaMemcpyAsync(d_y, y, N * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        }
+        const int st = spingp_eval_batched_device(ctx, leaves, n_leaves, theta, n_theta, S, n, d_t, d_y, sigma,
+                                                  flags, d_ll, d_g, d_m, d_v);
+        if (st != SPINGP_OK) return st;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CUDA_OK(cudaMemcpyAsync(out_loglik, d_ll, S * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        if (ng) CUDA_OK(cudaMemcpyAsync(out_grad, d_g, ng * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        if (nm) CUDA_OK(cudaMemcpyAsync(out_mean, d_m, nm * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        if (nv) CUDA_OK(cudaMemcpyAsync(out_var, d_v, nv * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        return take_status(ctx, fail_block);
+    });
+}
+
+int spingp_eval(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves, const double* theta,
+                int32_t n_theta, const double* t, const double* y, int64_t n, double sigma,
+                uint32_t flags, double* out_loglik, double* out_grad, double* out_mean,
+                double* out_var, int64_t* fail_block) {
+    return spingp_eval_batched(ctx, leaves, n_leaves, theta, n_theta, 1, n, t, y, &sigma, flags, out_loglik,
+                               out_grad, out_mean, out_var, fail_block);
+}
+
+int spingp_assemble(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
+                    const double* theta, int32_t n_theta, const double* t, const double* y,
+                    int64_t n, double sigma, double* diag, double* upper, double* rhs,
+                    int64_t* fail_block) {
+    return guarded(fail_block, [&] {
+        checked(ctx);
+        if (!t || !y || !diag || n < 1) throw std::invalid_argument("bad argument");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        const HostModel hm = build_model(leaves, n_leaves, n_theta);
+        const int b = hm.b;
+        static thread_local DeviceVec dbuf;
+        const size_t nd = static_cast<size_t>(n) * b * b, nu = static_cast<size_t>(n > 1 ? n - 1 : 0) * b * b;
+        double* d_t = dbuf.get(2 * n + nd + nu + n * b);
+        double* d_y = d_t + n;
+        double* d_d = d_y + n;
+        double* d_u = d_d + nd;
+        double* d_r = d_u + nu;
+        CUDA_OK(cudaMemcpyAsync(d_t, t, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_OK(cudaMemcpyAsync(d_y, y, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        const Plan plan = make_plan(n, 1, plan_bsize(hm), 0);
+        std::vector<double> params(hm.rec_stride, 0.0);
+        fill_record(hm, theta, sigma, params.data());
+        EvalArgs a{&hm, &plan, params.data(), params.size(), d_t, d_y, 0, nullptr, nullptr, nullptr, nullptr,
+                   1, d_d, d_u, d_r};
+        dispatch_eval(ctx, a);
+        CUDA_OK(cudaMemcpyAsync(diag, d_d, nd * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        if (upper && nu) CUDA_OK(cudaMemcpyAsync(upper, d_u, nu * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        if (rhs) CUDA_OK(cudaMemcpyAsync(rhs, d_r, n * b * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        return take_status(ctx, fail_block);
+    });
+}
+
+int spingp_btd_cr_solve_device(spingp_ctx* ctx, int64_t n, int32_t b, const double* d_diag,
+                               const double* d_upper, const double* d_rhs, int32_t k, double* d_x,
+                               double* d_logdet) {
+    return guarded(nullptr, [&] {
+        checked(ctx);
+        if (!d_diag || (n > 1 && !d_upper) || k < 0 || (k > 0 && (!d_rhs || !d_x)))
+            throw std::invalid_argument("bad argument");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if (k == 0) {
+            btd_dispatch(ctx, n, b, d_diag, d_upper, nullptr, 1, 0, nullptr, nullptr, nullptr, d_logdet, false);
+            return SPINGP_OK;
+        }
+        for (int col = 0; col < k; ++col)
+            btd_dispatch(ctx, n, b, d_diag, d_upper, d_rhs, k, col, d_x, nullptr, nullptr,
+                         col == 0 ? d_logdet : nullptr, false);
+        return SPINGP_OK;
+    });
+}
+
+int spingp_btd_cr_solve(spingp_ctx* ctx, int64_t n, int32_t b, const double* diag,
+                        const double* upper, const double* rhs, int32_t k, double* x,
+                        double* logdet, int64_t* fail_block) {
+    return guarded(fail_block, [&] {
+        checked(ctx);
+        if (!diag || n < 1 || b < 1 || k < 0) throw std::invalid_argument("bad argument");
+        static thread_local DeviceVec dbuf;
+        const size_t nd = static_cast<size_t>(n) * b * b, nu = static_cast<size_t>(n - 1) * b * b;
+        const size_t nr = static_cast<size_t>(n) * b * k;
+        double* d_d = dbuf.get(nd + nu + 2 * nr + 1);
+        double* d_u = d_d + nd;
+        double* d_r = d_u + nu;
+        double* d_x = d_r + nr;
+        double* d_ld = d_x + nr;
+        {
+            std::lock_guard<std::mutex> lk(ctx->mu);
+            CUDA_OK(cudaMemcpyAsync(d_d, diag, nd * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+            if (nu) CUDA_OK(cudaMemcpyAsync(d_u, upper, nu * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+            if (nr) CUDA_OK(cudaMemcpyAsync(d_r, rhs, nr * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        }
+        const int st = spingp_btd_cr_solve_device(ctx, n, b, d_d, d_u, nr ? d_r : nullptr, k, nr ? d_x : nullptr, d_ld);
+        if (st != SPINGP_OK) return st;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if (nr && x) CUDA_OK(cudaMemcpyAsync(x, d_x, nr * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        if (logdet) CUDA_OK(cudaMemcpyAsync(logdet, d_ld, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        return take_status(ctx, fail_block);
+    });
+}
+
+int spingp_btd_selinv_device(spingp_ctx* ctx, int64_t n, int32_t b, const double* d_diag,
+                             const double* d_upper, double* d_cdiag, double* d_cupper,
+                             double* d_logdet) {
+    return guarded(nullptr, [&] {
+        checked(ctx);
+        if (!d_diag || !d_cdiag || (n > 1 && (!d_upper || !d_cupper))) throw std::invalid_argument("bad argument");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        btd_dispatch(ctx, n, b, d_diag, d_upper, nullptr, 1, 0, nullptr, d_cdiag, d_cupper, d_logdet, true);
+        return SPINGP_OK;
+    });
+}
+
+int spingp_btd_selinv(spingp_ctx* ctx, int64_t n, int32_t b, const double* diag,
+                      const double* upper, double* cdiag, double* cupper, double* logdet,
+                      int64_t* fail_block) {
+    return guarded(fail_block, [&] {
+        checked(ctx);
+        if (!diag || !cdiag || n < 1 || b < 1) throw std::invalid_argument("bad argument");
+        static thread_local DeviceVec dbuf;
+        const size_t nd = static_cast<size_t>(n) * b * b, nu = static_cast<size_t>(n - 1) * b * b;
+        double* d_d = dbuf.get(2 * nd + 2 * nu + 1);
+        double* d_u = d_d + nd;
+        double* d_cd = d_u + nu;
+        double* d_cu = d_cd + nd;
+        double* d_ld = d_cu + nu;
+        {
+            std::lock_guard<std::mutex> lk(ctx->mu);
+            CUDA_OK(cudaMemcpyAsync(d_d, diag, nd * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+            if (nu) CUDA_OK(cudaMemcpyAsync(d_u, upper, nu * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        }
+        const int st = spingp_btd_selinv_device(ctx, n, b, d_d, d_u, d_cd, d_cu, d_ld);
+        if (st != SPINGP_OK) return st;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CUDA_OK(cudaMemcpyAsync(cdiag, d_cd, nd * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        if (nu && cupper) CUDA_OK(cudaMemcpyAsync(cupper, d_cu, nu * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        if (logdet) CUDA_OK(cudaMemcpyAsync(logdet, d_ld, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        return take_status(ctx, fail_block);
+    });
+}
+
+int spingp_btd_matvec(spingp_ctx* ctx, int64_t n, int32_t b, const double* diag,
+                      const double* upper, const double* v, double* out) {
+    return guarded(nullptr, [&] {
+        checked(ctx);
+        if (!diag || !v || !out || n < 1 || b < 1) throw std::invalid_argument("bad argument");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        static thread_local DeviceVec dbuf;
+        const size_t nd = static_cast<size_t>(n) * b * b, nu = static_cast<size_t>(n - 1) * b * b;
+        const size_t nv = static_cast<size_t>(n) * b;
+        double* d_d = dbuf.get(nd + nu + 2 * nv);
+        double* d_u = d_d + nd;
+        double* d_v = d_u + nu;
+        double* d_o = d_v + nv;
+        CUDA_OK(cudaMemcpyAsync(d_d, diag, nd * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        if (nu) CUDA_OK(cudaMemcpyAsync(d_u, upper, nu * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_OK(cudaMemcpyAsync(d_v, v, nv * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        k_matvec<<<blocks_for(n, 128), 128, 0, ctx->stream>>>(n, b, d_d, d_u, d_v, d_o);
+        ctx->launched();
+        CUDA_OK(cudaMemcpyAsync(out, d_o, nv * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_OK(cudaStreamSynchronize(ctx->stream));
+        return SPINGP_OK;
+    });
+}
+
+}  // extern "C"

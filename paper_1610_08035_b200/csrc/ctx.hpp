@@ -1,0 +1,168 @@
+// ctx.hpp — the context behind the C ABI (device, stream, workspace, status word)
+// and the host-side reduction plan.  Shared by the nvcc translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "engine.cuh"
+#include "host_model.hpp"
+#include "spingp_c.h"
+
+namespace spingp_host {
+
+#define CUDA_OK(expr)                                                                          \
+    do {                                                                                       \
+        cudaError_t e_ = (expr);                                                               \
+        if (e_ != cudaSuccess)                                                                 \
+            throw ::spingp_host::ApiError{SPINGP_CUDA_ERR, -1,                                 \
+                                          std::string(#expr) + ": " + cudaGetErrorString(e_)}; \
+    } while (0)
+
+std::string& last_error();
+
+template <class F>
+int guarded(int64_t* fail_block, F&& body) {
+    if (fail_block) *fail_block = -1;
+    try {
+        return body();
+    } catch (const ApiError& e) {
+        if (fail_block) *fail_block = e.block;
+        last_error() = e.what;
+        return e.status;
+    } catch (const std::invalid_argument& e) {
+        last_error() = e.what();
+        return SPINGP_BAD_ARG;
+    } catch (const std::exception& e) {
+        last_error() = e.what();
+        return SPINGP_UNSUPPORTED;
+    }
+}
+
+struct Arena {
+    char* base = nullptr;
+    size_t size = 0, used = 0;
+    void reset() { used = 0; }
+    template <class T>
+    T* take(size_t count) {
+        const size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
+        if (used + bytes > size) throw ApiError{SPINGP_CUDA_ERR, -1, "workspace overflow"};
+        T* p = reinterpret_cast<T*>(base + used);
+        used += bytes;
+        return p;
+    }
+};
+
+inline size_t arena_bytes(size_t count) { return (count * sizeof(double) + 255) & ~size_t(255); }
+
+inline unsigned blocks_for(long long n, int tpb) { return static_cast<unsigned>((n + tpb - 1) / tpb); }
+
+}  // namespace spingp_host
+
+struct spingp_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    spingp_host::Arena ws;
+    unsigned long long* d_status = nullptr;
+    double* h_stage[2] = {nullptr, nullptr};
+    size_t h_stage_cap[2] = {0, 0};
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+    int stage_slot = 0, cur_slot = 0;
+    int64_t launches = 0;
+    int64_t m0_override = 0;  // testing knob: force the level-0 chunk length
+    std::mutex mu;
+
+    void ensure_ws(size_t bytes) {
+        if (bytes <= ws.size) return;
+        if (ws.base) {
+            CUDA_OK(cudaStreamSynchronize(stream));
+            CUDA_OK(cudaFree(ws.base));
+            ws.base = nullptr;
+            ws.size = 0;
+        }
+        const size_t cap = std::max(bytes, ws.size + ws.size / 2);
+        CUDA_OK(cudaMalloc(&ws.base, cap));
+        ws.size = cap;
+    }
+    // pinned staging slot for small host->device parameter uploads (double-buffered;
+    // a slot is reused only after the copy that read it has executed)
+    double* stage(size_t count) {
+        const int k = stage_slot;
+        stage_slot ^= 1;
+        CUDA_OK(cudaEventSynchronize(stage_ev[k]));
+        if (count > h_stage_cap[k]) {
+            if (h_stage[k]) CUDA_OK(cudaFreeHost(h_stage[k]));
+            const size_t cap = std::max<size_t>(count, 4096);
+            CUDA_OK(cudaMallocHost(&h_stage[k], cap * sizeof(double)));
+            h_stage_cap[k] = cap;
+        }
+        cur_slot = k;
+        return h_stage[k];
+    }
+    void stage_done() { CUDA_OK(cudaEventRecord(stage_ev[cur_slot], stream)); }
+    void launched() {
+        launches++;
+        CUDA_OK(cudaGetLastError());
+    }
+};
+
+namespace spingp_host {
+
+// Synchronise and collect (then clear) the device status word.
+int take_status(spingp_ctx* ctx, int64_t* fail_block);
+
+// Upload `count` doubles from host memory through the context's pinned stage.
+void upload(spingp_ctx* ctx, double* dst, const double* src, size_t count);
+
+// One evaluation (S series) on device-resident t, y: entry points per kernel
+// instantiation family live in separate translation units.
+struct EvalArgs {
+    const HostModel* hm;
+    const Plan* plan;
+    const double* h_params;
+    size_t nparams;
+    const double* d_t;
+    const double* d_y;
+    uint32_t flags;
+    double* d_loglik;
+    double* d_grad;
+    double* d_mean;
+    double* d_var;
+    // mode 1: assemble only into d_diag / d_upper / d_rhs (S = 1)
+    int mode;
+    double* d_diag;
+    double* d_upper;
+    double* d_rhs;
+};
+// one translation unit per instantiation (inst_*.cu, btd_b*.cu) so they build in parallel
+void eval_matern_1(spingp_ctx* ctx, const EvalArgs& a);
+void eval_matern_2(spingp_ctx* ctx, const EvalArgs& a);
+void eval_matern_3(spingp_ctx* ctx, const EvalArgs& a);
+void eval_generic_3(spingp_ctx* ctx, const EvalArgs& a);
+void eval_generic_4(spingp_ctx* ctx, const EvalArgs& a);
+void eval_generic_6(spingp_ctx* ctx, const EvalArgs& a);
+void eval_generic_8(spingp_ctx* ctx, const EvalArgs& a);
+void eval_generic_12(spingp_ctx* ctx, const EvalArgs& a);
+void eval_generic_16(spingp_ctx* ctx, const EvalArgs& a);
+#define SPINGP_BTD_DECL(B)                                                                          \
+    void btd_run_##B(spingp_ctx* ctx, int64_t n, int b, const double* diag, const double* upper, \
+                     const double* rhs, int k, int col, double* x, double* cdiag, double* cupper, \
+                     double* logdet, bool needC);
+SPINGP_BTD_DECL(1)
+SPINGP_BTD_DECL(2)
+SPINGP_BTD_DECL(3)
+SPINGP_BTD_DECL(4)
+SPINGP_BTD_DECL(6)
+SPINGP_BTD_DECL(8)
+SPINGP_BTD_DECL(12)
+SPINGP_BTD_DECL(16)
+#undef SPINGP_BTD_DECL
+
+}  // namespace spingp_host

@@ -1,0 +1,238 @@
+// devmat.cuh — fixed-size dense fp64 block algebra for one thread (b x b blocks,
+// row-major arrays).  For b <= 3 everything lives in registers; the templates
+// are fully unrolled so the compiler can schedule the independent DFMAs.
+//
+// These are the per-block operations of the SPEC's btd_core:
+// Cholesky pivots (factorize :146), triangular solves, explicit SPD inverses
+// (selective_inverse :170-178) and the Schur-complement updates.
+#pragma once
+
+#ifndef SPINGP_HOST_EMU
+#include <cuda_runtime.h>
+#endif
+
+namespace spingp_dev {
+
+#define SP_DEV __device__ __forceinline__
+// Loop-unrolling hint for the b x b loops.  Deliberately empty: nvcc fully
+// unrolls the constant-trip loops of the register-resident sizes (b <= 4) on
+// its own, and an explicit `#pragma unroll (B <= 4 ? 64 : 1)` was measured to
+// MISCOMPILE the triangular loops (inner trip count depending on the outer
+// index) with nvcc 12.9 for sm_100a — wrong covariance blocks on the device
+// while the same source was correct on the host (tools/dbg/dbg_pipe.cu).
+#ifndef SP_UNROLL
+#define SP_UNROLL
+#endif
+
+template <int B>
+SP_DEV void mzero(double* a) {
+SP_UNROLL
+    for (int i = 0; i < B * B; ++i) a[i] = 0.0;
+}
+template <int B>
+SP_DEV void mcopy(double* d, const double* s) {
+SP_UNROLL
+    for (int i = 0; i < B * B; ++i) d[i] = s[i];
+}
+template <int B>
+SP_DEV void vzero(double* a) {
+SP_UNROLL
+    for (int i = 0; i < B; ++i) a[i] = 0.0;
+}
+
+// C = A * B
+template <int B>
+SP_DEV void mm(double* C, const double* A, const double* Bm) {
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j < B; ++j) {
+            double s = 0.0;
+SP_UNROLL
+            for (int k = 0; k < B; ++k) s = fma(A[i * B + k], Bm[k * B + j], s);
+            C[i * B + j] = s;
+        }
+}
+// C = A^T * B
+template <int B>
+SP_DEV void mtm(double* C, const double* A, const double* Bm) {
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j < B; ++j) {
+            double s = 0.0;
+SP_UNROLL
+            for (int k = 0; k < B; ++k) s = fma(A[k * B + i], Bm[k * B + j], s);
+            C[i * B + j] = s;
+        }
+}
+// C = A * B^T
+template <int B>
+SP_DEV void mmt(double* C, const double* A, const double* Bm) {
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j < B; ++j) {
+            double s = 0.0;
+SP_UNROLL
+            for (int k = 0; k < B; ++k) s = fma(A[i * B + k], Bm[j * B + k], s);
+            C[i * B + j] = s;
+        }
+}
+// C = A^T * B, known to be symmetric: compute the lower triangle and mirror.
+template <int B>
+SP_DEV void mtm_sym(double* C, const double* A, const double* Bm) {
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j <= i; ++j) {
+            double s = 0.0;
+SP_UNROLL
+            for (int k = 0; k < B; ++k) s = fma(A[k * B + i], Bm[k * B + j], s);
+            C[i * B + j] = s;
+            C[j * B + i] = s;
+        }
+}
+// y = A x
+template <int B>
+SP_DEV void mv(double* y, const double* A, const double* x) {
+SP_UNROLL
+    for (int i = 0; i < B; ++i) {
+        double s = 0.0;
+SP_UNROLL
+        for (int k = 0; k < B; ++k) s = fma(A[i * B + k], x[k], s);
+        y[i] = s;
+    }
+}
+// y = A^T x
+template <int B>
+SP_DEV void mtv(double* y, const double* A, const double* x) {
+SP_UNROLL
+    for (int i = 0; i < B; ++i) {
+        double s = 0.0;
+SP_UNROLL
+        for (int k = 0; k < B; ++k) s = fma(A[k * B + i], x[k], s);
+        y[i] = s;
+    }
+}
+template <int B>
+SP_DEV void msym(double* a) {
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j < i; ++j) {
+            const double v = 0.5 * (a[i * B + j] + a[j * B + i]);
+            a[i * B + j] = v;
+            a[j * B + i] = v;
+        }
+}
+template <int B>
+SP_DEV double mtrace(const double* a) {
+    double s = 0.0;
+SP_UNROLL
+    for (int i = 0; i < B; ++i) s += a[i * B + i];
+    return s;
+}
+// Tr(A B)
+template <int B>
+SP_DEV double mtrprod(const double* A, const double* Bm) {
+    double s = 0.0;
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int k = 0; k < B; ++k) s = fma(A[i * B + k], Bm[k * B + i], s);
+    return s;
+}
+
+// Cholesky A = L L^T (L lower, stored full with zero upper); returns false on a
+// non-positive / non-finite pivot.  logdet accumulates 2 sum ln L_kk.
+template <int B>
+SP_DEV bool chol(double* L, const double* A, double& logdet) {
+    bool ok = true;
+    double ld = 0.0;
+SP_UNROLL
+    for (int j = 0; j < B; ++j) {
+        double d = A[j * B + j];
+SP_UNROLL
+        for (int k = 0; k < j; ++k) d = fma(-L[j * B + k], L[j * B + k], d);
+        ok = ok && (d > 0.0) && isfinite(d);
+        const double ljj = sqrt(d);
+        const double inv = 1.0 / ljj;
+        L[j * B + j] = ljj;
+        ld += log(ljj);
+SP_UNROLL
+        for (int i = j + 1; i < B; ++i) {
+            double s = A[i * B + j];
+SP_UNROLL
+            for (int k = 0; k < j; ++k) s = fma(-L[i * B + k], L[j * B + k], s);
+            L[i * B + j] = s * inv;
+        }
+SP_UNROLL
+        for (int i = 0; i < j; ++i) L[i * B + j] = 0.0;
+    }
+    logdet = 2.0 * ld;
+    return ok;
+}
+// same without the logarithms
+template <int B>
+SP_DEV bool chol_nolog(double* L, const double* A) {
+    bool ok = true;
+SP_UNROLL
+    for (int j = 0; j < B; ++j) {
+        double d = A[j * B + j];
+SP_UNROLL
+        for (int k = 0; k < j; ++k) d = fma(-L[j * B + k], L[j * B + k], d);
+        ok = ok && (d > 0.0) && isfinite(d);
+        const double ljj = sqrt(d);
+        const double inv = 1.0 / ljj;
+        L[j * B + j] = ljj;
+SP_UNROLL
+        for (int i = j + 1; i < B; ++i) {
+            double s = A[i * B + j];
+SP_UNROLL
+            for (int k = 0; k < j; ++k) s = fma(-L[i * B + k], L[j * B + k], s);
+            L[i * B + j] = s * inv;
+        }
+SP_UNROLL
+        for (int i = 0; i < j; ++i) L[i * B + j] = 0.0;
+    }
+    return ok;
+}
+template <int B>
+SP_DEV double chol_logdet(const double* L) {
+    double ld = 0.0;
+SP_UNROLL
+    for (int j = 0; j < B; ++j) ld += log(L[j * B + j]);
+    return 2.0 * ld;
+}
+
+// Ainv = (L L^T)^{-1} = L^{-T} L^{-1}, symmetric.
+template <int B>
+SP_DEV void chol_inverse(double* Ainv, const double* L) {
+    double Li[B * B];  // L^{-1}, lower
+SP_UNROLL
+    for (int j = 0; j < B; ++j) {
+        const double dj = 1.0 / L[j * B + j];
+SP_UNROLL
+        for (int i = 0; i < B; ++i) {
+            if (i < j) { Li[i * B + j] = 0.0; continue; }
+            if (i == j) { Li[i * B + j] = dj; continue; }
+            double s = 0.0;
+SP_UNROLL
+            for (int k = j; k < i; ++k) s = fma(L[i * B + k], (k == j ? dj : Li[k * B + j]), s);
+            Li[i * B + j] = -s / L[i * B + i];
+        }
+    }
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j <= i; ++j) {
+            double s = 0.0;
+SP_UNROLL
+            for (int k = i; k < B; ++k) s = fma(Li[k * B + i], Li[k * B + j], s);
+            Ainv[i * B + j] = s;
+            Ainv[j * B + i] = s;
+        }
+}
+
+}  // namespace spingp_dev

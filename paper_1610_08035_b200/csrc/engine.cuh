@@ -1,0 +1,974 @@
+// engine.cuh — partitioned block-tridiagonal elimination on the B200.
+//
+// What it replaces.  SPEC.md btd_core factorize/solve/logdet/selective_inverse/
+// cr_solve (:143-205) and spingp_engine assemble/add_observation_term/
+// log_marginal_likelihood/mll_gradient/predict (:262-306).  The reference design
+// is a sequential block Thomas recursion over all N blocks; here the N blocks are
+// cut into chunks and reduced hierarchically (the SPEC's "cyclic reduction"
+// contract, generalised from 2 to m blocks per chunk):
+//
+//   level 0   one thread per chunk of m0 consecutive time points.  It discretises
+//             every step in closed form, assembles D_i, U_i, rhs_i on the fly
+//             (never materialising the SymBTD), and eliminates the chunk's
+//             interior blocks in forward order against its two separators: the
+//             previous chunk's last block (L, carried as a "spike" W) and its own
+//             last block (R).  Output: a 2-separator Schur record per chunk.
+//   level l   the records form a BTD of one block per chunk; it is reduced the
+//             same way (one thread per chunk of m_l blocks) until one block is left.
+//   top       the single remaining block is inverted.
+//   reverse   levels are walked back down: every chunk back-substitutes its
+//             interior mean and runs the Takahashi recursion,
+//             seeded by its separators' mean, variance and cross-covariance.  At
+//             level 0 the same sweep recomputes each step's Φ, Q̃ and their
+//             θ-derivatives and accumulates the stationary-form log-likelihood
+//             terms, the per-step gradient and the per-point mean/variance.
+//
+// Elimination with a left spike (chunk interior j = s .. e-2, separators L, R):
+//   S_j = D_j - T_j,  G_j = S_j^{-1} U_j,  V_j = S_j^{-1} W_j,  h_j = S_j^{-1} r_j
+//   T_{j+1} = U_j^T G_j,  W_{j+1} = -U_j^T V_j,  r_{j+1} = rhs_{j+1} - U_j^T h_j
+//   acc_LL -= W_j^T V_j,  acc_rL -= W_j^T h_j,   logdet += log det S_j
+// Back substitution / selected inverse (x_j = h_j - V_j x_L - G_j x_{j+1} + ε_j,
+// Cov ε_j = S_j^{-1}):
+//   C_{jL} = -V_j C_LL - G_j C_{j+1,L}
+//   C_{j,j+1} = -V_j C_{L,j+1} - G_j C_{j+1,j+1}
+//   C_jj = S_j^{-1} - C_{jL} V_j^T - C_{j,j+1} G_j^T
+#pragma once
+
+#include <cstdint>
+
+#include "devmat.cuh"
+#include "model_dev.cuh"
+
+namespace spingp_dev {
+
+// status word: min over (index << 4 | code) of every failure seen on the device
+enum DevStatus {
+    ST_NOT_PD = 1, ST_SINGULAR_Q = 2, ST_BAD_ARG = 3, ST_DUPLICATE = 6, ST_NEG_VAR = 8
+};
+
+SP_DEV void report(unsigned long long* st, long long idx, int code) {
+    atomicMin(st, (static_cast<unsigned long long>(idx) << 4) | static_cast<unsigned long long>(code));
+}
+
+
+// level-l block k -> level-0 block index (the separator chain)
+SP_DEV long long to_global(const Geom& g, int lev, long long k) {
+    for (int l = lev; l > 0; --l) {
+        const long long e = min(g.n[l - 1], (k + 1) * static_cast<long long>(g.m[l - 1]));
+        k = e - 1;
+    }
+    return k;
+}
+
+// record layout, component-major: rec[comp * SK + chunk]
+template <int B>
+struct Rec {
+    static constexpr int RDIAG = 0;
+    static constexpr int LDIAG = B * B;
+    static constexpr int LR = 2 * B * B;
+    static constexpr int RRHS = 3 * B * B;
+    static constexpr int LRHS = 3 * B * B + B;
+    static constexpr int LOGDET = 3 * B * B + 2 * B;
+    static constexpr int N = 3 * B * B + 2 * B + 1;
+};
+// per-step factor layout: fac[(jj * NF + comp) * SK + chunk]
+template <int B>
+struct Fac {
+    static constexpr int SINV = 0;
+    static constexpr int V = B * B;
+    static constexpr int H = 2 * B * B;
+    static constexpr int N = 2 * B * B + B;
+};
+// solution layout at level >= 1: sol[comp * Sn + block]
+template <int B>
+struct Sol {
+    static constexpr int X = 0;
+    static constexpr int CD = B;
+    static constexpr int CU = B + B * B;
+    static constexpr int N = B + 2 * B * B;
+};
+// level-0 per-chunk partial sums: part[comp * SK + chunk]
+enum Part { P_LOGDET = 0, P_FITY = 1, P_FITE = 2, P_LDQ = 3, P_NOISE = 4, P_GRAD = 5 };
+
+template <int B>
+struct ElimState {
+    double T[B * B];
+    double rc[B];
+    double W[B * B];
+    double accLL[B * B];
+    double accrL[B];
+    double logdet;
+};
+
+template <int B>
+SP_DEV void elim_init(ElimState<B>& es) {
+    mzero<B>(es.T);
+    vzero<B>(es.rc);
+    mzero<B>(es.W);
+    mzero<B>(es.accLL);
+    vzero<B>(es.accrL);
+    es.logdet = 0.0;
+}
+
+// Eliminate one interior block; stores S^{-1}, V, h at fp[comp * SK].
+template <int B>
+SP_DEV bool elim_block(ElimState<B>& es, const double* D, const double* U, const double* rhs,
+                       bool hasL, double* fp, long long SK) {
+    double S[B * B];
+SP_UNROLL
+    for (int i = 0; i < B * B; ++i) S[i] = D[i] - es.T[i];
+    msym<B>(S);  // pivot symmetrisation
+    double L[B * B], ld;
+    if (!chol<B>(L, S, ld)) return false;
+    es.logdet += ld;
+    double Si[B * B];
+    chol_inverse<B>(Si, L);
+    double r[B], h[B];
+SP_UNROLL
+    for (int i = 0; i < B; ++i) r[i] = rhs[i] - es.rc[i];
+    mv<B>(h, Si, r);
+    double G[B * B];
+    mm<B>(G, Si, U);
+    if (hasL) {
+        double V[B * B], X[B * B];
+        mm<B>(V, Si, es.W);
+        mtm_sym<B>(X, es.W, V);
+SP_UNROLL
+        for (int i = 0; i < B * B; ++i) es.accLL[i] -= X[i];
+        double wh[B];
+        mtv<B>(wh, es.W, h);
+SP_UNROLL
+        for (int i = 0; i < B; ++i) es.accrL[i] -= wh[i];
+        mtm<B>(X, U, V);
+SP_UNROLL
+        for (int i = 0; i < B * B; ++i) es.W[i] = -X[i];
+SP_UNROLL
+        for (int i = 0; i < B * B; ++i) fp[(Fac<B>::V + i) * SK] = V[i];
+    }
+    mtm_sym<B>(es.T, U, G);
+    mtv<B>(es.rc, U, h);
+SP_UNROLL
+    for (int i = 0; i < B * B; ++i) fp[(Fac<B>::SINV + i) * SK] = Si[i];
+SP_UNROLL
+    for (int i = 0; i < B; ++i) fp[(Fac<B>::H + i) * SK] = h[i];
+    return true;
+}
+
+template <int B>
+SP_DEV void write_rec(double* rec, long long SK, long long g, const ElimState<B>& es,
+                      const double* Rdiag, const double* Rrhs, bool hasL) {
+    double* r = rec + g;
+SP_UNROLL
+    for (int i = 0; i < B * B; ++i) r[(Rec<B>::RDIAG + i) * SK] = Rdiag[i];
+SP_UNROLL
+    for (int i = 0; i < B * B; ++i) r[(Rec<B>::LDIAG + i) * SK] = es.accLL[i];
+    // coupling (L, R) of the reduced system = (P'_{R,L})^T = W^T
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j < B; ++j) r[(Rec<B>::LR + i * B + j) * SK] = hasL ? es.W[j * B + i] : 0.0;
+SP_UNROLL
+    for (int i = 0; i < B; ++i) r[(Rec<B>::RRHS + i) * SK] = Rrhs[i];
+SP_UNROLL
+    for (int i = 0; i < B; ++i) r[(Rec<B>::LRHS + i) * SK] = es.accrL[i];
+    r[Rec<B>::LOGDET * SK] = es.logdet;
+}
+
+// Q̃ = Q + jit I -> Q̃^{-1} (and its log-determinant).
+template <int B>
+SP_DEV bool qt_inverse(const double* Q, double jit, int breal, double* Qinv, double* ldq) {
+    double Qt[B * B], L[B * B];
+SP_UNROLL
+    for (int i = 0; i < B * B; ++i) Qt[i] = Q[i];
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+        if (i < breal) Qt[i * B + i] += jit;
+    bool ok;
+    if (ldq) ok = chol<B>(L, Qt, *ldq);
+    else ok = chol_nolog<B>(L, Qt);
+    if (!ok) return false;
+    chol_inverse<B>(Qinv, L);
+    return true;
+}
+
+// ======================================================= level 0 (fused) ======
+
+template <class T>
+__global__ void __launch_bounds__(128) k_fwd0(ModelDesc md, const double* __restrict__ params,
+                                              const double* __restrict__ t,
+                                              const double* __restrict__ y, Geom geo,
+                                              double* __restrict__ fac, double* __restrict__ rec,
+                                              double* __restrict__ part,
+                                              unsigned long long* status) {
+    constexpr int B = T::B;
+    const long long K = geo.K[0], SK = K * geo.S;
+    const long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (g >= SK) return;
+    const int s = static_cast<int>(g / K);
+    const long long c = g - s * K;
+    const long long n = geo.n[0];
+    const int m = geo.m[0];
+    const long long st = c * m, en = min(n, st + m);
+    const double* ts = t + s * n;
+    const double* ys = y + s * n;
+    const double* rp = params + static_cast<long long>(s) * md.rec_stride;
+    const double sig = rp[0], jit = rp[1], is2 = 1.0 / (sig * sig);
+    const long long gbase = static_cast<long long>(s) * n;
+    const bool hasL = c > 0;
+
+    double Phi[B * B], Q[B * B], Qinv[B * B];
+    double dt = -1.0;
+    if (st > 0) {
+        dt = ts[st] - ts[st - 1];
+        if (!(dt > 0.0) || !isfinite(dt)) {
+            report(status, gbase + st, dt == 0.0 ? ST_DUPLICATE : ST_BAD_ARG);
+            return;
+        }
+    }
+    T::step(md, rp, dt, Phi, Q);
+    if (!qt_inverse<B>(Q, jit, md.b, Qinv, nullptr)) {
+        report(status, gbase + st, ST_SINGULAR_Q);
+        return;
+    }
+    ElimState<B> es;
+    elim_init<B>(es);
+    if (hasL) {  // P_{s, s-1} = U_{s-1}^T = -Q̃_s^{-1} Φ_s
+        mm<B>(es.W, Qinv, Phi);
+SP_UNROLL
+        for (int i = 0; i < B * B; ++i) es.W[i] = -es.W[i];
+    }
+    double HH[B * B];
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j < B; ++j) HH[i * B + j] = T::H(md, i) * T::H(md, j) * is2;
+
+    for (long long j = st; j < en - 1; ++j) {
+        const double dtn = ts[j + 1] - ts[j];
+        if (!(dtn > 0.0) || !isfinite(dtn)) {
+            report(status, gbase + j + 1, dtn == 0.0 ? ST_DUPLICATE : ST_BAD_ARG);
+            return;
+        }
+        double Phn[B * B], Qn[B * B], Qinvn[B * B];
+        T::step(md, rp, dtn, Phn, Qn);
+        if (!qt_inverse<B>(Qn, jit, md.b, Qinvn, nullptr)) {
+            report(status, gbase + j + 1, ST_SINGULAR_Q);
+            return;
+        }
+        double PtQ[B * B], D[B * B], U[B * B], r[B];
+        mtm<B>(PtQ, Phn, Qinvn);
+        mm<B>(D, PtQ, Phn);
+        msym<B>(D);
+SP_UNROLL
+        for (int i = 0; i < B * B; ++i) {
+            D[i] += Qinv[i] + HH[i];
+            U[i] = -PtQ[i];
+        }
+        const double yj = ys[j];
+        if (!isfinite(yj)) {
+            report(status, gbase + j, ST_BAD_ARG);
+            return;
+        }
+SP_UNROLL
+        for (int i = 0; i < B; ++i) r[i] = T::H(md, i) * yj * is2;
+        double* fp = fac + (j - st) * Fac<B>::N * SK + g;
+        if (!elim_block<B>(es, D, U, r, hasL, fp, SK)) {
+            report(status, gbase + j, ST_NOT_PD);
+            return;
+        }
+        mcopy<B>(Qinv, Qinvn);
+    }
+    // separator R = en - 1
+    double D[B * B], Rr[B];
+SP_UNROLL
+    for (int i = 0; i < B * B; ++i) D[i] = Qinv[i] + HH[i];
+    if (en < n) {
+        const double dte = ts[en] - ts[en - 1];
+        if (!(dte > 0.0) || !isfinite(dte)) {
+            report(status, gbase + en, dte == 0.0 ? ST_DUPLICATE : ST_BAD_ARG);
+            return;
+        }
+        double Phn[B * B], Qn[B * B], Qinvn[B * B], PtQ[B * B], X[B * B];
+        T::step(md, rp, dte, Phn, Qn);
+        if (!qt_inverse<B>(Qn, jit, md.b, Qinvn, nullptr)) {
+            report(status, gbase + en, ST_SINGULAR_Q);
+            return;
+        }
+        mtm<B>(PtQ, Phn, Qinvn);
+        mm<B>(X, PtQ, Phn);
+        msym<B>(X);
+SP_UNROLL
+        for (int i = 0; i < B * B; ++i) D[i] += X[i];
+    }
+    const double yR = ys[en - 1];
+    if (!isfinite(yR)) {
+        report(status, gbase + en - 1, ST_BAD_ARG);
+        return;
+    }
+SP_UNROLL
+    for (int i = 0; i < B * B; ++i) D[i] -= es.T[i];
+SP_UNROLL
+    for (int i = 0; i < B; ++i) Rr[i] = T::H(md, i) * yR * is2 - es.rc[i];
+    write_rec<B>(rec, SK, g, es, D, Rr, hasL);
+    part[P_LOGDET * SK + g] = es.logdet;
+}
+
+// ============================================= materialised / upper levels ====
+// Block source for level l >= 1: the records of level l-1 chunks.
+template <int B>
+struct RecSource {
+    const double* rec;  // level l-1 records
+    long long SKp;      // S * K[l-1]
+    long long n;        // blocks per series at this level (= K[l-1])
+    SP_DEV void block(int s, long long k, double* D, double* U, double* r, bool wantU) const {
+        const long long i0 = static_cast<long long>(s) * n + k;
+        const bool nx = k + 1 < n;
+SP_UNROLL
+        for (int q = 0; q < B * B; ++q)
+            D[q] = rec[(Rec<B>::RDIAG + q) * SKp + i0] + (nx ? rec[(Rec<B>::LDIAG + q) * SKp + i0 + 1] : 0.0);
+SP_UNROLL
+        for (int q = 0; q < B; ++q)
+            r[q] = rec[(Rec<B>::RRHS + q) * SKp + i0] + (nx ? rec[(Rec<B>::LRHS + q) * SKp + i0 + 1] : 0.0);
+        if (wantU) upper(s, k, U);
+    }
+    // upper block (k, k+1)
+    SP_DEV void upper(int s, long long k, double* U) const {
+        const long long i1 = static_cast<long long>(s) * n + k + 1;
+SP_UNROLL
+        for (int q = 0; q < B * B; ++q) U[q] = rec[(Rec<B>::LR + q) * SKp + i1];
+    }
+};
+
+// Block source for a user SymBTD (row-major diag[n][b][b], upper[n-1][b][b],
+// rhs[n][b] column `col` of k), padded from b to B with identity blocks.
+template <int B>
+struct UserSource {
+    const double* diag;
+    const double* up;
+    const double* rhs;
+    long long n;
+    int b, k, col;
+    SP_DEV void block(int, long long i, double* D, double* U, double* r, bool wantU) const {
+SP_UNROLL
+        for (int p = 0; p < B; ++p)
+SP_UNROLL
+            for (int q = 0; q < B; ++q)
+                D[p * B + q] = (p < b && q < b) ? diag[(i * b + p) * b + q] : (p == q ? 1.0 : 0.0);
+SP_UNROLL
+        for (int p = 0; p < B; ++p) r[p] = (p < b && rhs) ? rhs[(i * b + p) * k + col] : 0.0;
+        if (wantU) upper(0, i, U);
+    }
+    SP_DEV void upper(int, long long i, double* U) const {
+SP_UNROLL
+        for (int p = 0; p < B; ++p)
+SP_UNROLL
+            for (int q = 0; q < B; ++q) U[p * B + q] = (p < b && q < b) ? up[(i * b + p) * b + q] : 0.0;
+    }
+};
+
+template <int B, class Src>
+__global__ void __launch_bounds__(128) k_fwdL(Src src, Geom geo, int lev, double* __restrict__ fac,
+                                              double* __restrict__ rec,
+                                              unsigned long long* status) {
+    const long long K = geo.K[lev], SK = K * geo.S;
+    const long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (g >= SK) return;
+    const int s = static_cast<int>(g / K);
+    const long long c = g - s * K;
+    const long long n = geo.n[lev];
+    const int m = geo.m[lev];
+    const long long st = c * m, en = min(n, st + m);
+    const bool hasL = c > 0;
+    const long long gbase = static_cast<long long>(s) * geo.n[0];
+    ElimState<B> es;
+    elim_init<B>(es);
+    if (hasL) {  // P_{st, st-1} = upper(st-1)^T
+        double U[B * B];
+        src.upper(s, st - 1, U);
+SP_UNROLL
+        for (int i = 0; i < B; ++i)
+SP_UNROLL
+            for (int j = 0; j < B; ++j) es.W[i * B + j] = U[j * B + i];
+    }
+    for (long long j = st; j < en - 1; ++j) {
+        double D[B * B], U[B * B], r[B];
+        src.block(s, j, D, U, r, true);
+        double* fp = fac + (j - st) * Fac<B>::N * SK + g;
+        if (!elim_block<B>(es, D, U, r, hasL, fp, SK)) {
+            report(status, gbase + to_global(geo, lev, j), ST_NOT_PD);
+            return;
+        }
+    }
+    double D[B * B], U[B * B], r[B];
+    src.block(s, en - 1, D, U, r, false);
+SP_UNROLL
+    for (int i = 0; i < B * B; ++i) D[i] -= es.T[i];
+SP_UNROLL
+    for (int i = 0; i < B; ++i) r[i] -= es.rc[i];
+    write_rec<B>(rec, SK, g, es, D, r, hasL);
+}
+
+// The single block left per series: invert it.
+template <int B>
+__global__ void k_top(Geom geo, const double* __restrict__ rec, double* __restrict__ sol,
+                      double* __restrict__ toplogdet, unsigned long long* status) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= geo.S) return;
+    const int L = geo.nlev;
+    const long long SK = geo.S;  // K = 1 at the last level
+    double D[B * B], r[B], Lc[B * B], C[B * B], x[B], ld;
+SP_UNROLL
+    for (int q = 0; q < B * B; ++q) D[q] = rec[(Rec<B>::RDIAG + q) * SK + s];
+SP_UNROLL
+    for (int q = 0; q < B; ++q) r[q] = rec[(Rec<B>::RRHS + q) * SK + s];
+    msym<B>(D);
+    if (!chol<B>(Lc, D, ld)) {
+        report(status, static_cast<long long>(s) * geo.n[0] + to_global(geo, L, 0), ST_NOT_PD);
+        return;
+    }
+    chol_inverse<B>(C, Lc);
+    mv<B>(x, C, r);
+    const long long Sn = geo.S;
+SP_UNROLL
+    for (int q = 0; q < B; ++q) sol[(Sol<B>::X + q) * Sn + s] = x[q];
+SP_UNROLL
+    for (int q = 0; q < B * B; ++q) sol[(Sol<B>::CD + q) * Sn + s] = C[q];
+    toplogdet[s] = ld;
+}
+
+// Separator data of chunk c from the level above.
+template <int B>
+struct SepData {
+    double xR[B], CRR[B * B], xL[B], CLL[B * B], CLR[B * B];
+};
+template <int B>
+SP_DEV void load_sep(const double* solU, long long SnU, long long iR, bool hasL, bool needC,
+                     SepData<B>& sd) {
+SP_UNROLL
+    for (int q = 0; q < B; ++q) sd.xR[q] = solU[(Sol<B>::X + q) * SnU + iR];
+    if (needC)
+SP_UNROLL
+        for (int q = 0; q < B * B; ++q) sd.CRR[q] = solU[(Sol<B>::CD + q) * SnU + iR];
+    if (hasL) {
+SP_UNROLL
+        for (int q = 0; q < B; ++q) sd.xL[q] = solU[(Sol<B>::X + q) * SnU + iR - 1];
+        if (needC) {
+SP_UNROLL
+            for (int q = 0; q < B * B; ++q) sd.CLL[q] = solU[(Sol<B>::CD + q) * SnU + iR - 1];
+SP_UNROLL
+            for (int q = 0; q < B * B; ++q) sd.CLR[q] = solU[(Sol<B>::CU + q) * SnU + iR - 1];
+        }
+    } else {
+        vzero<B>(sd.xL);
+        mzero<B>(sd.CLL);
+        mzero<B>(sd.CLR);
+    }
+}
+
+// One step of the reverse sweep: given S^{-1}, V, h, G of block j and the carried
+// (x_n, C_nn, C_nL) of block n = j+1, produce x_j (and C_jL, C_jn, C_jj).
+template <int B>
+SP_DEV void back_step(const double* Si, const double* V, const double* h, const double* G,
+                      bool hasL, bool needC, const SepData<B>& sd, const double* xn,
+                      const double* Cnn, const double* CnL, double* xj, double* CjL, double* Cjn,
+                      double* Cjj) {
+    double tmp[B];
+    mv<B>(xj, G, xn);
+SP_UNROLL
+    for (int i = 0; i < B; ++i) xj[i] = h[i] - xj[i];
+    if (hasL) {
+        mv<B>(tmp, V, sd.xL);
+SP_UNROLL
+        for (int i = 0; i < B; ++i) xj[i] -= tmp[i];
+    }
+    if (!needC) return;
+    double X[B * B];
+    mm<B>(CjL, G, CnL);
+    mm<B>(Cjn, G, Cnn);
+    if (hasL) {
+        mm<B>(X, V, sd.CLL);
+SP_UNROLL
+        for (int i = 0; i < B * B; ++i) CjL[i] += X[i];
+        mmt<B>(X, V, CnL);  // V C_{L,n} = V C_{n,L}^T
+SP_UNROLL
+        for (int i = 0; i < B * B; ++i) Cjn[i] += X[i];
+    }
+SP_UNROLL
+    for (int i = 0; i < B * B; ++i) {
+        CjL[i] = -CjL[i];
+        Cjn[i] = -Cjn[i];
+    }
+    mmt<B>(Cjj, Cjn, G);
+SP_UNROLL
+    for (int i = 0; i < B * B; ++i) Cjj[i] = Si[i] - Cjj[i];
+    if (hasL) {
+        mmt<B>(X, CjL, V);
+SP_UNROLL
+        for (int i = 0; i < B * B; ++i) Cjj[i] -= X[i];
+    }
+    msym<B>(Cjj);
+}
+
+template <int B>
+SP_DEV void load_fac(const double* fp, long long SK, bool hasL, double* Si, double* V, double* h) {
+SP_UNROLL
+    for (int i = 0; i < B * B; ++i) Si[i] = fp[(Fac<B>::SINV + i) * SK];
+    if (hasL)
+SP_UNROLL
+        for (int i = 0; i < B * B; ++i) V[i] = fp[(Fac<B>::V + i) * SK];
+SP_UNROLL
+    for (int i = 0; i < B; ++i) h[i] = fp[(Fac<B>::H + i) * SK];
+}
+
+// Solution sinks for the reverse sweep of levels >= 1.
+template <int B>
+struct SolSink {  // component-major sol of this level
+    double* sol;
+    long long Sn;  // S * n
+    long long n;
+    SP_DEV void put(int s, long long i, const double* x, const double* Cd, bool needC) const {
+        const long long k = static_cast<long long>(s) * n + i;
+SP_UNROLL
+        for (int q = 0; q < B; ++q) sol[(Sol<B>::X + q) * Sn + k] = x[q];
+        if (needC)
+SP_UNROLL
+            for (int q = 0; q < B * B; ++q) sol[(Sol<B>::CD + q) * Sn + k] = Cd[q];
+    }
+    SP_DEV void put_upper(int s, long long i, const double* Cu) const {
+        const long long k = static_cast<long long>(s) * n + i;
+SP_UNROLL
+        for (int q = 0; q < B * B; ++q) sol[(Sol<B>::CU + q) * Sn + k] = Cu[q];
+    }
+};
+template <int B>
+struct UserSink {  // row-major user outputs (b <= B), any may be null
+    double* x;
+    double* cdiag;
+    double* cupper;
+    int b, k, col;
+    SP_DEV void put(int, long long i, const double* xv, const double* Cd, bool needC) const {
+        if (x)
+            for (int p = 0; p < b; ++p) x[(i * b + p) * k + col] = xv[p];
+        if (needC && cdiag)
+            for (int p = 0; p < b; ++p)
+                for (int q = 0; q < b; ++q) cdiag[(i * b + p) * b + q] = Cd[p * B + q];
+    }
+    SP_DEV void put_upper(int, long long i, const double* Cu) const {
+        if (cupper)
+            for (int p = 0; p < b; ++p)
+                for (int q = 0; q < b; ++q) cupper[(i * b + p) * b + q] = Cu[p * B + q];
+    }
+};
+
+template <int B, class Src, class Sink>
+__global__ void __launch_bounds__(128) k_revL(Src src, Sink sink, Geom geo, int lev,
+                                              const double* __restrict__ fac,
+                                              const double* __restrict__ solU, int needC) {
+    const long long K = geo.K[lev], SK = K * geo.S;
+    const long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (g >= SK) return;
+    const int s = static_cast<int>(g / K);
+    const long long c = g - s * K;
+    const long long n = geo.n[lev];
+    const int m = geo.m[lev];
+    const long long st = c * m, en = min(n, st + m);
+    const bool hasL = c > 0;
+    SepData<B> sd;
+    load_sep<B>(solU, static_cast<long long>(geo.S) * geo.n[lev + 1], g, hasL, needC, sd);
+    double xn[B], Cnn[B * B], CnL[B * B];
+SP_UNROLL
+    for (int q = 0; q < B; ++q) xn[q] = sd.xR[q];
+    mcopy<B>(Cnn, sd.CRR);
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j < B; ++j) CnL[i * B + j] = sd.CLR[j * B + i];
+    sink.put(s, en - 1, xn, Cnn, needC);
+    for (long long j = en - 2; j >= st; --j) {
+        double Si[B * B], V[B * B], h[B], U[B * B], G[B * B];
+        load_fac<B>(fac + (j - st) * Fac<B>::N * SK + g, SK, hasL, Si, V, h);
+        src.upper(s, j, U);
+        mm<B>(G, Si, U);
+        double xj[B], CjL[B * B], Cjn[B * B], Cjj[B * B];
+        back_step<B>(Si, V, h, G, hasL, needC, sd, xn, Cnn, CnL, xj, CjL, Cjn, Cjj);
+        sink.put(s, j, xj, Cjj, needC);
+        if (needC) sink.put_upper(s, j, Cjn);
+SP_UNROLL
+        for (int q = 0; q < B; ++q) xn[q] = xj[q];
+        if (needC) {
+            mcopy<B>(Cnn, Cjj);
+            mcopy<B>(CnL, CjL);
+        }
+    }
+    if (hasL && needC) {  // C_{st-1, st} = C_{st, L}^T
+        double X[B * B];
+SP_UNROLL
+        for (int i = 0; i < B; ++i)
+SP_UNROLL
+            for (int j = 0; j < B; ++j) X[i * B + j] = CnL[j * B + i];
+        sink.put_upper(s, st - 1, X);
+    }
+}
+
+// ============================================ level-0 reverse (fused outputs) ==
+
+struct Outs {
+    double* mean;
+    double* var;
+    int include_noise;
+    int want_grad;
+    int need_c;
+};
+
+template <class T>
+SP_DEV void point_out(const ModelDesc& md, const Outs& o, long long gi, double yv, double is2,
+                      double sig, const double* x, const double* C, double& fy, double& noise,
+                      unsigned long long* status) {
+    constexpr int B = T::B;
+    double mu = 0.0;
+SP_UNROLL
+    for (int k = 0; k < B; ++k) mu += T::H(md, k) * x[k];
+    const double r = yv - mu;
+    fy += r * r * is2;
+    if (o.mean) o.mean[gi] = mu;
+    if (o.need_c) {
+        double v = 0.0;
+SP_UNROLL
+        for (int a = 0; a < B; ++a)
+SP_UNROLL
+            for (int b2 = 0; b2 < B; ++b2) v += T::H(md, a) * C[a * B + b2] * T::H(md, b2);
+        noise += r * r + v;
+        if (o.var) {
+            if (v < -1e-10) report(status, gi, ST_NEG_VAR);
+            if (v < 0.0) v = 0.0;  // clamp [-1e-10, 0) -> 0
+            o.var[gi] = o.include_noise ? v + sig * sig : v;
+        }
+    }
+}
+
+// Likelihood / gradient terms of step i with transition Φ (Φ := 0 at the anchor),
+// previous block (xp, Cpp) and cross-covariance Cpc = C_{i-1,i}.
+template <class T>
+SP_DEV void step_terms(const ModelDesc& md, const double* rp, double dt, const double* Phi,
+                       const double* Qraw, const double* Qinv, const double* xc, const double* Ccc,
+                       const double* xp, const double* Cpp, const double* Cpc, bool anchor,
+                       bool grad, double& fe, double* g) {
+    constexpr int B = T::B;
+    double e[B], tmp[B];
+    if (anchor) {
+SP_UNROLL
+        for (int i = 0; i < B; ++i) e[i] = xc[i];
+    } else {
+        mv<B>(tmp, Phi, xp);
+SP_UNROLL
+        for (int i = 0; i < B; ++i) e[i] = xc[i] - tmp[i];
+    }
+    mv<B>(tmp, Qinv, e);
+    double q = 0.0;
+SP_UNROLL
+    for (int i = 0; i < B; ++i) q += e[i] * tmp[i];
+    fe += q;
+    if (!grad) return;
+    double E[B * B], Bm[B * B], X[B * B], Y[B * B];
+    if (anchor) {
+SP_UNROLL
+        for (int i = 0; i < B; ++i)
+SP_UNROLL
+            for (int j = 0; j < B; ++j) E[i * B + j] = Ccc[i * B + j] + e[i] * e[j];
+        mzero<B>(Bm);
+    } else {
+        // E = C_cc - Φ C_pc - (Φ C_pc)^T + Φ C_pp Φ^T + e e^T
+        mm<B>(X, Phi, Cpc);
+        mm<B>(Y, Phi, Cpp);
+        double Z[B * B];
+        mmt<B>(Z, Y, Phi);
+SP_UNROLL
+        for (int i = 0; i < B; ++i)
+SP_UNROLL
+            for (int j = 0; j < B; ++j)
+                E[i * B + j] = Ccc[i * B + j] - X[i * B + j] - X[j * B + i] + Z[i * B + j] + e[i] * e[j];
+        // Z_i = C_pc - C_pp Φ^T + x_p e^T ;  Bm = Z Q̃^{-1}
+        mmt<B>(Y, Cpp, Phi);
+SP_UNROLL
+        for (int i = 0; i < B; ++i)
+SP_UNROLL
+            for (int j = 0; j < B; ++j) Z[i * B + j] = Cpc[i * B + j] - Y[i * B + j] + xp[i] * e[j];
+        mm<B>(Bm, Z, Qinv);
+    }
+    // M = Q̃^{-1} E Q̃^{-1} - Q̃^{-1}
+    mm<B>(X, Qinv, E);
+    mm<B>(Y, X, Qinv);
+SP_UNROLL
+    for (int i = 0; i < B * B; ++i) Y[i] -= Qinv[i];
+    msym<B>(Y);
+    T::grad(md, rp, dt, Phi, Qraw, Y, Bm, g);
+}
+
+template <class T>
+__global__ void __launch_bounds__(128) k_rev0(ModelDesc md, const double* __restrict__ params,
+                                              const double* __restrict__ t,
+                                              const double* __restrict__ y, Geom geo,
+                                              const double* __restrict__ fac,
+                                              const double* __restrict__ solU,
+                                              double* __restrict__ part, Outs outs,
+                                              unsigned long long* status) {
+    constexpr int B = T::B;
+    const long long K = geo.K[0], SK = K * geo.S;
+    const long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (g >= SK) return;
+    const int s = static_cast<int>(g / K);
+    const long long c = g - s * K;
+    const long long n = geo.n[0];
+    const int m = geo.m[0];
+    const long long st = c * m, en = min(n, st + m);
+    const double* ts = t + s * n;
+    const double* ys = y + s * n;
+    const double* rp = params + static_cast<long long>(s) * md.rec_stride;
+    const double sig = rp[0], jit = rp[1], is2 = 1.0 / (sig * sig);
+    const long long gbase = static_cast<long long>(s) * n;
+    const bool hasL = c > 0;
+    const bool needC = outs.need_c != 0, grad = outs.want_grad != 0;
+
+    SepData<B> sd;
+    load_sep<B>(solU, static_cast<long long>(geo.S) * geo.n[1], g, hasL, needC, sd);
+    double xn[B], Cnn[B * B], CnL[B * B];
+SP_UNROLL
+    for (int q = 0; q < B; ++q) xn[q] = sd.xR[q];
+    mcopy<B>(Cnn, sd.CRR);
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j < B; ++j) CnL[i * B + j] = sd.CLR[j * B + i];
+
+    double fy = 0.0, fe = 0.0, ldq = 0.0, noise = 0.0;
+    double gr[kMaxTheta];
+    for (int p = 0; p < md.nt; ++p) gr[p] = 0.0;
+
+    for (long long j = en - 2; j >= st; --j) {
+        const long long nb = j + 1;
+        const double dt = ts[nb] - ts[j];
+        double Phn[B * B], Qn[B * B], Qinvn[B * B], ldqn;
+        T::step(md, rp, dt, Phn, Qn);
+        qt_inverse<B>(Qn, jit, md.b, Qinvn, &ldqn);
+        double Si[B * B], V[B * B], h[B], U[B * B], G[B * B];
+        load_fac<B>(fac + (j - st) * Fac<B>::N * SK + g, SK, hasL, Si, V, h);
+        mtm<B>(U, Phn, Qinvn);
+SP_UNROLL
+        for (int i = 0; i < B * B; ++i) U[i] = -U[i];
+        mm<B>(G, Si, U);
+        double xj[B], CjL[B * B], Cjn[B * B], Cjj[B * B];
+        back_step<B>(Si, V, h, G, hasL, needC, sd, xn, Cnn, CnL, xj, CjL, Cjn, Cjj);
+        point_out<T>(md, outs, gbase + nb, ys[nb], is2, sig, xn, Cnn, fy, noise, status);
+        ldq += ldqn;
+        step_terms<T>(md, rp, dt, Phn, Qn, Qinvn, xn, Cnn, xj, Cjj, Cjn, false, grad, fe, gr);
+SP_UNROLL
+        for (int q = 0; q < B; ++q) xn[q] = xj[q];
+        if (needC) {
+            mcopy<B>(Cnn, Cjj);
+            mcopy<B>(CnL, CjL);
+        }
+    }
+    // block st: previous block is the left separator (or the anchor at st = 0)
+    point_out<T>(md, outs, gbase + st, ys[st], is2, sig, xn, Cnn, fy, noise, status);
+    {
+        const bool anchor = st == 0;
+        const double dt = anchor ? -1.0 : ts[st] - ts[st - 1];
+        double Ph[B * B], Qr[B * B], Qi[B * B], ldq0;
+        T::step(md, rp, dt, Ph, Qr);
+        qt_inverse<B>(Qr, jit, md.b, Qi, &ldq0);
+        ldq += ldq0;
+        double CLs[B * B];  // C_{L, st} = C_{st, L}^T
+SP_UNROLL
+        for (int i = 0; i < B; ++i)
+SP_UNROLL
+            for (int j = 0; j < B; ++j) CLs[i * B + j] = CnL[j * B + i];
+        step_terms<T>(md, rp, dt, Ph, Qr, Qi, xn, Cnn, sd.xL, sd.CLL, CLs, anchor, grad, fe, gr);
+    }
+    part[P_FITY * SK + g] = fy;
+    part[P_FITE * SK + g] = fe;
+    part[P_LDQ * SK + g] = ldq;
+    part[P_NOISE * SK + g] = noise;
+    for (int p = 0; p < md.nt; ++p) part[(P_GRAD + p) * SK + g] = gr[p];
+}
+
+// ================================================================ reductions ==
+
+// Stage 1: per series, per segment of kSeg chunks, fixed-order sums of the
+// level-0 partial components.  out[(s * nseg + seg) * NC + comp]
+constexpr int kSeg = 1024;
+static __global__ void k_reduce_seg(const double* __restrict__ part, long long K, int S, int NC,
+                             double* __restrict__ out) {
+    __shared__ double sh[kSeg / 4];
+    const int s = blockIdx.y, seg = blockIdx.x;
+    const int nseg = gridDim.x;
+    const long long SK = K * S;
+    const long long base = static_cast<long long>(s) * K + static_cast<long long>(seg) * kSeg;
+    const long long lim = min(static_cast<long long>(kSeg), K - static_cast<long long>(seg) * kSeg);
+    for (int comp = 0; comp < NC; ++comp) {
+        double v = 0.0;
+        // thread t sums elements t, t+256, t+512, t+768 in order
+        for (int k = threadIdx.x; k < lim; k += blockDim.x) v += part[comp * SK + base + k];
+        sh[threadIdx.x] = v;
+        __syncthreads();
+        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+            if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) out[(static_cast<long long>(s) * nseg + seg) * NC + comp] = sh[0];
+        __syncthreads();
+    }
+}
+
+struct FinalArgs {
+    const double* seg;     // [S][nseg][NC]
+    int nseg, NC;
+    const double* recs[kMaxLev];  // records of every level (logdet component)
+    int logdet_comp;       // Rec<B>::LOGDET
+    const double* toplogdet;
+    const double* params;
+    int rec_stride, nt;
+    long long n;
+    double* loglik;        // [S]
+    double* grad;          // [S][nt+1] or null
+};
+
+// Stage 2: one CTA per series.  Deterministic fixed-order tree sums.
+static __global__ void k_reduce_final(FinalArgs a, Geom geo) {
+    __shared__ double sh[256];
+    __shared__ double acc[8 + kMaxTheta];
+    const int s = blockIdx.x;
+    // level-0 partial components from the segments
+    for (int comp = 0; comp < a.NC; ++comp) {
+        double v = 0.0;
+        for (int k = threadIdx.x; k < a.nseg; k += blockDim.x)
+            v += a.seg[(static_cast<long long>(s) * a.nseg + k) * a.NC + comp];
+        sh[threadIdx.x] = v;
+        __syncthreads();
+        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+            if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) acc[comp] = sh[0];
+        __syncthreads();
+    }
+    // logdets of the upper levels
+    double v = 0.0;
+    for (int l = 1; l < geo.nlev; ++l) {
+        const long long K = geo.K[l], SK = K * geo.S;
+        for (long long k = threadIdx.x; k < K; k += blockDim.x)
+            v += a.recs[l][a.logdet_comp * SK + static_cast<long long>(s) * K + k];
+    }
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double ldP = acc[P_LOGDET] + sh[0] + a.toplogdet[s];
+        const double* rp = a.params + static_cast<long long>(s) * a.rec_stride;
+        const double sig = rp[0], s2 = sig * sig;
+        const double nn = static_cast<double>(a.n);
+        const double kLog2Pi = 1.8378770664093454835606594728112;
+        a.loglik[s] = -0.5 * (acc[P_FITY] + acc[P_FITE]) -
+                      0.5 * (ldP + acc[P_LDQ] + nn * log(s2)) - 0.5 * nn * kLog2Pi;
+        if (a.grad) {
+            double* gs = a.grad + static_cast<long long>(s) * (a.nt + 1);
+            for (int p = 0; p < a.nt; ++p) gs[p] = acc[P_GRAD + p];
+            gs[a.nt] = 2.0 * sig * (-0.5 * nn / s2 + acc[P_NOISE] / (2.0 * s2 * s2));
+        }
+    }
+}
+
+// logdet for the standalone BTD operators: sum of all level records + top.
+struct LogdetArgs {
+    const double* recs[kMaxLev];
+    int logdet_comp;
+    const double* toplogdet;
+    double* out;
+};
+static __global__ void k_logdet_btd(Geom geo, LogdetArgs a) {
+    __shared__ double sh[256];
+    double v = 0.0;
+    for (int l = 0; l < geo.nlev; ++l) {
+        const long long K = geo.K[l];
+        for (long long k = threadIdx.x; k < K; k += blockDim.x) v += a.recs[l][a.logdet_comp * K + k];
+    }
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *a.out = sh[0] + a.toplogdet[0];
+}
+
+// y = M v for a user SymBTD (one thread per block row).
+static __global__ void k_matvec(long long n, int b, const double* __restrict__ diag,
+                         const double* __restrict__ up, const double* __restrict__ v,
+                         double* __restrict__ out) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    for (int p = 0; p < b; ++p) {
+        double s = 0.0;
+        for (int q = 0; q < b; ++q) s += diag[(i * b + p) * b + q] * v[i * b + q];
+        if (i + 1 < n)
+            for (int q = 0; q < b; ++q) s += up[(i * b + p) * b + q] * v[(i + 1) * b + q];
+        if (i > 0)
+            for (int q = 0; q < b; ++q) s += up[((i - 1) * b + q) * b + p] * v[(i - 1) * b + q];
+        out[i * b + p] = s;
+    }
+}
+
+// assemble_prior_precision + add_observation_term: one thread per
+// time point writes D_i, U_i (b_real x b_real) and rhs_i.
+template <class T>
+__global__ void __launch_bounds__(128) k_assemble(ModelDesc md, const double* __restrict__ params,
+                                                  const double* __restrict__ t,
+                                                  const double* __restrict__ y, long long n,
+                                                  double* __restrict__ diag, double* __restrict__ up,
+                                                  double* __restrict__ rhs, unsigned long long* status) {
+    constexpr int B = T::B;
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const double sig = params[0], jit = params[1], is2 = 1.0 / (sig * sig);
+    const int b = md.b;
+    double Phi[B * B], Q[B * B], Qinv[B * B], D[B * B];
+    const double dt = i == 0 ? -1.0 : t[i] - t[i - 1];
+    if (i > 0 && (!(dt > 0.0) || !isfinite(dt))) {
+        report(status, i, dt == 0.0 ? ST_DUPLICATE : ST_BAD_ARG);
+        return;
+    }
+    T::step(md, params, dt, Phi, Q);
+    if (!qt_inverse<B>(Q, jit, b, Qinv, nullptr)) {
+        report(status, i, ST_SINGULAR_Q);
+        return;
+    }
+    mcopy<B>(D, Qinv);
+    if (i + 1 < n) {
+        const double dtn = t[i + 1] - t[i];
+        if (!(dtn > 0.0) || !isfinite(dtn)) {
+            report(status, i + 1, dtn == 0.0 ? ST_DUPLICATE : ST_BAD_ARG);
+            return;
+        }
+        double Phn[B * B], Qn[B * B], Qinvn[B * B], PtQ[B * B], X[B * B];
+        T::step(md, params, dtn, Phn, Qn);
+        if (!qt_inverse<B>(Qn, jit, b, Qinvn, nullptr)) {
+            report(status, i + 1, ST_SINGULAR_Q);
+            return;
+        }
+        mtm<B>(PtQ, Phn, Qinvn);
+        mm<B>(X, PtQ, Phn);
+        msym<B>(X);
+        for (int q = 0; q < B * B; ++q) D[q] += X[q];
+        for (int p = 0; p < b; ++p)
+            for (int q = 0; q < b; ++q) up[(i * b + p) * b + q] = -PtQ[p * B + q];
+    }
+    for (int p = 0; p < b; ++p)
+        for (int q = 0; q < b; ++q)
+            diag[(i * b + p) * b + q] = D[p * B + q] + T::H(md, p) * T::H(md, q) * is2;
+    if (rhs)
+        for (int p = 0; p < b; ++p) rhs[i * b + p] = T::H(md, p) * y[i] * is2;
+}
+
+}  // namespace spingp_dev

@@ -1,0 +1,281 @@
+// host_model.cpp — host-side model setup (g++, C++20): kernel leaves -> device
+// model description and per-series parameter records, plus the host-only C ABI
+// entry points (spingp_kernel_dims, spingp_state_space).  Uses the drop-in
+// C++ API of include/spingp/kernels.hpp for the reference's state_space_of.
+#include "host_model.hpp"
+
+#include <cmath>
+#include <cstring>
+#include <numbers>
+#include <stdexcept>
+
+#include "spingp/kernels.hpp"
+
+using namespace spingp_dev;
+
+namespace spingp_host {
+
+namespace {
+int leaf_dim(const spingp_leaf& l) {
+    switch (l.type) {
+        case SPINGP_MATERN12: return 1;
+        case SPINGP_MATERN32: return 2;
+        case SPINGP_MATERN52: return 3;
+        case SPINGP_EQ: return l.order;
+        case SPINGP_QP: return 2 * (l.order + 1);
+    }
+    throw std::invalid_argument("unknown kernel leaf type");
+}
+int leaf_np(const spingp_leaf& l) { return l.type == SPINGP_QP ? 4 : 2; }
+
+spingp::KernelSpec spec_of(const spingp_leaf* leaves, int32_t n_leaves) {
+    std::vector<spingp::KernelSpec> parts;
+    for (int i = 0; i < n_leaves; ++i) {
+        const spingp_leaf& l = leaves[i];
+        switch (l.type) {
+            case SPINGP_MATERN12: parts.push_back(spingp::KernelSpec::matern12()); break;
+            case SPINGP_MATERN32: parts.push_back(spingp::KernelSpec::matern32()); break;
+            case SPINGP_MATERN52: parts.push_back(spingp::KernelSpec::matern52()); break;
+            case SPINGP_EQ: parts.push_back(spingp::KernelSpec::eq(1.0, 1.0, l.order)); break;
+            case SPINGP_QP: parts.push_back(spingp::KernelSpec::quasi_periodic(1.0, 1.0, 1.0, 1.0, l.order)); break;
+            default: throw std::invalid_argument("unknown kernel leaf type");
+        }
+    }
+    if (parts.empty()) throw std::invalid_argument("kernel has no leaves");
+    if (parts.size() == 1) return parts[0];
+    return spingp::KernelSpec::sum(parts);
+}
+
+}  // namespace
+
+HostModel build_model(const spingp_leaf* leaves, int32_t n_leaves, int32_t n_theta) {
+    if (!leaves || n_leaves < 1) throw std::invalid_argument("kernel has no leaves");
+    if (n_leaves > kMaxLeaves) throw ApiError{SPINGP_UNSUPPORTED, -1, "too many kernel leaves"};
+    HostModel hm;
+    ModelDesc& d = hm.desc;
+    int off = 0, th = 0, rec = 0;
+    for (int l = 0; l < n_leaves; ++l) {
+        const spingp_leaf& lf = leaves[l];
+        if (lf.type == SPINGP_EQ && (lf.order < 2 || lf.order % 2 || lf.order > 16))
+            throw std::invalid_argument("eq approximation order must be even and in [2, 16]");
+        if (lf.type == SPINGP_QP && (lf.order < 0 || lf.order > 15))
+            throw std::invalid_argument("qp harmonics must be in [0, 15]");
+        d.type[l] = lf.type;
+        d.off[l] = off;
+        d.dim[l] = leaf_dim(lf);
+        d.order[l] = lf.order;
+        d.th[l] = th;
+        off += d.dim[l];
+        th += leaf_np(lf);
+    }
+    if (n_theta != th) throw std::invalid_argument("theta size does not match kernel parameter count");
+    if (off > kMaxB) throw ApiError{SPINGP_UNSUPPORTED, -1, "state dimension above 16 is not built"};
+    hm.b = off;
+    hm.nt = th;
+    d.b = off;
+    d.nleaves = n_leaves;
+    d.nt = th;
+    rec = 2 + th;
+    for (int l = 0; l < n_leaves; ++l) {
+        d.rec[l] = rec;
+        switch (leaves[l].type) {
+            case SPINGP_MATERN12: case SPINGP_MATERN32: case SPINGP_MATERN52: rec += 3; break;
+            case SPINGP_EQ: rec += 2; break;
+            case SPINGP_QP: rec += 5 + 2 * (leaves[l].order + 1); break;
+        }
+        d.eqc[l] = 0;
+        if (leaves[l].type == SPINGP_EQ) {
+            // unit variance / unit lengthscale model: roots (a, c) and P1
+            const int J = leaves[l].order;
+            const auto m = spingp::eq_approx_ss(1.0, 1.0, J);
+            d.eqc[l] = static_cast<int>(hm.eqconst.size());
+            for (int p = 0; p < J / 2; ++p) {
+                hm.eqconst.push_back(m.F(2 * p, 2 * p));
+                hm.eqconst.push_back(m.F(2 * p, 2 * p + 1));
+            }
+            for (int i = 0; i < J; ++i)
+                for (int j = 0; j < J; ++j) hm.eqconst.push_back(m.Pinf(i, j));
+        }
+    }
+    hm.rec_stride = rec;
+    d.rec_stride = rec;
+    // emission row
+    const auto ssm = spingp::state_space_of(spec_of(leaves, n_leaves), spingp::default_theta(spec_of(leaves, n_leaves)));
+    for (int i = 0; i < kMaxB; ++i) d.H[i] = i < hm.b ? ssm.H(i) : 0.0;
+    hm.single_matern = n_leaves == 1 && leaves[0].type <= SPINGP_MATERN52;
+    return hm;
+}
+
+// Per-series record (see model_dev.cuh): sigma, jitter, d jitter/dθ, leaf records.
+void fill_record(const HostModel& hm, const double* theta, double sigma, double* r) {
+    if (!(sigma > 0.0) || !std::isfinite(sigma)) throw std::invalid_argument("sigma must be positive");
+    const ModelDesc& d = hm.desc;
+    const double b = hm.b;
+    double tr = 0.0;
+    std::vector<double> dtr(hm.nt, 0.0);
+    for (int l = 0; l < d.nleaves; ++l) {
+        const double* th = theta + d.th[l];
+        const char* nm[4] = {"var", "len", "period", "env"};
+        for (int p = 0; p < (d.type[l] == QP ? 4 : 2); ++p)
+            if (!(th[p] > 0.0) || !std::isfinite(th[p]))
+                throw std::invalid_argument(std::string("hyperparameter must be positive: ") + nm[p]);
+        const double var = th[0], len = th[1];
+        double* lr = r + d.rec[l];
+        switch (d.type[l]) {
+            case MATERN12: case MATERN32: case MATERN52: {
+                const double lam = d.type[l] == MATERN12 ? 1.0 / len
+                                   : d.type[l] == MATERN32 ? std::sqrt(3.0) / len
+                                                           : std::sqrt(5.0) / len;
+                lr[0] = var; lr[1] = len; lr[2] = lam;
+                // Pinf diagonal: var * (1, lam^2, lam^4 / ...) as in kernels.hpp:137-200
+                double pd[3] = {var, 0.0, 0.0};
+                if (d.type[l] == MATERN32) pd[1] = var * lam * lam;
+                if (d.type[l] == MATERN52) {
+                    pd[1] = var * lam * lam / 3.0;
+                    pd[2] = var * lam * lam * lam * lam;
+                }
+                for (int i = 0; i < d.dim[l]; ++i) {
+                    tr += pd[i];
+                    dtr[d.th[l]] += pd[i] / var;
+                    dtr[d.th[l] + 1] += -(2.0 * i) / len * pd[i];
+                }
+                break;
+            }
+            case EQ: {
+                lr[0] = var; lr[1] = len;
+                const int J = d.dim[l];
+                const double* P1 = hm.eqconst.data() + d.eqc[l] + J;
+                for (int i = 0; i < J; ++i) {
+                    tr += var * P1[i * J + i];
+                    dtr[d.th[l]] += P1[i * J + i];
+                }
+                break;
+            }
+            case QP: {
+                const double period = th[2], env = th[3];
+                const int J = d.order[l];
+                lr[0] = var; lr[1] = len; lr[2] = period; lr[3] = env;
+                lr[4] = 2.0 * std::numbers::pi / period;
+                const double x = 1.0 / (len * len), ex = std::exp(-x);
+                for (int j = 0; j <= J; ++j) {
+                    const double cj = j == 0 ? 1.0 : 2.0;
+                    const double ij = std::cyl_bessel_i(double(j), x);
+                    const double ip = j == 0 ? std::cyl_bessel_i(1.0, x)
+                                             : 0.5 * (std::cyl_bessel_i(double(j - 1), x) +
+                                                      std::cyl_bessel_i(double(j + 1), x));
+                    const double q2 = cj * ij * ex;
+                    const double dq2 = cj * ex * (ip - ij) * (-2.0 / (len * len * len));
+                    lr[5 + j] = q2;
+                    lr[5 + J + 1 + j] = dq2;
+                    tr += 2.0 * var * q2;
+                    dtr[d.th[l]] += 2.0 * q2;
+                    dtr[d.th[l] + 1] += 2.0 * var * dq2;
+                }
+                break;
+            }
+        }
+    }
+    r[0] = sigma;
+    r[1] = 1e-10 * tr / b;
+    for (int p = 0; p < hm.nt; ++p) r[2 + p] = 1e-10 * dtr[p] / b;
+}
+
+// Padded block sizes with kernel instantiations (padding states are exactly
+// decoupled, see model_dev.cuh GenericTraits).
+int pad_b(int b) {
+    static const int sizes[] = {1, 2, 3, 4, 6, 8, 12, 16};
+    for (int s : sizes)
+        if (b <= s) return s;
+    throw ApiError{SPINGP_UNSUPPORTED, -1, "state dimension above 16 is not built"};
+}
+
+// Level 0: enough chunks to give every one of the 148 SMs ~256 resident threads
+// (b <= 3) or ~128 (larger blocks); upper levels: chunks of 8 blocks until one
+// block is left.
+Plan make_plan(int64_t n, int64_t S, int Bsz, int64_t m0_override) {
+    if (n < 1 || S < 1) throw std::invalid_argument("need at least one point and one series");
+    Plan p;
+    Geom& g = p.geo;
+    g.S = static_cast<int>(S);
+    const int64_t target = Bsz <= 3 ? 37888 : 18944;
+    int64_t m0 = m0_override > 0 ? m0_override : std::max<int64_t>(8, (n * S + target - 1) / target);
+    m0 = std::max<int64_t>(1, std::min<int64_t>(m0, n));
+    int lev = 0;
+    int64_t cur = n, m = m0;
+    while (true) {
+        if (lev >= kMaxLev) throw ApiError{SPINGP_UNSUPPORTED, -1, "too many reduction levels"};
+        if (lev > 0) m = cur <= 16 ? cur : 8;
+        if (m < 2 && cur > 1) m = 2;
+        g.n[lev] = cur;
+        g.m[lev] = static_cast<int>(m);
+        g.K[lev] = (cur + m - 1) / m;
+        cur = g.K[lev];
+        ++lev;
+        if (cur == 1) break;
+    }
+    g.nlev = lev;
+    g.n[lev] = 1;
+    return p;
+}
+
+}  // namespace spingp_host
+
+using namespace spingp_host;
+
+namespace {
+thread_local std::string g_host_error;
+template <class F>
+int host_guarded(F&& body) {
+    try {
+        return body();
+    } catch (const ApiError& e) {
+        g_host_error = e.what;
+        return e.status;
+    } catch (const std::invalid_argument& e) {
+        g_host_error = e.what();
+        return SPINGP_BAD_ARG;
+    } catch (const std::exception& e) {
+        g_host_error = e.what();
+        return SPINGP_UNSUPPORTED;
+    }
+}
+}  // namespace
+
+extern "C" {
+
+int spingp_kernel_dims(const spingp_leaf* leaves, int32_t n_leaves, int32_t* b, int32_t* n_theta) {
+    return host_guarded([&] {
+        if (!leaves || n_leaves < 1) throw std::invalid_argument("kernel has no leaves");
+        int bb = 0, nt = 0;
+        for (int i = 0; i < n_leaves; ++i) {
+            bb += leaf_dim(leaves[i]);
+            nt += leaf_np(leaves[i]);
+        }
+        if (b) *b = bb;
+        if (n_theta) *n_theta = nt;
+        return SPINGP_OK;
+    });
+}
+
+int spingp_state_space(const spingp_leaf* leaves, int32_t n_leaves, const double* theta,
+                       int32_t n_theta, double* F, double* H, double* Pinf, double* dF,
+                       double* dPinf, int32_t* f_constant) {
+    return host_guarded([&] {
+        const auto spec = spec_of(leaves, n_leaves);
+        if (static_cast<size_t>(n_theta) != spingp::param_count(spec))
+            throw std::invalid_argument("theta size does not match kernel parameter count");
+        const auto m = spingp::state_space_of(spec, std::vector<double>(theta, theta + n_theta));
+        const auto b = m.dim();
+        if (F) std::memcpy(F, m.F.data(), sizeof(double) * b * b);
+        if (H) std::memcpy(H, m.H.data(), sizeof(double) * b);
+        if (Pinf) std::memcpy(Pinf, m.Pinf.data(), sizeof(double) * b * b);
+        for (size_t p = 0; p < m.theta.size(); ++p) {
+            if (dF) std::memcpy(dF + p * b * b, m.theta[p].dF.data(), sizeof(double) * b * b);
+            if (dPinf) std::memcpy(dPinf + p * b * b, m.theta[p].dPinf.data(), sizeof(double) * b * b);
+            if (f_constant) f_constant[p] = m.theta[p].f_constant ? 1 : 0;
+        }
+        return SPINGP_OK;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,45 @@
+// host_model.hpp — host-side model setup for the device kernels (compiled by g++,
+// C++20; used by the nvcc-compiled launch code through this plain interface).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "model_desc.h"
+#include "spingp_c.h"
+
+namespace spingp_host {
+
+// Error carried to the C ABI boundary (status code + failing block).
+struct ApiError {
+    int status;
+    int64_t block;
+    std::string what;
+};
+
+struct HostModel {
+    spingp_dev::ModelDesc desc{};
+    int b = 0, nt = 0, rec_stride = 0;
+    bool single_matern = false;
+    std::vector<double> eqconst;  // shared per-model constants (EQ leaves)
+};
+
+// Validates the leaves and builds the device description (state_space_of,
+// kernels.hpp:326-381, in the form the closed-form device discretisation needs).
+HostModel build_model(const spingp_leaf* leaves, int32_t n_leaves, int32_t n_theta);
+
+// Per-series record: sigma, jitter, d jitter / d theta, leaf params.
+// Throws std::invalid_argument on non-positive hyperparameters (kernels.hpp:132-135).
+void fill_record(const HostModel& hm, const double* theta, double sigma, double* rec);
+
+// Level structure of the hierarchical reduction for S series of n points.
+struct Plan {
+    spingp_dev::Geom geo{};
+};
+Plan make_plan(int64_t n, int64_t S, int Bsz, int64_t m0_override = 0);
+
+// Padded block size with a kernel instantiation (1, 2, 3, 4, 6, 8, 12, 16).
+int pad_b(int b);
+
+}  // namespace spingp_host

@@ -1,0 +1,126 @@
+// launch_eval.cuh — the fused evaluation pipeline for one kernel-traits type:
+// level-0 fused forward -> upper-level forwards -> top inverse -> upper-level
+// reverses -> level-0 fused reverse (outputs, loglik terms, gradient) ->
+// deterministic two-stage reduction.  Included by the inst_*.cu files only.
+#pragma once
+
+#include "ctx.hpp"
+
+namespace spingp_host {
+
+using namespace spingp_dev;
+
+struct EvalBufs {
+    double* params;
+    double* fac[kMaxLev];
+    double* rec[kMaxLev];
+    double* sol[kMaxLev + 1];
+    double* toplogdet;
+    double* part;
+    double* seg;
+    int nseg;
+};
+
+template <int B>
+EvalBufs carve_eval(spingp_ctx* ctx, const Plan& p, int nt, size_t params_count) {
+    const Geom& g = p.geo;
+    size_t tot = arena_bytes(params_count) + 4096;
+    for (int l = 0; l < g.nlev; ++l) {
+        const size_t SK = static_cast<size_t>(g.K[l]) * g.S;
+        tot += arena_bytes(static_cast<size_t>(g.m[l]) * Fac<B>::N * SK) + arena_bytes(Rec<B>::N * SK);
+    }
+    for (int l = 1; l <= g.nlev; ++l) tot += arena_bytes(Sol<B>::N * static_cast<size_t>(g.n[l]) * g.S);
+    const size_t SK0 = static_cast<size_t>(g.K[0]) * g.S;
+    const int nseg = static_cast<int>((g.K[0] + kSeg - 1) / kSeg);
+    tot += arena_bytes(g.S) + arena_bytes((P_GRAD + nt) * SK0) +
+           arena_bytes(static_cast<size_t>(nseg) * g.S * (P_GRAD + nt));
+    ctx->ensure_ws(tot);
+    ctx->ws.reset();
+    EvalBufs eb{};
+    eb.params = ctx->ws.take<double>(params_count);
+    for (int l = 0; l < g.nlev; ++l) {
+        const size_t SK = static_cast<size_t>(g.K[l]) * g.S;
+        eb.fac[l] = ctx->ws.take<double>(static_cast<size_t>(g.m[l]) * Fac<B>::N * SK);
+        eb.rec[l] = ctx->ws.take<double>(Rec<B>::N * SK);
+    }
+    for (int l = 1; l <= g.nlev; ++l)
+        eb.sol[l] = ctx->ws.take<double>(Sol<B>::N * static_cast<size_t>(g.n[l]) * g.S);
+    eb.toplogdet = ctx->ws.take<double>(g.S);
+    eb.part = ctx->ws.take<double>((P_GRAD + nt) * SK0);
+    eb.nseg = nseg;
+    eb.seg = ctx->ws.take<double>(static_cast<size_t>(nseg) * g.S * (P_GRAD + nt));
+    return eb;
+}
+
+template <class T>
+void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
+    constexpr int B = T::B;
+    const HostModel& hm = *a.hm;
+    const Geom& g = a.plan->geo;
+    const int nt = hm.nt;
+    const size_t ncount = a.nparams + hm.eqconst.size();
+    EvalBufs eb = carve_eval<B>(ctx, *a.plan, nt, ncount);
+    // parameters + EQ constants: one upload through the pinned stage
+    double* st = ctx->stage(ncount);
+    std::memcpy(st, a.h_params, a.nparams * sizeof(double));
+    if (!hm.eqconst.empty()) std::memcpy(st + a.nparams, hm.eqconst.data(), hm.eqconst.size() * sizeof(double));
+    CUDA_OK(cudaMemcpyAsync(eb.params, st, ncount * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    ctx->stage_done();
+    ModelDesc md = hm.desc;
+    md.eqconst = eb.params + a.nparams;
+
+    const int tpb = 128;
+    if (a.mode == 1) {
+        k_assemble<T><<<blocks_for(g.n[0], tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g.n[0], a.d_diag,
+                                                                       a.d_upper, a.d_rhs, ctx->d_status);
+        ctx->launched();
+        return;
+    }
+    const long long SK0 = g.K[0] * g.S;
+    k_fwd0<T><<<blocks_for(SK0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
+                                                             eb.rec[0], eb.part, ctx->d_status);
+    ctx->launched();
+    for (int l = 1; l < g.nlev; ++l) {
+        RecSource<B> src{eb.rec[l - 1], g.K[l - 1] * g.S, g.n[l]};
+        k_fwdL<B, RecSource<B>><<<blocks_for(g.K[l] * g.S, tpb), tpb, 0, ctx->stream>>>(
+            src, g, l, eb.fac[l], eb.rec[l], ctx->d_status);
+        ctx->launched();
+    }
+    k_top<B><<<blocks_for(g.S, 128), 128, 0, ctx->stream>>>(g, eb.rec[g.nlev - 1], eb.sol[g.nlev],
+                                                           eb.toplogdet, ctx->d_status);
+    ctx->launched();
+    const bool grad = a.flags & SPINGP_WANT_GRAD;
+    const bool needC = grad || (a.flags & SPINGP_WANT_VAR);
+    for (int l = g.nlev - 1; l >= 1; --l) {
+        RecSource<B> src{eb.rec[l - 1], g.K[l - 1] * g.S, g.n[l]};
+        SolSink<B> sink{eb.sol[l], g.n[l] * g.S, g.n[l]};
+        k_revL<B, RecSource<B>, SolSink<B>><<<blocks_for(g.K[l] * g.S, tpb), tpb, 0, ctx->stream>>>(
+            src, sink, g, l, eb.fac[l], eb.sol[l + 1], needC ? 1 : 0);
+        ctx->launched();
+    }
+    Outs outs{(a.flags & SPINGP_WANT_MEAN) ? a.d_mean : nullptr, (a.flags & SPINGP_WANT_VAR) ? a.d_var : nullptr,
+              (a.flags & SPINGP_INCLUDE_NOISE) ? 1 : 0, grad ? 1 : 0, needC ? 1 : 0};
+    k_rev0<T><<<blocks_for(SK0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
+                                                             eb.sol[1], eb.part, outs, ctx->d_status);
+    ctx->launched();
+    const int NC = P_GRAD + nt;
+    k_reduce_seg<<<dim3(eb.nseg, g.S), 256, 0, ctx->stream>>>(eb.part, g.K[0], g.S, NC, eb.seg);
+    ctx->launched();
+    FinalArgs fa{};
+    fa.seg = eb.seg;
+    fa.nseg = eb.nseg;
+    fa.NC = NC;
+    for (int l = 0; l < g.nlev; ++l) fa.recs[l] = eb.rec[l];
+    fa.logdet_comp = Rec<B>::LOGDET;
+    fa.toplogdet = eb.toplogdet;
+    fa.params = eb.params;
+    fa.rec_stride = hm.rec_stride;
+    fa.nt = nt;
+    fa.n = g.n[0];
+    fa.loglik = a.d_loglik;
+    fa.grad = grad ? a.d_grad : nullptr;
+    k_reduce_final<<<g.S, 256, 0, ctx->stream>>>(fa, g);
+    ctx->launched();
+}
+
+}  // namespace spingp_host

@@ -1,0 +1,36 @@
+// model_desc.h — plain-C++ description of a state-space model as the device
+// kernels see it (shared by the g++-compiled host model code and the nvcc
+// device code; no CUDA types).
+#pragma once
+
+namespace spingp_dev {
+
+constexpr int kMaxLeaves = 8;
+constexpr int kMaxB = 16;
+constexpr int kMaxTheta = 2 + 4 * kMaxLeaves;
+
+enum LeafType { MATERN12 = 0, MATERN32 = 1, MATERN52 = 2, EQ = 3, QP = 4 };
+
+struct ModelDesc {
+    int b;           // true state dimension (kernels may be instantiated for a padded B)
+    int nleaves;
+    int nt;          // kernel hyperparameters (sigma excluded)
+    int rec_stride;  // doubles per series record
+    int type[kMaxLeaves], off[kMaxLeaves], dim[kMaxLeaves], order[kMaxLeaves];
+    int rec[kMaxLeaves], th[kMaxLeaves], eqc[kMaxLeaves];
+    double H[kMaxB];
+    const double* eqconst;  // per EQ leaf at eqc[l]: (a_p, c_p) p < J/2, then P1[J*J]
+};
+
+constexpr int kMaxLev = 24;
+
+// Level structure of the hierarchical reduction (host-planned, passed to kernels).
+struct Geom {
+    int nlev;                  // number of reduction levels (level nlev-1 has K = 1)
+    int S;                     // independent series
+    long long n[kMaxLev + 1];  // blocks per series at each level (n[0] = points)
+    long long K[kMaxLev];      // chunks per series at each level
+    int m[kMaxLev];            // chunk length at each level
+};
+
+}  // namespace spingp_dev

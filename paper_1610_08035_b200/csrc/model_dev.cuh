@@ -1,0 +1,400 @@
+// model_dev.cuh — per-step discretisation of the state-space models on the device.
+//
+// Replaces the reference's per-step `discretize` / `discretize_with_grad`
+// (kernels.hpp:392-443), which run a Padé expm and one 2b x 2b Van Loan
+// exponential per hyperparameter per step.  Here every leaf uses its exact
+// closed form:
+//   Matérn-ν (b = ν + 1/2):  F + λI is nilpotent, so
+//       Φ = e^{-λΔt} Σ_{k<b} (F+λI)^k Δt^k / k!,
+//       dΦ/dℓ = -(1/ℓ)[K, Φ] - (Δt/ℓ) F Φ   with K = diag(0, 1, ..., b-1)
+//       (F(λ) = λ T F(1) T^{-1}, T = diag(1, λ, λ², ...)).
+//   EQ order J (modal 2x2 rotation blocks, kernels.hpp:286-306):
+//       Φ_p = e^{aΔt/ℓ} R(cΔt/ℓ),  dΦ/dℓ = -(Δt/ℓ) F Φ.
+//   Quasi-periodic harmonic j:  Φ_j = e^{-Δt/env} R(j ω0 Δt),
+//       Q_j = var q_j² (1 - e^{-2Δt/env}) I₂.
+// Q = Pinf - Φ Pinf Φ^T symmetrised exactly as the reference (:402-403), and
+// dQ by the reference's product rule (:419-423).  Step 0 (the anchor,
+// SPEC.md:326) is encoded as dt < 0: Φ := 0, so Q = Pinf and dQ = dPinf.
+//
+// Per-series parameters live in a flat record (built on the host, capi.cpp):
+//   rec[0] = sigma, rec[1] = jitter, rec[2 .. 2+nt) = d jitter / d theta,
+//   then one sub-record per leaf at desc.rec[l]:
+//     Matérn: var, len, lam
+//     EQ    : var, len                     (+ shared constants in desc.eqconst)
+//     QP    : var, len, period, env, w0, q2[0..J], dq2/dlen[0..J]
+#pragma once
+
+#include "devmat.cuh"
+#include "model_desc.h"
+
+namespace spingp_dev {
+
+// ------------------------------------------------------------------ Matérn --
+// Block of dimension D at offset o inside LD x LD arrays.
+template <int D, int LD>
+SP_DEV void matern_block(const double* lr, double dt, int o, double* Phi, double* Q) {
+    const double var = lr[0], lam = lr[2];
+    double P[D * D];
+    // Pinf (kernels.hpp:137-200)
+    if constexpr (D == 1) {
+        P[0] = var;
+    } else if constexpr (D == 2) {
+        P[0] = var; P[1] = 0.0; P[2] = 0.0; P[3] = var * lam * lam;
+    } else {
+        const double kap = lam * lam / 3.0;
+        P[0] = var; P[1] = 0.0; P[2] = -var * kap;
+        P[3] = 0.0; P[4] = var * kap; P[5] = 0.0;
+        P[6] = -var * kap; P[7] = 0.0; P[8] = var * lam * lam * lam * lam;
+    }
+    if (dt < 0.0) {
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                Phi[(o + i) * LD + o + j] = 0.0;
+                Q[(o + i) * LD + o + j] = P[i * D + j];
+            }
+        return;
+    }
+    // Φ = e^{-λΔt} (I + NΔt + N²Δt²/2), N = F + λI
+    const double e = exp(-lam * dt);
+    double ph[D * D];
+    if constexpr (D == 1) {
+        ph[0] = e;
+    } else if constexpr (D == 2) {
+        // N = [[λ, 1], [-λ², -λ]]
+        const double x = lam * dt;
+        ph[0] = e * (1.0 + x); ph[1] = e * dt;
+        ph[2] = -e * lam * x; ph[3] = e * (1.0 - x);
+    } else {
+        // N = [[λ,1,0],[0,λ,1],[-λ³,-3λ²,-2λ]]; N² = [[λ²,2λ,1],[-λ³,-2λ²,-λ],[λ⁴,λ³,λ²]]... computed generically
+        const double l2 = lam * lam, l3 = l2 * lam;
+        const double N[9] = {lam, 1.0, 0.0, 0.0, lam, 1.0, -l3, -3.0 * l2, -2.0 * lam};
+        double N2[9];
+        mm<3>(N2, N, N);
+        const double h = 0.5 * dt * dt;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) ph[k] = e * ((k % 4 == 0 ? 1.0 : 0.0) + dt * N[k] + h * N2[k]);
+    }
+    // Q = Pinf - Φ Pinf Φ^T (symmetrised)
+    double X[D * D], Y[D * D];
+    mm<D>(X, ph, P);
+    mmt<D>(Y, X, ph);
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            Phi[(o + i) * LD + o + j] = ph[i * D + j];
+            Q[(o + i) * LD + o + j] =
+                0.5 * ((P[i * D + j] - Y[i * D + j]) + (P[j * D + i] - Y[j * D + i]));
+        }
+}
+
+// g[var] += ½Tr(M dQ̃_var) ; g[len] += ½Tr(M dQ̃_len) + Tr(dΦ_len Bm)
+// (the jitter-derivative part ½ djit Tr(M) is added by the caller for every θ).
+template <int D, int LD>
+SP_DEV void matern_grad(const double* lr, double dt, int o, const double* Phi, const double* Q,
+                        const double* M, const double* Bm, double& gvar, double& glen) {
+    const double var = lr[0], len = lr[1], lam = lr[2];
+    double P[D * D], dP[D * D], ph[D * D], Mb[D * D], Bb[D * D], Qb[D * D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            ph[i * D + j] = Phi[(o + i) * LD + o + j];
+            Mb[i * D + j] = M[(o + i) * LD + o + j];
+            Bb[i * D + j] = Bm[(o + i) * LD + o + j];
+            Qb[i * D + j] = Q[(o + i) * LD + o + j];
+        }
+    if constexpr (D == 1) {
+        P[0] = var;
+    } else if constexpr (D == 2) {
+        P[0] = var; P[1] = 0.0; P[2] = 0.0; P[3] = var * lam * lam;
+    } else {
+        const double kap = lam * lam / 3.0;
+        P[0] = var; P[1] = 0.0; P[2] = -var * kap;
+        P[3] = 0.0; P[4] = var * kap; P[5] = 0.0;
+        P[6] = -var * kap; P[7] = 0.0; P[8] = var * lam * lam * lam * lam;
+    }
+    // d/dvar: dΦ = 0, dQ = Q / var (also at the anchor, where Q = Pinf)
+    gvar += 0.5 * mtrprod<D>(Mb, Qb) / var;
+    // d/dlen: dPinf_ij = -(i+j)/ℓ Pinf_ij
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) dP[i * D + j] = -double(i + j) / len * P[i * D + j];
+    if (dt < 0.0) {
+        glen += 0.5 * mtrprod<D>(Mb, dP);
+        return;
+    }
+    // dΦ = -(1/ℓ)[K, Φ] - (Δt/ℓ) F Φ
+    double F[D * D];
+    if constexpr (D == 1) {
+        F[0] = -lam;
+    } else if constexpr (D == 2) {
+        F[0] = 0.0; F[1] = 1.0; F[2] = -lam * lam; F[3] = -2.0 * lam;
+    } else {
+        F[0] = 0.0; F[1] = 1.0; F[2] = 0.0; F[3] = 0.0; F[4] = 0.0; F[5] = 1.0;
+        F[6] = -lam * lam * lam; F[7] = -3.0 * lam * lam; F[8] = -3.0 * lam;
+    }
+    double FP[D * D], dph[D * D];
+    mm<D>(FP, F, ph);
+    const double c1 = -1.0 / len, c2 = -dt / len;
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+            dph[i * D + j] = c1 * double(i - j) * ph[i * D + j] + c2 * FP[i * D + j];
+    // dQ = dP - dΦ P Φ^T - Φ dP Φ^T - Φ P dΦ^T   (symmetrised)
+    double X[D * D], Y[D * D], dQ[D * D];
+    mm<D>(X, dph, P);     // dΦ P
+    mmt<D>(Y, X, ph);     // dΦ P Φ^T
+    double Z[D * D], W[D * D];
+    mm<D>(Z, ph, dP);     // Φ dP
+    mmt<D>(W, Z, ph);     // Φ dP Φ^T
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+            dQ[i * D + j] = dP[i * D + j] - Y[i * D + j] - W[i * D + j] - Y[j * D + i];
+    msym<D>(dQ);
+    glen += 0.5 * mtrprod<D>(Mb, dQ) + mtrprod<D>(dph, Bb);
+}
+
+// ---------------------------------------------------------------------- EQ --
+// Generic-path only (dynamic offsets, LD = padded B).
+template <int LD>
+SP_DEV void eq_block(const ModelDesc& md, int l, const double* lr, double dt, double* Phi,
+                     double* Q) {
+    const int o = md.off[l], J = md.dim[l];
+    const double var = lr[0], len = lr[1];
+    const double* ac = md.eqconst + md.eqc[l];
+    const double* P1 = ac + J;  // J/2 pairs of (a, c), then P1
+    if (dt < 0.0) {
+        for (int i = 0; i < J; ++i)
+            for (int j = 0; j < J; ++j) {
+                Phi[(o + i) * LD + o + j] = 0.0;
+                Q[(o + i) * LD + o + j] = var * P1[i * J + j];
+            }
+        return;
+    }
+    for (int i = 0; i < J; ++i)
+        for (int j = 0; j < J; ++j) Phi[(o + i) * LD + o + j] = 0.0;
+    for (int p = 0; p < J / 2; ++p) {
+        const double a = ac[2 * p], c = ac[2 * p + 1];
+        const double rho = exp(a * dt / len);
+        double sn, cs;
+        sincos(c * dt / len, &sn, &cs);
+        const int k = o + 2 * p;
+        Phi[k * LD + k] = rho * cs;
+        Phi[k * LD + k + 1] = rho * sn;
+        Phi[(k + 1) * LD + k] = -rho * sn;
+        Phi[(k + 1) * LD + k + 1] = rho * cs;
+    }
+    // Q = var (P1 - Φ P1 Φ^T), Φ 2x2-block diagonal
+    for (int i = 0; i < J; ++i)
+        for (int j = 0; j <= i; ++j) {
+            const int pi = i & ~1, pj = j & ~1;
+            double s = 0.0;
+            for (int u = 0; u < 2; ++u)
+                for (int v = 0; v < 2; ++v)
+                    s += Phi[(o + i) * LD + o + pi + u] * P1[(pi + u) * J + pj + v] *
+                         Phi[(o + j) * LD + o + pj + v];
+            const double qij = var * (P1[i * J + j] - s);
+            const double qji = var * (P1[j * J + i] - s);
+            const double v = 0.5 * (qij + qji);
+            Q[(o + i) * LD + o + j] = v;
+            Q[(o + j) * LD + o + i] = v;
+        }
+}
+
+template <int LD>
+SP_DEV void eq_grad(const ModelDesc& md, int l, const double* lr, double dt, const double* Phi,
+                    const double* Q, const double* M, const double* Bm, double& gvar,
+                    double& glen) {
+    const int o = md.off[l], J = md.dim[l];
+    const double var = lr[0], len = lr[1];
+    const double* ac = md.eqconst + md.eqc[l];
+    const double* P1 = ac + J;
+    // var: dQ = Q / var
+    double s = 0.0;
+    for (int i = 0; i < J; ++i)
+        for (int k = 0; k < J; ++k) s += M[(o + i) * LD + o + k] * Q[(o + k) * LD + o + i];
+    gvar += 0.5 * s / var;
+    if (dt < 0.0) return;  // dPinf/dlen = 0 and dΦ = 0 at the anchor
+    // len: dΦ = -(Δt/ℓ) F Φ (2x2 blocks), dQ = -(dΦ P Φ^T + Φ P dΦ^T)
+    double tq = 0.0, tb = 0.0;
+    for (int p = 0; p < J / 2; ++p) {
+        const double a = ac[2 * p], c = ac[2 * p + 1];
+        const int k = o + 2 * p;
+        const double f00 = a / len, f01 = c / len, f10 = -c / len, f11 = a / len;
+        const double p00 = Phi[k * LD + k], p01 = Phi[k * LD + k + 1];
+        const double p10 = Phi[(k + 1) * LD + k], p11 = Phi[(k + 1) * LD + k + 1];
+        const double cdt = -dt / len;
+        const double d00 = cdt * (f00 * p00 + f01 * p10), d01 = cdt * (f00 * p01 + f01 * p11);
+        const double d10 = cdt * (f10 * p00 + f11 * p10), d11 = cdt * (f10 * p01 + f11 * p11);
+        tb += d00 * Bm[k * LD + k] + d01 * Bm[(k + 1) * LD + k] + d10 * Bm[k * LD + k + 1] +
+              d11 * Bm[(k + 1) * LD + k + 1];
+    }
+    // Tr(M dQ) with dQ = -var (dΦ P1 Φ^T + Φ P1 dΦ^T): both terms have equal trace
+    // against the symmetric M, so Tr(M dQ) = -2 var Tr(M dΦ P1 Φ^T).
+    for (int i = 0; i < J; ++i) {
+        const int pi = i & ~1;
+        for (int j = 0; j < J; ++j) {
+            const int pj = j & ~1;
+            // (dΦ P1 Φ^T)_{ij}
+            double v = 0.0;
+            for (int u = 0; u < 2; ++u) {
+                const int ku = o + pi + u;
+                const double a = ac[pi], c = ac[pi + 1];
+                const double fr0 = (i - pi == 0) ? a / len : -c / len;
+                const double fr1 = (i - pi == 0) ? c / len : a / len;
+                const double dph = -dt / len * (fr0 * Phi[(o + pi) * LD + ku] + fr1 * Phi[(o + pi + 1) * LD + ku]);
+                for (int w = 0; w < 2; ++w)
+                    v += dph * P1[(pi + u) * J + pj + w] * Phi[(o + j) * LD + o + pj + w];
+            }
+            tq += M[(o + j) * LD + o + i] * v;
+        }
+    }
+    glen += 0.5 * (-2.0 * var * tq) + tb;
+}
+
+// ---------------------------------------------------------------------- QP --
+template <int LD>
+SP_DEV void qp_block(const ModelDesc& md, int l, const double* lr, double dt, double* Phi,
+                     double* Q) {
+    const int o = md.off[l], J = md.order[l], d = md.dim[l];
+    const double var = lr[0], env = lr[3], w0 = lr[4];
+    const double* q2 = lr + 5;
+    for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j) {
+            Phi[(o + i) * LD + o + j] = 0.0;
+            Q[(o + i) * LD + o + j] = 0.0;
+        }
+    const double rho = dt < 0.0 ? 0.0 : exp(-dt / env);
+    const double one_m = dt < 0.0 ? 1.0 : -expm1(-2.0 * dt / env);
+    for (int j = 0; j <= J; ++j) {
+        const int k = o + 2 * j;
+        if (dt >= 0.0) {
+            double sn, cs;
+            sincos(double(j) * w0 * dt, &sn, &cs);
+            Phi[k * LD + k] = rho * cs;
+            Phi[k * LD + k + 1] = -rho * sn;
+            Phi[(k + 1) * LD + k] = rho * sn;
+            Phi[(k + 1) * LD + k + 1] = rho * cs;
+        }
+        const double qv = var * q2[j] * one_m;
+        Q[k * LD + k] = qv;
+        Q[(k + 1) * LD + k + 1] = qv;
+    }
+}
+
+// gradients w.r.t. (var, len, period, env) of one QP leaf
+template <int LD>
+SP_DEV void qp_grad(const ModelDesc& md, int l, const double* lr, double dt, const double* Phi,
+                    const double* M, const double* Bm, double* g4) {
+    const int o = md.off[l], J = md.order[l];
+    const double var = lr[0], period = lr[2], env = lr[3], w0 = lr[4];
+    const double* q2 = lr + 5;
+    const double* dq2 = lr + 5 + (J + 1);
+    const double rho2 = dt < 0.0 ? 0.0 : exp(-2.0 * dt / env);
+    const double one_m = dt < 0.0 ? 1.0 : -expm1(-2.0 * dt / env);
+    for (int j = 0; j <= J; ++j) {
+        const int k = o + 2 * j;
+        const double trM = M[k * LD + k] + M[(k + 1) * LD + k + 1];
+        g4[0] += 0.5 * trM * q2[j] * one_m;         // dQ/dvar = q2 (1 - ρ²) I
+        g4[1] += 0.5 * trM * var * dq2[j] * one_m;  // dQ/dlen = var dq2 (1 - ρ²) I
+        if (dt < 0.0) continue;
+        // env: dΦ = (Δt/env²) Φ ; dQ = -2 var q2 (Δt/env²) ρ² I
+        const double ce = dt / (env * env);
+        const double trPB = Phi[k * LD + k] * Bm[k * LD + k] + Phi[k * LD + k + 1] * Bm[(k + 1) * LD + k] +
+                            Phi[(k + 1) * LD + k] * Bm[k * LD + k + 1] +
+                            Phi[(k + 1) * LD + k + 1] * Bm[(k + 1) * LD + k + 1];
+        g4[3] += 0.5 * trM * (-2.0 * var * q2[j] * ce * rho2) + ce * trPB;
+        // period: dF = j dω [[0,-1],[1,0]], dω = -ω0/period; dΦ = Δt dF Φ; dQ = 0
+        const double s = double(j) * (-w0 / period) * dt;
+        // dΦ = s * [[-Φ10, -Φ11], [Φ00, Φ01]]
+        const double d00 = -s * Phi[(k + 1) * LD + k], d01 = -s * Phi[(k + 1) * LD + k + 1];
+        const double d10 = s * Phi[k * LD + k], d11 = s * Phi[k * LD + k + 1];
+        g4[2] += d00 * Bm[k * LD + k] + d01 * Bm[(k + 1) * LD + k] + d10 * Bm[k * LD + k + 1] +
+                 d11 * Bm[(k + 1) * LD + k + 1];
+    }
+}
+
+// ------------------------------------------------------------------ traits --
+// A Traits type provides B (block size of the instantiation), the emission row
+// and the two per-step model functions used by the elimination kernels.
+
+// Single Matérn leaf: everything in registers.
+template <int D>
+struct MaternTraits {
+    static constexpr int B = D;
+    SP_DEV static double H(const ModelDesc&, int i) { return i == 0 ? 1.0 : 0.0; }
+    SP_DEV static void step(const ModelDesc& md, const double* rec, double dt, double* Phi,
+                            double* Q) {
+        matern_block<D, D>(rec + md.rec[0], dt, 0, Phi, Q);
+    }
+    SP_DEV static void grad(const ModelDesc& md, const double* rec, double dt, const double* Phi,
+                            const double* Q, const double* M, const double* Bm, double* g) {
+        double gv = 0.0, gl = 0.0;
+        matern_grad<D, D>(rec + md.rec[0], dt, 0, Phi, Q, M, Bm, gv, gl);
+        const double hm = 0.5 * mtrace<D>(M);
+        g[0] += gv + hm * rec[2];
+        g[1] += gl + hm * rec[3];
+    }
+};
+
+// Any sum of leaves, padded to B (padding states: Φ = 0, Q = 1, H = 0 — exactly
+// decoupled, so results are identical to the unpadded system).
+template <int BB>
+struct GenericTraits {
+    static constexpr int B = BB;
+    SP_DEV static double H(const ModelDesc& md, int i) { return i < md.b ? md.H[i] : 0.0; }
+    SP_DEV static void step(const ModelDesc& md, const double* rec, double dt, double* Phi,
+                            double* Q) {
+        mzero<BB>(Phi);
+        mzero<BB>(Q);
+        for (int i = md.b; i < BB; ++i) Q[i * BB + i] = 1.0;  // padding
+        for (int l = 0; l < md.nleaves; ++l) {
+            const double* lr = rec + md.rec[l];
+            switch (md.type[l]) {
+                case MATERN12: matern_block<1, BB>(lr, dt, md.off[l], Phi, Q); break;
+                case MATERN32: matern_block<2, BB>(lr, dt, md.off[l], Phi, Q); break;
+                case MATERN52: matern_block<3, BB>(lr, dt, md.off[l], Phi, Q); break;
+                case EQ: eq_block<BB>(md, l, lr, dt, Phi, Q); break;
+                case QP: qp_block<BB>(md, l, lr, dt, Phi, Q); break;
+            }
+        }
+    }
+    SP_DEV static void grad(const ModelDesc& md, const double* rec, double dt, const double* Phi,
+                            const double* Q, const double* M, const double* Bm, double* g) {
+        double hm = 0.0;
+        for (int i = 0; i < md.b; ++i) hm += M[i * BB + i];
+        hm *= 0.5;
+        for (int l = 0; l < md.nleaves; ++l) {
+            const double* lr = rec + md.rec[l];
+            const int t0 = md.th[l];
+            double gv = 0.0, gl = 0.0;
+            switch (md.type[l]) {
+                case MATERN12: matern_grad<1, BB>(lr, dt, md.off[l], Phi, Q, M, Bm, gv, gl); break;
+                case MATERN32: matern_grad<2, BB>(lr, dt, md.off[l], Phi, Q, M, Bm, gv, gl); break;
+                case MATERN52: matern_grad<3, BB>(lr, dt, md.off[l], Phi, Q, M, Bm, gv, gl); break;
+                case EQ: eq_grad<BB>(md, l, lr, dt, Phi, Q, M, Bm, gv, gl); break;
+                case QP: {
+                    double g4[4] = {0.0, 0.0, 0.0, 0.0};
+                    qp_grad<BB>(md, l, lr, dt, Phi, M, Bm, g4);
+                    g[t0 + 2] += g4[2];
+                    g[t0 + 3] += g4[3];
+                    gv = g4[0];
+                    gl = g4[1];
+                    break;
+                }
+            }
+            g[t0] += gv;
+            g[t0 + 1] += gl;
+        }
+        for (int p = 0; p < md.nt; ++p) g[p] += hm * rec[2 + p];
+    }
+};
+
+}  // namespace spingp_dev

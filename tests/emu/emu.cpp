@@ -1,0 +1,201 @@
+// emu.cpp — host emulation of the product's evaluation and btd_core pipelines,
+// running the SAME kernel code (engine.cuh) on the CPU thread by thread.
+// TEST INFRASTRUCTURE ONLY: lets the CPU test suite check the device algorithm
+// (partitioned elimination, selected inverse, fused gradient) against the oracle
+// without a GPU.  The product never links this.
+#include "cuda_host_emu.h"
+
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../paper_1610_08035_b200/csrc/engine.cuh"
+#include "../../paper_1610_08035_b200/csrc/host_model.hpp"
+
+using namespace spingp_dev;
+using namespace spingp_host;
+
+namespace {
+
+std::string g_err;
+unsigned long long g_status;
+
+unsigned nblocks(long long n, int tpb) { return static_cast<unsigned>((n + tpb - 1) / tpb); }
+
+template <class T>
+void emu_eval(const HostModel& hm, const Plan& plan, std::vector<double>& params, const double* t,
+              const double* y, uint32_t flags, double* loglik, double* grad, double* mean, double* var) {
+    constexpr int B = T::B;
+    const Geom& g = plan.geo;
+    const int nt = hm.nt;
+    std::vector<double> eqc = hm.eqconst;
+    ModelDesc md = hm.desc;
+    md.eqconst = eqc.data();
+    std::vector<std::vector<double>> fac(g.nlev), rec(g.nlev), sol(g.nlev + 1);
+    for (int l = 0; l < g.nlev; ++l) {
+        const size_t SK = static_cast<size_t>(g.K[l]) * g.S;
+        fac[l].assign(static_cast<size_t>(g.m[l]) * Fac<B>::N * SK, 0.0);
+        rec[l].assign(Rec<B>::N * SK, 0.0);
+    }
+    for (int l = 1; l <= g.nlev; ++l) sol[l].assign(Sol<B>::N * static_cast<size_t>(g.n[l]) * g.S, 0.0);
+    std::vector<double> top(g.S, 0.0);
+    const long long SK0 = g.K[0] * g.S;
+    std::vector<double> part(static_cast<size_t>(P_GRAD + nt) * SK0, 0.0);
+    const int tpb = 32;
+    unsigned long long* st = &g_status;
+    emu_launch(nblocks(SK0, tpb), tpb, [&] {
+        k_fwd0<T>(md, params.data(), t, y, g, fac[0].data(), rec[0].data(), part.data(), st);
+    });
+    for (int l = 1; l < g.nlev; ++l) {
+        RecSource<B> src{rec[l - 1].data(), g.K[l - 1] * g.S, g.n[l]};
+        emu_launch(nblocks(g.K[l] * g.S, tpb), tpb,
+                   [&] { k_fwdL<B, RecSource<B>>(src, g, l, fac[l].data(), rec[l].data(), st); });
+    }
+    emu_launch(nblocks(g.S, tpb), tpb, [&] { k_top<B>(g, rec[g.nlev - 1].data(), sol[g.nlev].data(), top.data(), st); });
+    const bool gr = flags & 1u, needC = gr || (flags & 4u);
+    for (int l = g.nlev - 1; l >= 1; --l) {
+        RecSource<B> src{rec[l - 1].data(), g.K[l - 1] * g.S, g.n[l]};
+        SolSink<B> sink{sol[l].data(), g.n[l] * g.S, g.n[l]};
+        emu_launch(nblocks(g.K[l] * g.S, tpb), tpb, [&] {
+            k_revL<B, RecSource<B>, SolSink<B>>(src, sink, g, l, fac[l].data(), sol[l + 1].data(), needC ? 1 : 0);
+        });
+    }
+    Outs outs{(flags & 2u) ? mean : nullptr, (flags & 4u) ? var : nullptr, (flags & 8u) ? 1 : 0, gr ? 1 : 0,
+              needC ? 1 : 0};
+    emu_launch(nblocks(SK0, tpb), tpb, [&] {
+        k_rev0<T>(md, params.data(), t, y, g, fac[0].data(), sol[1].data(), part.data(), outs, st);
+    });
+    for (int s = 0; s < g.S; ++s) {
+        double acc[P_GRAD + kMaxTheta] = {};
+        for (int c = 0; c < P_GRAD + nt; ++c)
+            for (long long k = 0; k < g.K[0]; ++k) acc[c] += part[c * SK0 + s * g.K[0] + k];
+        double ld = acc[P_LOGDET] + top[s];
+        for (int l = 1; l < g.nlev; ++l)
+            for (long long k = 0; k < g.K[l]; ++k) ld += rec[l][Rec<B>::LOGDET * g.K[l] * g.S + s * g.K[l] + k];
+        const double* rp = params.data() + static_cast<size_t>(s) * hm.rec_stride;
+        const double sig = rp[0], s2 = sig * sig, nn = static_cast<double>(g.n[0]);
+        loglik[s] = -0.5 * (acc[P_FITY] + acc[P_FITE]) - 0.5 * (ld + acc[P_LDQ] + nn * std::log(s2)) -
+                    0.5 * nn * 1.8378770664093454835606594728112;
+        if (gr) {
+            for (int p = 0; p < nt; ++p) grad[s * (nt + 1) + p] = acc[P_GRAD + p];
+            grad[s * (nt + 1) + nt] = 2.0 * sig * (-0.5 * nn / s2 + acc[P_NOISE] / (2.0 * s2 * s2));
+        }
+    }
+}
+
+template <int B>
+void emu_btd(int64_t n, int b, const double* diag, const double* upper, const double* rhs, int k, int col,
+             double* x, double* cdiag, double* cupper, double* logdet, bool needC, int64_t m0) {
+    const Plan plan = make_plan(n, 1, B, m0);
+    const Geom& g = plan.geo;
+    std::vector<std::vector<double>> fac(g.nlev), rec(g.nlev), sol(g.nlev + 1);
+    for (int l = 0; l < g.nlev; ++l) {
+        fac[l].assign(static_cast<size_t>(g.m[l]) * Fac<B>::N * g.K[l], 0.0);
+        rec[l].assign(Rec<B>::N * g.K[l], 0.0);
+    }
+    for (int l = 1; l <= g.nlev; ++l) sol[l].assign(Sol<B>::N * static_cast<size_t>(g.n[l]), 0.0);
+    std::vector<double> top(1, 0.0);
+    unsigned long long* st = &g_status;
+    const int tpb = 32;
+    UserSource<B> usrc{diag, upper, rhs, n, b, k, col};
+    emu_launch(nblocks(g.K[0], tpb), tpb, [&] { k_fwdL<B, UserSource<B>>(usrc, g, 0, fac[0].data(), rec[0].data(), st); });
+    for (int l = 1; l < g.nlev; ++l) {
+        RecSource<B> src{rec[l - 1].data(), g.K[l - 1], g.n[l]};
+        emu_launch(nblocks(g.K[l], tpb), tpb, [&] { k_fwdL<B, RecSource<B>>(src, g, l, fac[l].data(), rec[l].data(), st); });
+    }
+    emu_launch(1, 1, [&] { k_top<B>(g, rec[g.nlev - 1].data(), sol[g.nlev].data(), top.data(), st); });
+    for (int l = g.nlev - 1; l >= 1; --l) {
+        RecSource<B> src{rec[l - 1].data(), g.K[l - 1], g.n[l]};
+        SolSink<B> sink{sol[l].data(), g.n[l], g.n[l]};
+        emu_launch(nblocks(g.K[l], tpb), tpb, [&] {
+            k_revL<B, RecSource<B>, SolSink<B>>(src, sink, g, l, fac[l].data(), sol[l + 1].data(), needC ? 1 : 0);
+        });
+    }
+    UserSink<B> usink{x, cdiag, cupper, b, k, col};
+    emu_launch(nblocks(g.K[0], tpb), tpb, [&] {
+        k_revL<B, UserSource<B>, UserSink<B>>(usrc, usink, g, 0, fac[0].data(), sol[1].data(), needC ? 1 : 0);
+    });
+    if (logdet) {
+        double ld = top[0];
+        for (int l = 0; l < g.nlev; ++l)
+            for (long long kk = 0; kk < g.K[l]; ++kk) ld += rec[l][Rec<B>::LOGDET * g.K[l] + kk];
+        *logdet = ld;
+    }
+}
+
+int finish() {
+    if (g_status == ~0ULL) return SPINGP_OK;
+    return static_cast<int>(g_status & 15ULL);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* emu_last_error(void) { return g_err.c_str(); }
+
+int emu_eval_batched(const spingp_leaf* leaves, int32_t n_leaves, const double* theta, int32_t n_theta,
+                     int64_t S, int64_t n, const double* t, const double* y, const double* sigma,
+                     uint32_t flags, double* loglik, double* grad, double* mean, double* var,
+                     int64_t* fail_block, int64_t m0, int force_generic) {
+    g_status = ~0ULL;
+    try {
+        const HostModel hm = build_model(leaves, n_leaves, n_theta);
+        const bool matern = hm.single_matern && !force_generic;
+        const int Bsz = matern ? hm.b : std::max(3, pad_b(hm.b));
+        const Plan plan = make_plan(n, S, Bsz, m0);
+        std::vector<double> params(static_cast<size_t>(S) * hm.rec_stride, 0.0);
+        for (int64_t s = 0; s < S; ++s) fill_record(hm, theta + s * n_theta, sigma[s], params.data() + s * hm.rec_stride);
+#define E(T) emu_eval<T>(hm, plan, params, t, y, flags, loglik, grad, mean, var)
+        if (matern) {
+            if (hm.b == 1) E(MaternTraits<1>);
+            else if (hm.b == 2) E(MaternTraits<2>);
+            else E(MaternTraits<3>);
+        } else {
+            switch (Bsz) {
+                case 3: E(GenericTraits<3>); break;
+                case 4: E(GenericTraits<4>); break;
+                case 6: E(GenericTraits<6>); break;
+                case 8: E(GenericTraits<8>); break;
+                case 12: E(GenericTraits<12>); break;
+                case 16: E(GenericTraits<16>); break;
+            }
+        }
+#undef E
+    } catch (const ApiError& e) {
+        g_err = e.what;
+        return e.status;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return SPINGP_BAD_ARG;
+    }
+    if (fail_block) *fail_block = g_status == ~0ULL ? -1 : static_cast<int64_t>(g_status >> 4);
+    return finish();
+}
+
+int emu_btd(int64_t n, int32_t b, const double* diag, const double* upper, const double* rhs, int32_t k,
+            double* x, double* cdiag, double* cupper, double* logdet, int64_t* fail_block, int64_t m0) {
+    g_status = ~0ULL;
+    const bool needC = cdiag != nullptr;
+    const int B = pad_b(b);
+    for (int col = 0; col < (k > 0 ? k : 1); ++col) {
+        double* ld = col == 0 ? logdet : nullptr;
+        const double* r = k > 0 ? rhs : nullptr;
+        double* xx = k > 0 ? x : nullptr;
+        switch (B) {
+            case 1: emu_btd<1>(n, b, diag, upper, r, k, col, xx, cdiag, cupper, ld, needC, m0); break;
+            case 2: emu_btd<2>(n, b, diag, upper, r, k, col, xx, cdiag, cupper, ld, needC, m0); break;
+            case 3: emu_btd<3>(n, b, diag, upper, r, k, col, xx, cdiag, cupper, ld, needC, m0); break;
+            case 4: emu_btd<4>(n, b, diag, upper, r, k, col, xx, cdiag, cupper, ld, needC, m0); break;
+            case 6: emu_btd<6>(n, b, diag, upper, r, k, col, xx, cdiag, cupper, ld, needC, m0); break;
+            case 8: emu_btd<8>(n, b, diag, upper, r, k, col, xx, cdiag, cupper, ld, needC, m0); break;
+            case 12: emu_btd<12>(n, b, diag, upper, r, k, col, xx, cdiag, cupper, ld, needC, m0); break;
+            case 16: emu_btd<16>(n, b, diag, upper, r, k, col, xx, cdiag, cupper, ld, needC, m0); break;
+        }
+    }
+    if (fail_block) *fail_block = g_status == ~0ULL ? -1 : static_cast<int64_t>(g_status >> 4);
+    return finish();
+}
+
+}  // extern "C"

@@ -1,0 +1,93 @@
+"""ctypes binding of the host emulation of the product kernels (tests/emu/).
+
+TEST INFRASTRUCTURE ONLY.  Runs the exact kernel code of
+paper_1610_08035_b200/csrc/engine.cuh on the CPU so the CPU suite can check the
+partitioned-elimination algorithm against the oracle without a GPU.
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB_PATH = os.path.join(ROOT, "tests", "emu", "build", "libspingp_emu.so")
+_d = ctypes.POINTER(ctypes.c_double)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_lib = None
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "emu")], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(LIB_PATH)
+        L.emu_last_error.restype = ctypes.c_char_p
+        L.emu_eval_batched.argtypes = [ctypes.c_void_p, ctypes.c_int32, _d, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
+                                       _d, _d, _d, ctypes.c_uint32, _d, _d, _d, _d, _i64p, ctypes.c_int64, ctypes.c_int]
+        L.emu_btd.argtypes = [ctypes.c_int64, ctypes.c_int32, _d, _d, _d, ctypes.c_int32, _d, _d, _d, _d, _i64p,
+                              ctypes.c_int64]
+        _lib = L
+    return _lib
+
+
+class EmuError(RuntimeError):
+    def __init__(self, status, block, msg):
+        super().__init__(f"emu status {status} block {block}: {msg}")
+        self.status, self.block = status, block
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(_d)
+
+
+def _leaves(leaves):
+    arr = np.zeros(2 * len(leaves), dtype=np.int32)
+    for i, lf in enumerate(leaves):
+        typ, order = (lf, 0) if isinstance(lf, (int, np.integer)) else lf
+        arr[2 * i], arr[2 * i + 1] = typ, order
+    return arr
+
+
+def evaluate(leaves, theta, t, y, sigma, grad=True, mean=True, var=True, include_noise=False, m0=0, force_generic=False):
+    t = np.ascontiguousarray(np.atleast_2d(t), dtype=np.float64)
+    y = np.ascontiguousarray(np.atleast_2d(y), dtype=np.float64)
+    S, n = t.shape
+    th = np.ascontiguousarray(np.atleast_2d(theta), dtype=np.float64)
+    th = np.ascontiguousarray(np.broadcast_to(th, (S, th.shape[1])))
+    sg = np.ascontiguousarray(np.broadcast_to(np.asarray(sigma, dtype=np.float64), (S,)))
+    flags = (1 if grad else 0) | (2 if mean else 0) | (4 if var else 0) | (8 if include_noise else 0)
+    ll = np.zeros(S); g = np.zeros((S, th.shape[1] + 1)); mu = np.zeros((S, n)); v = np.zeros((S, n))
+    fb = ctypes.c_int64()
+    lv = _leaves(leaves)
+    st = lib().emu_eval_batched(lv.ctypes.data, len(leaves), _p(th), th.shape[1], S, n, _p(t), _p(y), _p(sg), flags,
+                                _p(ll), _p(g), _p(mu), _p(v), ctypes.byref(fb), int(m0), int(force_generic))
+    if st:
+        raise EmuError(st, fb.value, lib().emu_last_error().decode())
+    if S == 1:
+        return dict(loglik=ll[0], grad=g[0] if grad else None, mean=mu[0] if mean else None, var=v[0] if var else None)
+    return dict(loglik=ll, grad=g if grad else None, mean=mu if mean else None, var=v if var else None)
+
+
+def btd(diag, upper, rhs=None, selinv=False, m0=0):
+    diag = np.ascontiguousarray(diag, dtype=np.float64)
+    n, b, _ = diag.shape
+    upper = np.ascontiguousarray(upper if n > 1 else np.zeros((1, b, b)), dtype=np.float64)
+    k = 0
+    x = None
+    if rhs is not None:
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64).reshape(n * b, -1)
+        k = rhs.shape[1]
+        x = np.zeros_like(rhs)
+    cd = np.zeros_like(diag) if selinv else None
+    cu = np.zeros((max(n - 1, 1), b, b)) if selinv else None
+    ld = ctypes.c_double(); fb = ctypes.c_int64()
+    st = lib().emu_btd(n, b, _p(diag), _p(upper), _p(rhs), k, _p(x), _p(cd), _p(cu), ctypes.byref(ld), ctypes.byref(fb),
+                       int(m0))
+    if st:
+        raise EmuError(st, fb.value, "btd failure")
+    return dict(x=x, cdiag=cd, cupper=None if cu is None else cu[:n - 1], logdet=ld.value)
