@@ -235,4 +235,113 @@ SP_UNROLL
         }
 }
 
+// ---- triangular-factor forms (the numerically preferred route) -------------
+// Li = L^{-1} for lower-triangular L (Li lower, zero upper).
+template <int B>
+SP_DEV void tri_inverse(double* Li, const double* L) {
+SP_UNROLL
+    for (int j = 0; j < B; ++j) {
+        const double dj = 1.0 / L[j * B + j];
+SP_UNROLL
+        for (int i = 0; i < B; ++i) {
+            if (i < j) {
+                Li[i * B + j] = 0.0;
+            } else if (i == j) {
+                Li[i * B + j] = dj;
+            } else {
+                double s = L[i * B + j] * dj;
+SP_UNROLL
+                for (int k = j + 1; k < i; ++k) s = fma(L[i * B + k], Li[k * B + j], s);
+                Li[i * B + j] = -s / L[i * B + i];
+            }
+        }
+    }
+}
+// C = Li A   (Li lower triangular)
+template <int B>
+SP_DEV void lmul(double* C, const double* Li, const double* A) {
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j < B; ++j) {
+            double s = 0.0;
+SP_UNROLL
+            for (int k = 0; k <= i; ++k) s = fma(Li[i * B + k], A[k * B + j], s);
+            C[i * B + j] = s;
+        }
+}
+// C = Li^T A   (Li lower triangular)
+template <int B>
+SP_DEV void ltmul(double* C, const double* Li, const double* A) {
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j < B; ++j) {
+            double s = 0.0;
+SP_UNROLL
+            for (int k = i; k < B; ++k) s = fma(Li[k * B + i], A[k * B + j], s);
+            C[i * B + j] = s;
+        }
+}
+// y = Li x ; y = Li^T x
+template <int B>
+SP_DEV void lmv(double* y, const double* Li, const double* x) {
+SP_UNROLL
+    for (int i = 0; i < B; ++i) {
+        double s = 0.0;
+SP_UNROLL
+        for (int k = 0; k <= i; ++k) s = fma(Li[i * B + k], x[k], s);
+        y[i] = s;
+    }
+}
+template <int B>
+SP_DEV void ltmv(double* y, const double* Li, const double* x) {
+SP_UNROLL
+    for (int i = 0; i < B; ++i) {
+        double s = 0.0;
+SP_UNROLL
+        for (int k = i; k < B; ++k) s = fma(Li[k * B + i], x[k], s);
+        y[i] = s;
+    }
+}
+// C = Li^T X Li for symmetric X (result symmetric)
+template <int B>
+SP_DEV void sandwich(double* C, const double* Li, const double* X) {
+    double T[B * B];
+    // T = X Li
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j < B; ++j) {
+            double s = 0.0;
+SP_UNROLL
+            for (int k = j; k < B; ++k) s = fma(X[i * B + k], Li[k * B + j], s);
+            T[i * B + j] = s;
+        }
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j <= i; ++j) {
+            double s = 0.0;
+SP_UNROLL
+            for (int k = i; k < B; ++k) s = fma(Li[k * B + i], T[k * B + j], s);
+            C[i * B + j] = s;
+            C[j * B + i] = s;
+        }
+}
+// C = Li^T Li = (L L^T)^{-1}
+template <int B>
+SP_DEV void ltl(double* C, const double* Li) {
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j <= i; ++j) {
+            double s = 0.0;
+SP_UNROLL
+            for (int k = i; k < B; ++k) s = fma(Li[k * B + i], Li[k * B + j], s);
+            C[i * B + j] = s;
+            C[j * B + i] = s;
+        }
+}
+
 }  // namespace spingp_dev

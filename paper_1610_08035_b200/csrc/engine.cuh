@@ -72,12 +72,14 @@ struct Rec {
     static constexpr int N = 3 * B * B + 2 * B + 1;
 };
 // per-step factor layout: fac[(jj * NF + comp) * SK + chunk]
+//   LI: L_j^{-1} packed lower (row-major), Y: L_j^{-1} W_j, Z: L_j^{-1} r_j
 template <int B>
 struct Fac {
-    static constexpr int SINV = 0;
-    static constexpr int V = B * B;
-    static constexpr int H = 2 * B * B;
-    static constexpr int N = 2 * B * B + B;
+    static constexpr int NLI = B * (B + 1) / 2;
+    static constexpr int LI = 0;
+    static constexpr int Y = NLI;
+    static constexpr int Z = NLI + B * B;
+    static constexpr int N = NLI + B * B + B;
 };
 // solution layout at level >= 1: sol[comp * Sn + block]
 template <int B>
@@ -92,9 +94,9 @@ enum Part { P_LOGDET = 0, P_FITY = 1, P_FITE = 2, P_LDQ = 3, P_NOISE = 4, P_GRAD
 
 template <int B>
 struct ElimState {
-    double T[B * B];
-    double rc[B];
-    double W[B * B];
+    double T[B * B];    // carried Schur update X^T X for the next block
+    double rc[B];       // carried rhs update X^T z
+    double W[B * B];    // coupling of the current block with the left separator
     double accLL[B * B];
     double accrL[B];
     double logdet;
@@ -110,7 +112,11 @@ SP_DEV void elim_init(ElimState<B>& es) {
     es.logdet = 0.0;
 }
 
-// Eliminate one interior block; stores S^{-1}, V, h at fp[comp * SK].
+// Eliminate one interior block j with diagonal D, coupling U (to j+1) and rhs.
+// With S = D - T = L L^T and Li = L^{-1}:  X = Li U, Y = Li W, z = Li r.
+// Schur updates in Gram form (symmetric PSD by construction):
+//   T' = X^T X,  rc' = X^T z,  W' = -X^T Y,  accLL -= Y^T Y,  accrL -= Y^T z.
+// Stores Li (packed), Y and z at fp[comp * SK] for the reverse sweep.
 template <int B>
 SP_DEV bool elim_block(ElimState<B>& es, const double* D, const double* U, const double* rhs,
                        bool hasL, double* fp, long long SK) {
@@ -121,36 +127,39 @@ SP_UNROLL
     double L[B * B], ld;
     if (!chol<B>(L, S, ld)) return false;
     es.logdet += ld;
-    double Si[B * B];
-    chol_inverse<B>(Si, L);
-    double r[B], h[B];
+    double Li[B * B];
+    tri_inverse<B>(Li, L);
+    double r[B], z[B];
 SP_UNROLL
     for (int i = 0; i < B; ++i) r[i] = rhs[i] - es.rc[i];
-    mv<B>(h, Si, r);
-    double G[B * B];
-    mm<B>(G, Si, U);
+    lmv<B>(z, Li, r);
+    double X[B * B];
+    lmul<B>(X, Li, U);
     if (hasL) {
-        double V[B * B], X[B * B];
-        mm<B>(V, Si, es.W);
-        mtm_sym<B>(X, es.W, V);
+        double Y[B * B], G[B * B];
+        lmul<B>(Y, Li, es.W);
+        mtm_sym<B>(G, Y, Y);
 SP_UNROLL
-        for (int i = 0; i < B * B; ++i) es.accLL[i] -= X[i];
-        double wh[B];
-        mtv<B>(wh, es.W, h);
+        for (int i = 0; i < B * B; ++i) es.accLL[i] -= G[i];
+        double yz[B];
+        mtv<B>(yz, Y, z);
 SP_UNROLL
-        for (int i = 0; i < B; ++i) es.accrL[i] -= wh[i];
-        mtm<B>(X, U, V);
+        for (int i = 0; i < B; ++i) es.accrL[i] -= yz[i];
+        mtm<B>(G, X, Y);
 SP_UNROLL
-        for (int i = 0; i < B * B; ++i) es.W[i] = -X[i];
+        for (int i = 0; i < B * B; ++i) es.W[i] = -G[i];
 SP_UNROLL
-        for (int i = 0; i < B * B; ++i) fp[(Fac<B>::V + i) * SK] = V[i];
+        for (int i = 0; i < B * B; ++i) fp[(Fac<B>::Y + i) * SK] = Y[i];
     }
-    mtm_sym<B>(es.T, U, G);
-    mtv<B>(es.rc, U, h);
+    mtm_sym<B>(es.T, X, X);
+    mtv<B>(es.rc, X, z);
+    int q = 0;
 SP_UNROLL
-    for (int i = 0; i < B * B; ++i) fp[(Fac<B>::SINV + i) * SK] = Si[i];
+    for (int i = 0; i < B; ++i)
 SP_UNROLL
-    for (int i = 0; i < B; ++i) fp[(Fac<B>::H + i) * SK] = h[i];
+        for (int j = 0; j <= i; ++j) fp[(Fac<B>::LI + q++) * SK] = Li[i * B + j];
+SP_UNROLL
+    for (int i = 0; i < B; ++i) fp[(Fac<B>::Z + i) * SK] = z[i];
     return true;
 }
 
@@ -174,9 +183,9 @@ SP_UNROLL
     r[Rec<B>::LOGDET * SK] = es.logdet;
 }
 
-// Q̃ = Q + jit I -> Q̃^{-1} (and its log-determinant).
+// Q̃ = Q + jit I = L_Q L_Q^T  ->  Mq = L_Q^{-1} (and log det Q̃).
 template <int B>
-SP_DEV bool qt_inverse(const double* Q, double jit, int breal, double* Qinv, double* ldq) {
+SP_DEV bool qt_factor(const double* Q, double jit, int breal, double* Mq, double* ldq) {
     double Qt[B * B], L[B * B];
 SP_UNROLL
     for (int i = 0; i < B * B; ++i) Qt[i] = Q[i];
@@ -187,8 +196,27 @@ SP_UNROLL
     if (ldq) ok = chol<B>(L, Qt, *ldq);
     else ok = chol_nolog<B>(L, Qt);
     if (!ok) return false;
-    chol_inverse<B>(Qinv, L);
+    tri_inverse<B>(Mq, L);
     return true;
+}
+
+// Assembly pieces from one step: with Z = Mq Φ,
+//   Φ^T Q̃^{-1} Φ = Z^T Z  and  U = -Φ^T Q̃^{-1} = -Z^T Mq.
+template <int B>
+SP_DEV void step_assembly(const double* Phi, const double* Mq, double* PQP, double* U) {
+    double Z[B * B];
+    lmul<B>(Z, Mq, Phi);
+    mtm_sym<B>(PQP, Z, Z);
+    // U = -Z^T Mq
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j < B; ++j) {
+            double s = 0.0;
+SP_UNROLL
+            for (int k = j; k < B; ++k) s = fma(Z[k * B + i], Mq[k * B + j], s);
+            U[i * B + j] = -s;
+        }
 }
 
 // ======================================================= level 0 (fused) ======
@@ -216,7 +244,7 @@ __global__ void __launch_bounds__(128) k_fwd0(ModelDesc md, const double* __rest
     const long long gbase = static_cast<long long>(s) * n;
     const bool hasL = c > 0;
 
-    double Phi[B * B], Q[B * B], Qinv[B * B];
+    double Phi[B * B], Q[B * B], Mq[B * B];
     double dt = -1.0;
     if (st > 0) {
         dt = ts[st] - ts[st - 1];
@@ -226,16 +254,21 @@ __global__ void __launch_bounds__(128) k_fwd0(ModelDesc md, const double* __rest
         }
     }
     T::step(md, rp, dt, Phi, Q);
-    if (!qt_inverse<B>(Q, jit, md.b, Qinv, nullptr)) {
+    if (!qt_factor<B>(Q, jit, md.b, Mq, nullptr)) {
         report(status, gbase + st, ST_SINGULAR_Q);
         return;
     }
+    double Qinv[B * B];  // Q̃_j^{-1} of the current block
+    ltl<B>(Qinv, Mq);
     ElimState<B> es;
     elim_init<B>(es);
-    if (hasL) {  // P_{s, s-1} = U_{s-1}^T = -Q̃_s^{-1} Φ_s
-        mm<B>(es.W, Qinv, Phi);
+    if (hasL) {  // P_{s, s-1} = U_{s-1}^T
+        double PQP[B * B], U[B * B];
+        step_assembly<B>(Phi, Mq, PQP, U);
 SP_UNROLL
-        for (int i = 0; i < B * B; ++i) es.W[i] = -es.W[i];
+        for (int i = 0; i < B; ++i)
+SP_UNROLL
+            for (int j = 0; j < B; ++j) es.W[i * B + j] = U[j * B + i];
     }
     double HH[B * B];
 SP_UNROLL
@@ -249,21 +282,16 @@ SP_UNROLL
             report(status, gbase + j + 1, dtn == 0.0 ? ST_DUPLICATE : ST_BAD_ARG);
             return;
         }
-        double Phn[B * B], Qn[B * B], Qinvn[B * B];
+        double Phn[B * B], Qn[B * B], Mqn[B * B];
         T::step(md, rp, dtn, Phn, Qn);
-        if (!qt_inverse<B>(Qn, jit, md.b, Qinvn, nullptr)) {
+        if (!qt_factor<B>(Qn, jit, md.b, Mqn, nullptr)) {
             report(status, gbase + j + 1, ST_SINGULAR_Q);
             return;
         }
-        double PtQ[B * B], D[B * B], U[B * B], r[B];
-        mtm<B>(PtQ, Phn, Qinvn);
-        mm<B>(D, PtQ, Phn);
-        msym<B>(D);
+        double D[B * B], U[B * B], r[B];
+        step_assembly<B>(Phn, Mqn, D, U);
 SP_UNROLL
-        for (int i = 0; i < B * B; ++i) {
-            D[i] += Qinv[i] + HH[i];
-            U[i] = -PtQ[i];
-        }
+        for (int i = 0; i < B * B; ++i) D[i] += Qinv[i] + HH[i];
         const double yj = ys[j];
         if (!isfinite(yj)) {
             report(status, gbase + j, ST_BAD_ARG);
@@ -276,7 +304,7 @@ SP_UNROLL
             report(status, gbase + j, ST_NOT_PD);
             return;
         }
-        mcopy<B>(Qinv, Qinvn);
+        ltl<B>(Qinv, Mqn);
     }
     // separator R = en - 1
     double D[B * B], Rr[B];
@@ -288,17 +316,15 @@ SP_UNROLL
             report(status, gbase + en, dte == 0.0 ? ST_DUPLICATE : ST_BAD_ARG);
             return;
         }
-        double Phn[B * B], Qn[B * B], Qinvn[B * B], PtQ[B * B], X[B * B];
+        double Phn[B * B], Qn[B * B], Mqn[B * B], PQP[B * B], U[B * B];
         T::step(md, rp, dte, Phn, Qn);
-        if (!qt_inverse<B>(Qn, jit, md.b, Qinvn, nullptr)) {
+        if (!qt_factor<B>(Qn, jit, md.b, Mqn, nullptr)) {
             report(status, gbase + en, ST_SINGULAR_Q);
             return;
         }
-        mtm<B>(PtQ, Phn, Qinvn);
-        mm<B>(X, PtQ, Phn);
-        msym<B>(X);
+        step_assembly<B>(Phn, Mqn, PQP, U);
 SP_UNROLL
-        for (int i = 0; i < B * B; ++i) D[i] += X[i];
+        for (int i = 0; i < B * B; ++i) D[i] += PQP[i];
     }
     const double yR = ys[en - 1];
     if (!isfinite(yR)) {
@@ -416,7 +442,7 @@ __global__ void k_top(Geom geo, const double* __restrict__ rec, double* __restri
     if (s >= geo.S) return;
     const int L = geo.nlev;
     const long long SK = geo.S;  // K = 1 at the last level
-    double D[B * B], r[B], Lc[B * B], C[B * B], x[B], ld;
+    double D[B * B], r[B], Lc[B * B], Li[B * B], C[B * B], x[B], z[B], ld;
 SP_UNROLL
     for (int q = 0; q < B * B; ++q) D[q] = rec[(Rec<B>::RDIAG + q) * SK + s];
 SP_UNROLL
@@ -426,8 +452,10 @@ SP_UNROLL
         report(status, static_cast<long long>(s) * geo.n[0] + to_global(geo, L, 0), ST_NOT_PD);
         return;
     }
-    chol_inverse<B>(C, Lc);
-    mv<B>(x, C, r);
+    tri_inverse<B>(Li, Lc);
+    ltl<B>(C, Li);
+    lmv<B>(z, Li, r);
+    ltmv<B>(x, Li, z);
     const long long Sn = geo.S;
 SP_UNROLL
     for (int q = 0; q < B; ++q) sol[(Sol<B>::X + q) * Sn + s] = x[q];
@@ -446,9 +474,12 @@ SP_DEV void load_sep(const double* solU, long long SnU, long long iR, bool hasL,
                      SepData<B>& sd) {
 SP_UNROLL
     for (int q = 0; q < B; ++q) sd.xR[q] = solU[(Sol<B>::X + q) * SnU + iR];
-    if (needC)
+    if (needC) {
 SP_UNROLL
         for (int q = 0; q < B * B; ++q) sd.CRR[q] = solU[(Sol<B>::CD + q) * SnU + iR];
+    } else {
+        mzero<B>(sd.CRR);
+    }
     if (hasL) {
 SP_UNROLL
         for (int q = 0; q < B; ++q) sd.xL[q] = solU[(Sol<B>::X + q) * SnU + iR - 1];
@@ -457,67 +488,78 @@ SP_UNROLL
             for (int q = 0; q < B * B; ++q) sd.CLL[q] = solU[(Sol<B>::CD + q) * SnU + iR - 1];
 SP_UNROLL
             for (int q = 0; q < B * B; ++q) sd.CLR[q] = solU[(Sol<B>::CU + q) * SnU + iR - 1];
+            return;
         }
     } else {
         vzero<B>(sd.xL);
-        mzero<B>(sd.CLL);
-        mzero<B>(sd.CLR);
     }
+    mzero<B>(sd.CLL);
+    mzero<B>(sd.CLR);
 }
 
-// One step of the reverse sweep: given S^{-1}, V, h, G of block j and the carried
-// (x_n, C_nn, C_nL) of block n = j+1, produce x_j (and C_jL, C_jn, C_jj).
+// One step of the reverse sweep.  With x_j = L^{-T}(z - X x_n - Y x_L) + ε_j,
+// Cov ε_j = S_j^{-1} = L^{-T} L^{-1}:
+//   P1 = X C_nL + Y C_LL,   C_jL = -L^{-T} P1
+//   P2 = X C_nn + Y C_Ln,   C_jn = -L^{-T} P2
+//   C_jj = L^{-T} (I + P2 X^T + P1 Y^T) L^{-1}
 template <int B>
-SP_DEV void back_step(const double* Si, const double* V, const double* h, const double* G,
+SP_DEV void back_step(const double* Li, const double* Y, const double* z, const double* X,
                       bool hasL, bool needC, const SepData<B>& sd, const double* xn,
                       const double* Cnn, const double* CnL, double* xj, double* CjL, double* Cjn,
                       double* Cjj) {
-    double tmp[B];
-    mv<B>(xj, G, xn);
+    double a[B], tmp[B];
+    mv<B>(tmp, X, xn);
 SP_UNROLL
-    for (int i = 0; i < B; ++i) xj[i] = h[i] - xj[i];
+    for (int i = 0; i < B; ++i) a[i] = z[i] - tmp[i];
     if (hasL) {
-        mv<B>(tmp, V, sd.xL);
+        mv<B>(tmp, Y, sd.xL);
 SP_UNROLL
-        for (int i = 0; i < B; ++i) xj[i] -= tmp[i];
+        for (int i = 0; i < B; ++i) a[i] -= tmp[i];
     }
+    ltmv<B>(xj, Li, a);
     if (!needC) return;
-    double X[B * B];
-    mm<B>(CjL, G, CnL);
-    mm<B>(Cjn, G, Cnn);
+    double P1[B * B], P2[B * B], M[B * B], N[B * B];
+    mm<B>(P1, X, CnL);
+    mm<B>(P2, X, Cnn);
     if (hasL) {
-        mm<B>(X, V, sd.CLL);
+        mm<B>(M, Y, sd.CLL);
 SP_UNROLL
-        for (int i = 0; i < B * B; ++i) CjL[i] += X[i];
-        mmt<B>(X, V, CnL);  // V C_{L,n} = V C_{n,L}^T
+        for (int i = 0; i < B * B; ++i) P1[i] += M[i];
+        mmt<B>(M, Y, CnL);  // Y C_{L,n} = Y C_{n,L}^T
 SP_UNROLL
-        for (int i = 0; i < B * B; ++i) Cjn[i] += X[i];
+        for (int i = 0; i < B * B; ++i) P2[i] += M[i];
     }
+    ltmul<B>(CjL, Li, P1);
+    ltmul<B>(Cjn, Li, P2);
 SP_UNROLL
     for (int i = 0; i < B * B; ++i) {
         CjL[i] = -CjL[i];
         Cjn[i] = -Cjn[i];
     }
-    mmt<B>(Cjj, Cjn, G);
-SP_UNROLL
-    for (int i = 0; i < B * B; ++i) Cjj[i] = Si[i] - Cjj[i];
+    mmt<B>(M, P2, X);
     if (hasL) {
-        mmt<B>(X, CjL, V);
+        mmt<B>(N, P1, Y);
 SP_UNROLL
-        for (int i = 0; i < B * B; ++i) Cjj[i] -= X[i];
+        for (int i = 0; i < B * B; ++i) M[i] += N[i];
     }
-    msym<B>(Cjj);
+SP_UNROLL
+    for (int i = 0; i < B; ++i) M[i * B + i] += 1.0;
+    msym<B>(M);
+    sandwich<B>(Cjj, Li, M);
 }
 
 template <int B>
-SP_DEV void load_fac(const double* fp, long long SK, bool hasL, double* Si, double* V, double* h) {
+SP_DEV void load_fac(const double* fp, long long SK, bool hasL, double* Li, double* Y, double* z) {
+    int q = 0;
 SP_UNROLL
-    for (int i = 0; i < B * B; ++i) Si[i] = fp[(Fac<B>::SINV + i) * SK];
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j < B; ++j) Li[i * B + j] = j <= i ? fp[(Fac<B>::LI + q++) * SK] : 0.0;
     if (hasL)
 SP_UNROLL
-        for (int i = 0; i < B * B; ++i) V[i] = fp[(Fac<B>::V + i) * SK];
+        for (int i = 0; i < B * B; ++i) Y[i] = fp[(Fac<B>::Y + i) * SK];
 SP_UNROLL
-    for (int i = 0; i < B; ++i) h[i] = fp[(Fac<B>::H + i) * SK];
+    for (int i = 0; i < B; ++i) z[i] = fp[(Fac<B>::Z + i) * SK];
 }
 
 // Solution sinks for the reverse sweep of levels >= 1.
@@ -585,12 +627,12 @@ SP_UNROLL
         for (int j = 0; j < B; ++j) CnL[i * B + j] = sd.CLR[j * B + i];
     sink.put(s, en - 1, xn, Cnn, needC);
     for (long long j = en - 2; j >= st; --j) {
-        double Si[B * B], V[B * B], h[B], U[B * B], G[B * B];
-        load_fac<B>(fac + (j - st) * Fac<B>::N * SK + g, SK, hasL, Si, V, h);
+        double Li[B * B], Y[B * B], z[B], U[B * B], X[B * B];
+        load_fac<B>(fac + (j - st) * Fac<B>::N * SK + g, SK, hasL, Li, Y, z);
         src.upper(s, j, U);
-        mm<B>(G, Si, U);
+        lmul<B>(X, Li, U);
         double xj[B], CjL[B * B], Cjn[B * B], Cjj[B * B];
-        back_step<B>(Si, V, h, G, hasL, needC, sd, xn, Cnn, CnL, xj, CjL, Cjn, Cjj);
+        back_step<B>(Li, Y, z, X, hasL, needC, sd, xn, Cnn, CnL, xj, CjL, Cjn, Cjj);
         sink.put(s, j, xj, Cjj, needC);
         if (needC) sink.put_upper(s, j, Cjn);
 SP_UNROLL
@@ -646,11 +688,16 @@ SP_UNROLL
     }
 }
 
-// Likelihood / gradient terms of step i with transition Φ (Φ := 0 at the anchor),
-// previous block (xp, Cpp) and cross-covariance Cpc = C_{i-1,i}.
+// Likelihood / gradient terms of step i with transition Φ
+// (Φ := 0 at the anchor), Mq = L_Q̃^{-1}, previous block (xp, Cpp) and
+// cross-covariance Cpc = C_{i-1,i}:
+//   ē = x_c - Φ x_p,  fe += |Mq ē|²
+//   E = C_cc - Φ C_pc - (Φ C_pc)^T + Φ C_pp Φ^T + ē ē^T
+//   Zc = C_pc - C_pp Φ^T + x_p ē^T
+//   M = Q̃^{-1}(E - Q̃)Q̃^{-1},  Bm = Zc Q̃^{-1};  T::grad adds ½Tr(M dQ̃) + Tr(dΦ Bm).
 template <class T>
 SP_DEV void step_terms(const ModelDesc& md, const double* rp, double dt, const double* Phi,
-                       const double* Qraw, const double* Qinv, const double* xc, const double* Ccc,
+                       const double* Qraw, const double* Mq, const double* xc, const double* Ccc,
                        const double* xp, const double* Cpp, const double* Cpc, bool anchor,
                        bool grad, double& fe, double* g) {
     constexpr int B = T::B;
@@ -663,12 +710,13 @@ SP_UNROLL
 SP_UNROLL
         for (int i = 0; i < B; ++i) e[i] = xc[i] - tmp[i];
     }
-    mv<B>(tmp, Qinv, e);
+    lmv<B>(tmp, Mq, e);
     double q = 0.0;
 SP_UNROLL
-    for (int i = 0; i < B; ++i) q += e[i] * tmp[i];
+    for (int i = 0; i < B; ++i) q += tmp[i] * tmp[i];
     fe += q;
     if (!grad) return;
+    const double jit = rp[1];
     double E[B * B], Bm[B * B], X[B * B], Y[B * B];
     if (anchor) {
 SP_UNROLL
@@ -677,30 +725,62 @@ SP_UNROLL
             for (int j = 0; j < B; ++j) E[i * B + j] = Ccc[i * B + j] + e[i] * e[j];
         mzero<B>(Bm);
     } else {
-        // E = C_cc - Φ C_pc - (Φ C_pc)^T + Φ C_pp Φ^T + e e^T
+        double Z[B * B];
         mm<B>(X, Phi, Cpc);
         mm<B>(Y, Phi, Cpp);
-        double Z[B * B];
         mmt<B>(Z, Y, Phi);
 SP_UNROLL
         for (int i = 0; i < B; ++i)
 SP_UNROLL
             for (int j = 0; j < B; ++j)
                 E[i * B + j] = Ccc[i * B + j] - X[i * B + j] - X[j * B + i] + Z[i * B + j] + e[i] * e[j];
-        // Z_i = C_pc - C_pp Φ^T + x_p e^T ;  Bm = Z Q̃^{-1}
         mmt<B>(Y, Cpp, Phi);
 SP_UNROLL
         for (int i = 0; i < B; ++i)
 SP_UNROLL
             for (int j = 0; j < B; ++j) Z[i * B + j] = Cpc[i * B + j] - Y[i * B + j] + xp[i] * e[j];
-        mm<B>(Bm, Z, Qinv);
-    }
-    // M = Q̃^{-1} E Q̃^{-1} - Q̃^{-1}
-    mm<B>(X, Qinv, E);
-    mm<B>(Y, X, Qinv);
+        // Bm = Zc Q̃^{-1} = (Zc Mq^T) Mq
+        double ZM[B * B];
 SP_UNROLL
-    for (int i = 0; i < B * B; ++i) Y[i] -= Qinv[i];
-    msym<B>(Y);
+        for (int i = 0; i < B; ++i)
+SP_UNROLL
+            for (int j = 0; j < B; ++j) {
+                double s = 0.0;
+SP_UNROLL
+                for (int k = 0; k <= j; ++k) s = fma(Z[i * B + k], Mq[j * B + k], s);
+                ZM[i * B + j] = s;
+            }
+SP_UNROLL
+        for (int i = 0; i < B; ++i)
+SP_UNROLL
+            for (int j = 0; j < B; ++j) {
+                double s = 0.0;
+SP_UNROLL
+                for (int k = j; k < B; ++k) s = fma(ZM[i * B + k], Mq[k * B + j], s);
+                Bm[i * B + j] = s;
+            }
+    }
+    // E - Q̃ (padding states: Q̃ = 1 there and E = 0, but their M rows are unused)
+SP_UNROLL
+    for (int i = 0; i < B * B; ++i) E[i] -= Qraw[i];
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+        if (i < md.b) E[i * B + i] -= jit;
+    msym<B>(E);
+    // M = Mq^T Mq (E - Q̃) Mq^T Mq = Mq^T [Mq (E - Q̃) Mq^T] Mq
+    double Inner[B * B];
+    lmul<B>(X, Mq, E);  // Mq (E - Q̃)
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j <= i; ++j) {
+            double s = 0.0;
+SP_UNROLL
+            for (int k = 0; k <= j; ++k) s = fma(X[i * B + k], Mq[j * B + k], s);
+            Inner[i * B + j] = s;
+            Inner[j * B + i] = s;
+        }
+    sandwich<B>(Y, Mq, Inner);
     T::grad(md, rp, dt, Phi, Qraw, Y, Bm, g);
 }
 
@@ -747,20 +827,18 @@ SP_UNROLL
     for (long long j = en - 2; j >= st; --j) {
         const long long nb = j + 1;
         const double dt = ts[nb] - ts[j];
-        double Phn[B * B], Qn[B * B], Qinvn[B * B], ldqn;
+        double Phn[B * B], Qn[B * B], Mqn[B * B], ldqn;
         T::step(md, rp, dt, Phn, Qn);
-        qt_inverse<B>(Qn, jit, md.b, Qinvn, &ldqn);
-        double Si[B * B], V[B * B], h[B], U[B * B], G[B * B];
-        load_fac<B>(fac + (j - st) * Fac<B>::N * SK + g, SK, hasL, Si, V, h);
-        mtm<B>(U, Phn, Qinvn);
-SP_UNROLL
-        for (int i = 0; i < B * B; ++i) U[i] = -U[i];
-        mm<B>(G, Si, U);
+        qt_factor<B>(Qn, jit, md.b, Mqn, &ldqn);
+        double Li[B * B], Y[B * B], z[B], U[B * B], X[B * B], PQP[B * B];
+        load_fac<B>(fac + (j - st) * Fac<B>::N * SK + g, SK, hasL, Li, Y, z);
+        step_assembly<B>(Phn, Mqn, PQP, U);
+        lmul<B>(X, Li, U);
         double xj[B], CjL[B * B], Cjn[B * B], Cjj[B * B];
-        back_step<B>(Si, V, h, G, hasL, needC, sd, xn, Cnn, CnL, xj, CjL, Cjn, Cjj);
+        back_step<B>(Li, Y, z, X, hasL, needC, sd, xn, Cnn, CnL, xj, CjL, Cjn, Cjj);
         point_out<T>(md, outs, gbase + nb, ys[nb], is2, sig, xn, Cnn, fy, noise, status);
         ldq += ldqn;
-        step_terms<T>(md, rp, dt, Phn, Qn, Qinvn, xn, Cnn, xj, Cjj, Cjn, false, grad, fe, gr);
+        step_terms<T>(md, rp, dt, Phn, Qn, Mqn, xn, Cnn, xj, Cjj, Cjn, false, grad, fe, gr);
 SP_UNROLL
         for (int q = 0; q < B; ++q) xn[q] = xj[q];
         if (needC) {
@@ -773,16 +851,16 @@ SP_UNROLL
     {
         const bool anchor = st == 0;
         const double dt = anchor ? -1.0 : ts[st] - ts[st - 1];
-        double Ph[B * B], Qr[B * B], Qi[B * B], ldq0;
+        double Ph[B * B], Qr[B * B], Mq[B * B], ldq0;
         T::step(md, rp, dt, Ph, Qr);
-        qt_inverse<B>(Qr, jit, md.b, Qi, &ldq0);
+        qt_factor<B>(Qr, jit, md.b, Mq, &ldq0);
         ldq += ldq0;
         double CLs[B * B];  // C_{L, st} = C_{st, L}^T
 SP_UNROLL
         for (int i = 0; i < B; ++i)
 SP_UNROLL
             for (int j = 0; j < B; ++j) CLs[i * B + j] = CnL[j * B + i];
-        step_terms<T>(md, rp, dt, Ph, Qr, Qi, xn, Cnn, sd.xL, sd.CLL, CLs, anchor, grad, fe, gr);
+        step_terms<T>(md, rp, dt, Ph, Qr, Mq, xn, Cnn, sd.xL, sd.CLL, CLs, anchor, grad, fe, gr);
     }
     part[P_FITY * SK + g] = fy;
     part[P_FITE * SK + g] = fe;
@@ -933,36 +1011,34 @@ __global__ void __launch_bounds__(128) k_assemble(ModelDesc md, const double* __
     if (i >= n) return;
     const double sig = params[0], jit = params[1], is2 = 1.0 / (sig * sig);
     const int b = md.b;
-    double Phi[B * B], Q[B * B], Qinv[B * B], D[B * B];
+    double Phi[B * B], Q[B * B], Mq[B * B], D[B * B];
     const double dt = i == 0 ? -1.0 : t[i] - t[i - 1];
     if (i > 0 && (!(dt > 0.0) || !isfinite(dt))) {
         report(status, i, dt == 0.0 ? ST_DUPLICATE : ST_BAD_ARG);
         return;
     }
     T::step(md, params, dt, Phi, Q);
-    if (!qt_inverse<B>(Q, jit, b, Qinv, nullptr)) {
+    if (!qt_factor<B>(Q, jit, b, Mq, nullptr)) {
         report(status, i, ST_SINGULAR_Q);
         return;
     }
-    mcopy<B>(D, Qinv);
+    ltl<B>(D, Mq);
     if (i + 1 < n) {
         const double dtn = t[i + 1] - t[i];
         if (!(dtn > 0.0) || !isfinite(dtn)) {
             report(status, i + 1, dtn == 0.0 ? ST_DUPLICATE : ST_BAD_ARG);
             return;
         }
-        double Phn[B * B], Qn[B * B], Qinvn[B * B], PtQ[B * B], X[B * B];
+        double Phn[B * B], Qn[B * B], Mqn[B * B], PQP[B * B], U[B * B];
         T::step(md, params, dtn, Phn, Qn);
-        if (!qt_inverse<B>(Qn, jit, b, Qinvn, nullptr)) {
+        if (!qt_factor<B>(Qn, jit, b, Mqn, nullptr)) {
             report(status, i + 1, ST_SINGULAR_Q);
             return;
         }
-        mtm<B>(PtQ, Phn, Qinvn);
-        mm<B>(X, PtQ, Phn);
-        msym<B>(X);
-        for (int q = 0; q < B * B; ++q) D[q] += X[q];
+        step_assembly<B>(Phn, Mqn, PQP, U);
+        for (int q = 0; q < B * B; ++q) D[q] += PQP[q];
         for (int p = 0; p < b; ++p)
-            for (int q = 0; q < b; ++q) up[(i * b + p) * b + q] = -PtQ[p * B + q];
+            for (int q = 0; q < b; ++q) up[(i * b + p) * b + q] = U[p * B + q];
     }
     for (int p = 0; p < b; ++p)
         for (int q = 0; q < b; ++q)

@@ -352,8 +352,14 @@ struct GenericTraits {
     SP_DEV static double H(const ModelDesc& md, int i) { return i < md.b ? md.H[i] : 0.0; }
     SP_DEV static void step(const ModelDesc& md, const double* rec, double dt, double* Phi,
                             double* Q) {
-        mzero<BB>(Phi);
-        mzero<BB>(Q);
+        // Zero-fill with a rolled loop: statically unrolled (vectorised) zero stores
+        // followed by the leaves' dynamically offset stores into the same local array
+        // were reordered by nvcc 12.9 / sm_100a (lost Q[0..1]; tools/dbg/dbg_generic.cu).
+#pragma unroll 1
+        for (int i = 0; i < BB * BB; ++i) {
+            Phi[i] = 0.0;
+            Q[i] = 0.0;
+        }
         for (int i = md.b; i < BB; ++i) Q[i * BB + i] = 1.0;  // padding
         for (int l = 0; l < md.nleaves; ++l) {
             const double* lr = rec + md.rec[l];

@@ -198,4 +198,63 @@ int emu_btd(int64_t n, int32_t b, const double* diag, const double* upper, const
     return finish();
 }
 
+// One step of the device discretisation (T::step) and its θ-derivatives (read
+// back through T::grad with unit M / Bm probes):  Phi, Q (raw, no jitter),
+// dPhi[nt][b][b], dQt[nt][b][b] (with the jitter derivative).  dt < 0 = anchor.
+int emu_discretize(const spingp_leaf* leaves, int32_t n_leaves, const double* theta, int32_t n_theta,
+                   double sigma, double dt, double* Phi, double* Q, double* dPhi, double* dQt, double* jit) {
+    try {
+        const HostModel hm = build_model(leaves, n_leaves, n_theta);
+        std::vector<double> rec(hm.rec_stride);
+        fill_record(hm, theta, sigma, rec.data());
+        std::vector<double> eqc = hm.eqconst;
+        ModelDesc md = hm.desc;
+        md.eqconst = eqc.data();
+        const int b = hm.b, nt = hm.nt;
+        if (jit) *jit = rec[1];
+        auto run = [&](auto tag) {
+            using T = decltype(tag);
+            constexpr int B = T::B;
+            double P[B * B], Qq[B * B];
+            T::step(md, rec.data(), dt, P, Qq);
+            for (int i = 0; i < b; ++i)
+                for (int j = 0; j < b; ++j) {
+                    Phi[i * b + j] = P[i * B + j];
+                    Q[i * b + j] = Qq[i * B + j];
+                }
+            if (!dPhi) return;
+            for (int a = 0; a < b; ++a)
+                for (int c = 0; c < b; ++c) {
+                    double M[B * B] = {}, Bm[B * B] = {}, g[kMaxTheta] = {};
+                    Bm[c * B + a] = 1.0;  // g = Tr(dPhi Bm) = dPhi[a][c]
+                    T::grad(md, rec.data(), dt, P, Qq, M, Bm, g);
+                    for (int p = 0; p < nt; ++p) dPhi[(p * b + a) * b + c] = g[p];
+                    double M2[B * B] = {}, B2[B * B] = {}, g2[kMaxTheta] = {};
+                    M2[a * B + c] += 1.0;
+                    M2[c * B + a] += 1.0;  // g = ½Tr(M dQ) = dQ[a][c] (a != c) or dQ[a][a]
+                    T::grad(md, rec.data(), dt, P, Qq, M2, B2, g2);
+                    for (int p = 0; p < nt; ++p) dQt[(p * b + a) * b + c] = g2[p];
+                }
+        };
+        if (hm.single_matern) {
+            if (hm.b == 1) run(MaternTraits<1>{});
+            else if (hm.b == 2) run(MaternTraits<2>{});
+            else run(MaternTraits<3>{});
+        } else {
+            switch (std::max(3, pad_b(hm.b))) {
+                case 3: run(GenericTraits<3>{}); break;
+                case 4: run(GenericTraits<4>{}); break;
+                case 6: run(GenericTraits<6>{}); break;
+                case 8: run(GenericTraits<8>{}); break;
+                case 12: run(GenericTraits<12>{}); break;
+                case 16: run(GenericTraits<16>{}); break;
+            }
+        }
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return SPINGP_BAD_ARG;
+    }
+    return 0;
+}
+
 }  // extern "C"

@@ -91,3 +91,22 @@ def btd(diag, upper, rhs=None, selinv=False, m0=0):
     if st:
         raise EmuError(st, fb.value, "btd failure")
     return dict(x=x, cdiag=cd, cupper=None if cu is None else cu[:n - 1], logdet=ld.value)
+
+
+def discretize(leaves, theta, dt, sigma=0.3):
+    """Device closed-form step (T::step / T::grad) run on the host: Phi, Q, dPhi, dQt, jitter."""
+    import oracle_lib
+    b = oracle_lib.state_space(leaves, theta)["b"]
+    nt = len(theta)
+    L = lib()
+    L.emu_discretize.argtypes = [ctypes.c_void_p, ctypes.c_int32, _d, ctypes.c_int32, ctypes.c_double, ctypes.c_double,
+                                 _d, _d, _d, _d, _d]
+    th = np.ascontiguousarray(theta, dtype=np.float64)
+    Phi = np.zeros((b, b)); Q = np.zeros((b, b)); dPhi = np.zeros((nt, b, b)); dQ = np.zeros((nt, b, b))
+    jit = ctypes.c_double()
+    lv = _leaves(leaves)
+    st = L.emu_discretize(lv.ctypes.data, len(leaves), _p(th), nt, float(sigma), float(dt), _p(Phi), _p(Q), _p(dPhi),
+                          _p(dQ), ctypes.byref(jit))
+    if st:
+        raise EmuError(st, -1, L.emu_last_error().decode())
+    return Phi, Q, dPhi, dQ, jit.value

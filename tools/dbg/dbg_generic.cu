@@ -16,7 +16,7 @@ typedef GenericTraits<GB> T;
 __global__ void kstep(ModelDesc md, const double* rp, double dt, double* out) {
     double Phi[GB * GB], Q[GB * GB], Qi[GB * GB];
     T::step(md, rp, dt, Phi, Q);
-    bool ok = qt_inverse<GB>(Q, rp[1], md.b, Qi, nullptr);
+    bool ok = qt_factor<GB>(Q, rp[1], md.b, Qi, nullptr);
     for (int i = 0; i < GB * GB; ++i) { out[i] = Phi[i]; out[GB * GB + i] = Q[i]; }
     out[2 * GB * GB] = ok;
 }
@@ -44,7 +44,7 @@ int main(int argc, char** argv) {
         md.eqconst = rec.data() + hm.rec_stride;
         double Qi[GB * GB];
         T::step(md, rec.data(), dt, out, out + GB * GB);
-        out[2 * GB * GB] = qt_inverse<GB>(out + GB * GB, rec[1], md.b, Qi, nullptr);
+        out[2 * GB * GB] = qt_factor<GB>(out + GB * GB, rec[1], md.b, Qi, nullptr);
         printf("HOST dt=%g ok=%g\n", dt, out[2 * GB * GB]);
 #endif
         for (int i = 0; i < GB; ++i) { for (int j = 0; j < GB; ++j) printf("%9.5f ", out[i * GB + j]); printf(" | "); for (int j = 0; j < GB; ++j) printf("%9.5f ", out[GB * GB + i * GB + j]); printf("\n"); }
