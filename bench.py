@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""Benchmark: SpInGP loglik+grad time points/s (fp64) on B200.
+
+Default workload (N=1): BASELINE cfg2 — Matérn-5/2 (b=3), one series of 1,000,000
+seeded synthetic points, log-likelihood + gradient (var, len, σ) + posterior mean,
+every step the full fused hot path (closed-form discretisation -> assembly ->
+partitioned block elimination -> selected inverse -> loglik/gradient reduction).
+
+  value  : device-resident inputs, CUDA events around each step on the library's
+           stream, L2 flushed (256 MiB write) between steps outside the events.
+  e2e    : the same metric through the host-pointer C ABI call (spingp_eval):
+           pinned host t,y -> H2D, kernels, D2H of loglik, gradient and mean.
+  N > 1  : torchrun, one rank per GPU; every rank evaluates its own seeded series
+           of the same size (independent series, weak scaling, no data-path
+           collective; SURVEY.md §8(e) "batches of independent series are sharded").
+  --impl reference : the CPU oracle (restatement of the reference algorithm, Padé/
+           Van Loan per step + block Thomas + Takahashi; the reference itself does
+           not build here) on all host cores, same workload, rank 0 only.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+
+METRIC = "SpInGP loglik+grad time points/s (fp64), 1/2/4/8 B200, % HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--points", type=int, default=0, help="override N (testing only; not a bench value)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload(name, rank, points):
+    from paper_1610_08035_b200 import datasets
+    kw = {}
+    if points:
+        kw["n"] = points
+    if rank:
+        kw["seed"] = datasets.SEEDS[name] + 7919 * rank
+    return datasets.make(name, **kw)
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+FP64_PEAK_TFLOPS = 34.1  # DFMA microbenchmark on this pool's B200 (profiles/r01_box_probe.log)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 9:
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower().startswith("active"):
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def alg_bytes_per_point(kernel, wl):
+    """Compulsory HBM bytes of one launch per time point (SURVEY.md §8(d) B_io split by kernel)."""
+    outs = 8 * (("mean" in wl.outputs) + ("var" in wl.outputs))
+    if kernel == "k_fwd0":
+        return 16.0           # t, y read once
+    if kernel == "k_rev0":
+        return 16.0 + outs    # t, y read once, per-point outputs written once
+    return 0.0
+
+
+def core_flops_per_point(b, n_theta):
+    """F_core = 8 b^3 + 4 b^2 (1 + n_θ) (factor + selected inverse + traces; lower bound)."""
+    return 8 * b ** 3 + 4 * b ** 2 * (1 + n_theta)
+
+
+def cpu_baseline(wl, seconds=10.0):
+    """The oracle (restatement of the reference CPU path) on all host cores, on a
+    bounded prefix of the same series, sized to ~`seconds` of CPU time."""
+    import oracle_lib as O
+    threads = os.cpu_count() or 1
+    grad, mean, var = "grad" in wl.outputs, "mean" in wl.outputs, "var" in wl.outputs
+    th = np.asarray(wl.theta, float)
+    if wl.batched:
+        pilot = max(1, min(wl.t.shape[0], 64))
+        t0 = time.perf_counter()
+        O.evaluate_batched(wl.leaves, th[:pilot], wl.t[:pilot], wl.y[:pilot], wl.sigma[:pilot], grad=grad,
+                           threads=threads)
+        rate = pilot * wl.t.shape[1] / (time.perf_counter() - t0)
+        S = int(min(wl.t.shape[0], max(pilot, rate * seconds / wl.t.shape[1])))
+        t0 = time.perf_counter()
+        O.evaluate_batched(wl.leaves, th[:S], wl.t[:S], wl.y[:S], wl.sigma[:S], grad=grad, threads=threads)
+        dt = time.perf_counter() - t0
+        return {"value": S * wl.t.shape[1] / dt, "unit": "points/s", "cores": threads, "kind": "port",
+                "sample": f"first {S} of {wl.t.shape[0]} series x {wl.t.shape[1]} points, loglik+grad, {dt:.1f} s"}
+    n = len(wl.t)
+    pilot = min(n, 20_000)
+    t0 = time.perf_counter()
+    O.evaluate(wl.leaves, th, wl.t[:pilot], wl.y[:pilot], wl.sigma, grad=grad, mean=mean, var=var, threads=threads)
+    rate = pilot / (time.perf_counter() - t0)
+    m = int(min(n, max(pilot, rate * seconds)))
+    t0 = time.perf_counter()
+    O.evaluate(wl.leaves, th, wl.t[:m], wl.y[:m], wl.sigma, grad=grad, mean=mean, var=var, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": m / dt, "unit": "points/s", "cores": threads, "kind": "port",
+            "sample": f"first {m} of {n} points, loglik+grad" + ("+mean" if mean else "") + ("+var" if var else "")
+                      + f", {dt:.1f} s"}
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    wl = workload(args.config, 0, args.points)
+    import oracle_lib as O
+    threads = os.cpu_count() or 1
+    grad, mean, var = "grad" in wl.outputs, "mean" in wl.outputs, "var" in wl.outputs
+    th = np.asarray(wl.theta, float)
+
+    def step():
+        if wl.batched:
+            O.evaluate_batched(wl.leaves, th, wl.t, wl.y, wl.sigma, grad=grad, threads=threads)
+        else:
+            O.evaluate(wl.leaves, th, wl.t, wl.y, wl.sigma, grad=grad, mean=mean, var=var, threads=threads)
+
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = wl.points * args.steps / total
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, BASELINE shapes)",
+            "config": {"workload": wl.description, "config": wl.name, "points": wl.points,
+                       "outputs": ["loglik"] + list(wl.outputs)},
+            "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": "port",
+                             "sample": f"full {wl.name} workload per step ({wl.points} points), all host threads; "
+                                       "the reference itself cannot be built (no Eigen/GTest), oracle/ restates it"},
+            "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+    import paper_1610_08035_b200 as P
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    wl = workload(args.config, rank, args.points)
+    b, nt = P.kernel_dims(wl.leaves)
+    flags = P.WANT_GRAD | (P.WANT_MEAN if "mean" in wl.outputs else 0) | (P.WANT_VAR if "var" in wl.outputs else 0)
+    S = wl.t.shape[0] if wl.batched else 1
+    n = wl.t.shape[-1]
+    ctx = P.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    d_t = torch.from_numpy(np.ascontiguousarray(wl.t)).to(dev)
+    d_y = torch.from_numpy(np.ascontiguousarray(wl.y)).to(dev)
+    d_ll = torch.zeros(S, dtype=torch.float64, device=dev)
+    d_g = torch.zeros(S * (nt + 1), dtype=torch.float64, device=dev)
+    d_m = torch.zeros(S * n, dtype=torch.float64, device=dev) if flags & P.WANT_MEAN else None
+    d_v = torch.zeros(S * n, dtype=torch.float64, device=dev) if flags & P.WANT_VAR else None
+    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        if wl.batched:
+            ctx.eval_batched_device(wl.leaves, wl.theta, S, n, d_t.data_ptr(), d_y.data_ptr(), wl.sigma, flags,
+                                    d_ll.data_ptr(), d_g.data_ptr(), d_m.data_ptr() if d_m is not None else 0,
+                                    d_v.data_ptr() if d_v is not None else 0)
+        else:
+            ctx.eval_device(wl.leaves, wl.theta, d_t.data_ptr(), d_y.data_ptr(), n, wl.sigma, flags,
+                            d_ll.data_ptr(), d_g.data_ptr(), d_m.data_ptr() if d_m is not None else 0,
+                            d_v.data_ptr() if d_v is not None else 0)
+
+    for _ in range(max(3, args.warmup)):
+        flush.zero_()
+        step()
+    ctx.status()
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = ctx.launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps, outside the events
+            evs[k][0].record(stream)
+            step()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize(dev)
+    launches = ctx.launch_count() - launches0
+    ctx.status()  # raises on any device-side failure in the timed steps
+    step_ms = [a.elapsed_time(bv) for a, bv in evs]
+    total_ms = float(sum(step_ms))
+    if ws > 1:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+        dist.barrier()
+    value = wl.points * ws * args.steps / (total_ms * 1e-3)
+
+    # per-kernel breakdown (separate, untimed profiling pass; events around every launch)
+    ctx.set_profiling(True)
+    kt = {}
+    reps = 3
+    for _ in range(reps):
+        flush.zero_()
+        step()
+        for name, ms in ctx.kernel_times():
+            kt.setdefault(name, []).append(ms)
+    ctx.set_profiling(False)
+    per_step = {k: sum(v) / reps for k, v in kt.items()}
+    dom = max(per_step, key=per_step.get)
+    dom_launch_ms = statistics.mean(kt[dom])
+    launches_per_step = {k: len(v) // reps for k, v in kt.items()}
+
+    # e2e through the host-pointer ABI call (pinned host inputs, D2H of the results)
+    h_t = torch.from_numpy(np.ascontiguousarray(wl.t)).pin_memory().numpy()
+    h_y = torch.from_numpy(np.ascontiguousarray(wl.y)).pin_memory().numpy()
+    want = dict(grad=True, mean="mean" in wl.outputs, var="var" in wl.outputs)
+
+    def e2e_step():
+        if wl.batched:
+            return ctx.eval_batched(wl.leaves, wl.theta, h_t, h_y, wl.sigma, **want)
+        return ctx.eval(wl.leaves, wl.theta, h_t, h_y, wl.sigma, **want)
+
+    for _ in range(2):
+        e2e_step()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e_ms = []
+    for _ in range(args.steps):
+        a = torch.cuda.Event(enable_timing=True)
+        bv = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        e2e_step()
+        bv.record(stream)
+        bv.synchronize()
+        e_ms.append(a.elapsed_time(bv))
+    e_total = float(sum(e_ms))
+    if ws > 1:
+        tt = torch.tensor([e_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e_total = float(tt.item())
+    e2e_value = wl.points * ws * args.steps / (e_total * 1e-3)
+    h2d = 2 * 8 * wl.points
+    d2h = 8 * (S + S * (nt + 1) + (S * n if want["mean"] else 0) + (S * n if want["var"] else 0))
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+    peak, peak_src = measured_peaks()
+    abytes = alg_bytes_per_point(dom, wl) * wl.points
+    achieved = abytes / (dom_launch_ms * 1e-3) / 1e9 if abytes else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tr = json.load(f).get(wl.name, {}).get(dom)
+        if tr is not None:
+            traffic = tr
+    F = core_flops_per_point(b, nt) * wl.points
+    fp64_achieved = F / (total_ms / args.steps * 1e-3) / 1e12
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE shapes; no public dataset)",
+        "config": {"workload": wl.description, "config": wl.name, "points_per_gpu": wl.points,
+                   "outputs": ["loglik"] + list(wl.outputs), "state_dim": b, "n_theta": nt,
+                   "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                   "parallelism": "single GPU" if ws == 1 else f"{ws} ranks, independent series per rank"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "note": f"algorithmic bytes = {alg_bytes_per_point(dom, wl):.0f} B/point x {wl.points} points "
+                             f"per launch / {dom_launch_ms:.4f} ms mean launch; peak {peak_src}"},
+        "roofline_fp64": {"bound": "fp64", "achieved": fp64_achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                          "frac": fp64_achieved / FP64_PEAK_TFLOPS,
+                          "note": "F_core = 8b^3 + 4b^2(1+n_theta) flop/point (SURVEY.md §8(d), lower bound) "
+                                  "over the whole step; peak = measured DFMA microbenchmark"},
+        "kernels_ms_per_step": {k: round(v, 5) for k, v in sorted(per_step.items(), key=lambda x: -x[1])},
+        "launches_per_step": launches_per_step,
+        "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e_total / args.steps},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    if ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(wl)
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_info()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    run_ours(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -117,6 +117,12 @@ int spingp_ctx_status(spingp_ctx* ctx, int64_t* fail_block);
 int64_t spingp_ctx_launch_count(spingp_ctx* ctx);
 /* Tuning/testing knob: force the level-0 chunk length (0 = automatic). */
 int spingp_ctx_set_chunk(spingp_ctx* ctx, int64_t m0);
+/* Diagnostics: bracket every kernel launch with CUDA events (on the context's
+ * stream) and report them: spingp_ctx_kernel_times synchronises, returns up to
+ * `cap` (name, milliseconds) pairs in launch order and clears the record. */
+int spingp_ctx_set_profiling(spingp_ctx* ctx, int on);
+int spingp_ctx_kernel_times(spingp_ctx* ctx, const char** names, double* ms, int32_t cap,
+                            int32_t* count);
 
 /* ---- the hot path: discretise -> assemble -> partitioned BTD factor/solve/selinv
  *      -> loglik, gradient, posterior mean/var, fused on the device ------------- */

@@ -82,6 +82,8 @@ SIGNATURES = {
     "spingp_ctx_status": (ctypes.c_int, [_vp, _i64p]),
     "spingp_ctx_launch_count": (_i64, [_vp]),
     "spingp_ctx_set_chunk": (ctypes.c_int, [_vp, _i64]),
+    "spingp_ctx_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "spingp_ctx_kernel_times": (ctypes.c_int, [_vp, _P(ctypes.c_char_p), _d, _i32, _i32p]),
     "spingp_eval": (ctypes.c_int, [_vp, _vp, _i32, _d, _i32, _d, _d, _i64, _dbl, _u32, _d, _d, _d, _d, _i64p]),
     "spingp_eval_device": (ctypes.c_int, [_vp, _vp, _i32, _d, _i32, _vp, _vp, _i64, _dbl, _u32, _vp, _vp, _vp, _vp]),
     "spingp_eval_batched": (ctypes.c_int, [_vp, _vp, _i32, _d, _i32, _i64, _i64, _d, _d, _d, _u32, _d, _d, _d, _d,
@@ -199,6 +201,18 @@ class Context:
 
     def set_chunk(self, m0):
         _raise(lib().spingp_ctx_set_chunk(self._h, int(m0)))
+
+    def set_profiling(self, on=True):
+        _raise(lib().spingp_ctx_set_profiling(self._h, 1 if on else 0))
+
+    def kernel_times(self, cap=4096):
+        """[(kernel name, ms)] for every launch since the last call (synchronises)."""
+        names = (ctypes.c_char_p * cap)()
+        ms = np.zeros(cap)
+        cnt = _i32()
+        _raise(lib().spingp_ctx_kernel_times(self._h, names, _p(ms), cap, ctypes.byref(cnt)))
+        k = min(cnt.value, cap)
+        return [(names[i].decode(), float(ms[i])) for i in range(k)]
 
     def launch_count(self):
         return int(lib().spingp_ctx_launch_count(self._h))

@@ -34,29 +34,34 @@ void launch_btd(spingp_ctx* ctx, int64_t n, int b, const double* d_diag, const d
     double* toplogdet = ctx->ws.take<double>(1);
     const int tpb = 128;
     UserSource<B> usrc{d_diag, d_upper, d_rhs, n, b, k, col};
+    ctx->pre();
     k_fwdL<B, UserSource<B>><<<blocks_for(g.K[0], tpb), tpb, 0, ctx->stream>>>(usrc, g, 0, fac[0], rec[0],
                                                                                ctx->d_status);
-    ctx->launched();
+    ctx->launched("k_fwd");
     for (int l = 1; l < g.nlev; ++l) {
         RecSource<B> src{rec[l - 1], g.K[l - 1], g.n[l]};
+        ctx->pre();
         k_fwdL<B, RecSource<B>><<<blocks_for(g.K[l], tpb), tpb, 0, ctx->stream>>>(src, g, l, fac[l], rec[l],
                                                                                  ctx->d_status);
-        ctx->launched();
+        ctx->launched("k_fwd");
     }
+    ctx->pre();
     k_top<B><<<1, 32, 0, ctx->stream>>>(g, rec[g.nlev - 1], sol[g.nlev], toplogdet, ctx->d_status);
-    ctx->launched();
+    ctx->launched("k_top");
     for (int l = g.nlev - 1; l >= 1; --l) {
         RecSource<B> src{rec[l - 1], g.K[l - 1], g.n[l]};
         SolSink<B> sink{sol[l], g.n[l], g.n[l]};
+        ctx->pre();
         k_revL<B, RecSource<B>, SolSink<B>><<<blocks_for(g.K[l], tpb), tpb, 0, ctx->stream>>>(
             src, sink, g, l, fac[l], sol[l + 1], needC ? 1 : 0);
-        ctx->launched();
+        ctx->launched("k_rev");
     }
     if (d_x || needC) {
         UserSink<B> usink{d_x, d_cdiag, d_cupper, b, k, col};
+        ctx->pre();
         k_revL<B, UserSource<B>, UserSink<B>><<<blocks_for(g.K[0], tpb), tpb, 0, ctx->stream>>>(
             usrc, usink, g, 0, fac[0], sol[1], needC ? 1 : 0);
-        ctx->launched();
+        ctx->launched("k_rev");
     }
     if (d_logdet) {
         LogdetArgs la{};
@@ -64,8 +69,9 @@ void launch_btd(spingp_ctx* ctx, int64_t n, int b, const double* d_diag, const d
         la.logdet_comp = Rec<B>::LOGDET;
         la.toplogdet = toplogdet;
         la.out = d_logdet;
+        ctx->pre();
         k_logdet_btd<<<1, 256, 0, ctx->stream>>>(g, la);
-        ctx->launched();
+        ctx->launched("k_logdet_btd");
     }
 }
 

@@ -170,6 +170,7 @@ int spingp_ctx_destroy(spingp_ctx* ctx) {
         if (ctx->h_stage[k]) cudaFreeHost(ctx->h_stage[k]);
         if (ctx->stage_ev[k]) cudaEventDestroy(ctx->stage_ev[k]);
     }
+    for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return SPINGP_OK;
@@ -209,6 +210,35 @@ int spingp_ctx_status(spingp_ctx* ctx, int64_t* fail_block) {
 }
 
 int64_t spingp_ctx_launch_count(spingp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int spingp_ctx_set_profiling(spingp_ctx* ctx, int on) {
+    if (!ctx) return SPINGP_BAD_ARG;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->profiling = on != 0;
+    ctx->timed.clear();
+    ctx->ev_used = 0;
+    return SPINGP_OK;
+}
+
+int spingp_ctx_kernel_times(spingp_ctx* ctx, const char** names, double* ms, int32_t cap,
+                            int32_t* count) {
+    return guarded(nullptr, [&] {
+        checked(ctx);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        CUDA_OK(cudaStreamSynchronize(ctx->stream));
+        const int n = static_cast<int>(ctx->timed.size());
+        if (count) *count = n;
+        for (int i = 0; i < n && i < cap; ++i) {
+            float t = 0.f;
+            CUDA_OK(cudaEventElapsedTime(&t, ctx->timed[i].a, ctx->timed[i].b));
+            if (names) names[i] = ctx->timed[i].name;
+            if (ms) ms[i] = t;
+        }
+        ctx->timed.clear();
+        ctx->ev_used = 0;
+        return SPINGP_OK;
+    });
+}
 
 int spingp_eval_batched_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
                                const double* theta, int32_t n_theta, int64_t S, int64_t n,

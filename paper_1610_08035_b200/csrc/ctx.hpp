@@ -10,6 +10,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "engine.cuh"
 #include "host_model.hpp"
@@ -78,6 +79,30 @@ struct spingp_ctx {
     int64_t launches = 0;
     int64_t m0_override = 0;  // testing knob: force the level-0 chunk length
     std::mutex mu;
+    // optional per-launch CUDA-event timing (spingp_ctx_set_profiling)
+    bool profiling = false;
+    struct Timed {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Timed> timed;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    cudaEvent_t next_event() {
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t e;
+            CUDA_OK(cudaEventCreate(&e));
+            ev_pool.push_back(e);
+        }
+        return ev_pool[ev_used++];
+    }
+    // bracket one kernel launch: pre() before, launched(name) after
+    cudaEvent_t pending = nullptr;
+    void pre() {
+        if (!profiling) return;
+        pending = next_event();
+        CUDA_OK(cudaEventRecord(pending, stream));
+    }
 
     void ensure_ws(size_t bytes) {
         if (bytes <= ws.size) return;
@@ -107,9 +132,15 @@ struct spingp_ctx {
         return h_stage[k];
     }
     void stage_done() { CUDA_OK(cudaEventRecord(stage_ev[cur_slot], stream)); }
-    void launched() {
+    void launched(const char* name = "kernel") {
         launches++;
         CUDA_OK(cudaGetLastError());
+        if (profiling && pending) {
+            cudaEvent_t e = next_event();
+            CUDA_OK(cudaEventRecord(e, stream));
+            timed.push_back(Timed{name, pending, e});
+            pending = nullptr;
+        }
     }
 };
 

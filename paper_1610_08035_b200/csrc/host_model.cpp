@@ -108,7 +108,7 @@ HostModel build_model(const spingp_leaf* leaves, int32_t n_leaves, int32_t n_the
 
 // Per-series record (see model_dev.cuh): sigma, jitter, d jitter/dθ, leaf records.
 void fill_record(const HostModel& hm, const double* theta, double sigma, double* r) {
-    if (!(sigma > 0.0) || !std::isfinite(sigma)) throw std::invalid_argument("sigma must be positive");
+    if (!(sigma > 0.0)) throw std::invalid_argument("sigma must be positive");  // +inf: no observation term
     const ModelDesc& d = hm.desc;
     const double b = hm.b;
     double tr = 0.0;

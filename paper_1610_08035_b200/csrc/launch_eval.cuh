@@ -71,41 +71,48 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
 
     const int tpb = 128;
     if (a.mode == 1) {
+        ctx->pre();
         k_assemble<T><<<blocks_for(g.n[0], tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g.n[0], a.d_diag,
                                                                        a.d_upper, a.d_rhs, ctx->d_status);
-        ctx->launched();
+        ctx->launched("k_assemble");
         return;
     }
     const long long SK0 = g.K[0] * g.S;
+    ctx->pre();
     k_fwd0<T><<<blocks_for(SK0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
                                                              eb.rec[0], eb.part, ctx->d_status);
-    ctx->launched();
+    ctx->launched("k_fwd0");
     for (int l = 1; l < g.nlev; ++l) {
         RecSource<B> src{eb.rec[l - 1], g.K[l - 1] * g.S, g.n[l]};
+        ctx->pre();
         k_fwdL<B, RecSource<B>><<<blocks_for(g.K[l] * g.S, tpb), tpb, 0, ctx->stream>>>(
             src, g, l, eb.fac[l], eb.rec[l], ctx->d_status);
-        ctx->launched();
+        ctx->launched("k_fwd");
     }
+    ctx->pre();
     k_top<B><<<blocks_for(g.S, 128), 128, 0, ctx->stream>>>(g, eb.rec[g.nlev - 1], eb.sol[g.nlev],
                                                            eb.toplogdet, ctx->d_status);
-    ctx->launched();
+    ctx->launched("k_top");
     const bool grad = a.flags & SPINGP_WANT_GRAD;
     const bool needC = grad || (a.flags & SPINGP_WANT_VAR);
     for (int l = g.nlev - 1; l >= 1; --l) {
         RecSource<B> src{eb.rec[l - 1], g.K[l - 1] * g.S, g.n[l]};
         SolSink<B> sink{eb.sol[l], g.n[l] * g.S, g.n[l]};
+        ctx->pre();
         k_revL<B, RecSource<B>, SolSink<B>><<<blocks_for(g.K[l] * g.S, tpb), tpb, 0, ctx->stream>>>(
             src, sink, g, l, eb.fac[l], eb.sol[l + 1], needC ? 1 : 0);
-        ctx->launched();
+        ctx->launched("k_rev");
     }
     Outs outs{(a.flags & SPINGP_WANT_MEAN) ? a.d_mean : nullptr, (a.flags & SPINGP_WANT_VAR) ? a.d_var : nullptr,
               (a.flags & SPINGP_INCLUDE_NOISE) ? 1 : 0, grad ? 1 : 0, needC ? 1 : 0};
+    ctx->pre();
     k_rev0<T><<<blocks_for(SK0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
                                                              eb.sol[1], eb.part, outs, ctx->d_status);
-    ctx->launched();
+    ctx->launched("k_rev0");
     const int NC = P_GRAD + nt;
+    ctx->pre();
     k_reduce_seg<<<dim3(eb.nseg, g.S), 256, 0, ctx->stream>>>(eb.part, g.K[0], g.S, NC, eb.seg);
-    ctx->launched();
+    ctx->launched("k_reduce_seg");
     FinalArgs fa{};
     fa.seg = eb.seg;
     fa.nseg = eb.nseg;
@@ -119,8 +126,9 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     fa.n = g.n[0];
     fa.loglik = a.d_loglik;
     fa.grad = grad ? a.d_grad : nullptr;
+    ctx->pre();
     k_reduce_final<<<g.S, 256, 0, ctx->stream>>>(fa, g);
-    ctx->launched();
+    ctx->launched("k_reduce_final");
 }
 
 }  // namespace spingp_host

@@ -1,0 +1,112 @@
+"""The product's device algorithm, executed on the CPU through the host emulation
+of the exact kernel code (tests/emu/: engine.cuh compiled as host C++), against
+the oracle.  Covers the partitioned elimination for every chunking (including the
+cyclic-reduction limit m = 2), ragged and tiny series, batched series, the
+closed-form discretisation and its θ-derivatives, and the btd_core operators."""
+import numpy as np
+import pytest
+
+import emu_lib as E
+import oracle_lib as O
+from conftest import rel
+
+KERNELS = [
+    ([O.MATERN12], [0.8, 1.7]),
+    ([O.MATERN32], [1.3, 0.9]),
+    ([O.MATERN52], [2.1, 1.2]),
+    ([(O.EQ, 6)], [1.1, 1.4]),
+    ([O.MATERN32, O.MATERN12], [1.0, 0.7, 0.5, 2.0]),
+    ([(O.QP, 3)], [1.0, 0.8, 1.3, 5.0]),
+    ([O.MATERN32, (O.QP, 6)], [1.0, 10.0, 1.0, 1.0, 1.0, 20.0]),
+]
+
+
+def series(seed, n, lo=0.05, hi=0.15):
+    rng = np.random.default_rng(seed)
+    t = np.cumsum(rng.uniform(lo, hi, n))
+    return t, np.sin(0.5 * t) + 0.3 * rng.standard_normal(n)
+
+
+@pytest.mark.parametrize("leaves,theta", KERNELS)
+@pytest.mark.parametrize("dt", [-1.0, 0.3, 0.01])
+def test_closed_form_discretisation_matches_pade(leaves, theta, dt):
+    """model_dev.cuh closed forms vs the oracle's Padé expm / Van Loan (kernels.hpp:392-443)."""
+    Pe, Qe, dPe, dQe, jit = E.discretize(leaves, theta, dt)
+    ss = O.state_space(leaves, theta)
+    b = ss["b"]
+    if dt < 0:  # anchor step: Φ := 0, Q = Pinf, dQ = dPinf
+        Po, Qo = np.zeros((b, b)), ss["Pinf"]
+        dPo, dQo = np.zeros((len(theta), b, b)), ss["dPinf"].copy()
+    else:
+        Po, Qo, dPo, dQo = O.discretize(leaves, theta, dt, grad=True)
+    for p in range(len(theta)):  # + d jitter / dθ
+        dQo[p] += 1e-10 * np.trace(ss["dPinf"][p]) / b * np.eye(b)
+    assert np.abs(Pe - Po).max() < 1e-14
+    assert np.abs(Qe - Qo).max() <= 1e-12 * max(1.0, np.abs(ss["Pinf"]).max())
+    assert np.abs(dPe - dPo).max() <= 1e-12 * max(1.0, np.abs(dPo).max())
+    assert np.abs(dQe - dQo).max() <= 1e-11 * max(1.0, np.abs(dQo).max())
+
+
+@pytest.mark.parametrize("leaves,theta", [k for k in KERNELS if k[0][0] != (O.EQ, 6)])
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 8, 9, 31, 33, 100])
+@pytest.mark.parametrize("m0", [0, 2, 3, 5])
+def test_partitioned_elimination_matches_oracle(leaves, theta, n, m0):
+    t, y = series(n * 7 + m0, n)
+    e = E.evaluate(leaves, theta, t, y, 0.3, m0=m0)
+    o = O.evaluate(leaves, theta, t, y, 0.3)
+    for k, tol in (("loglik", 1e-10), ("grad", 1e-9), ("mean", 1e-9), ("var", 1e-9)):
+        if rel(e[k], o[k]) >= tol:  # arbitrate with the long-double evaluation
+            ld = O.evaluate(leaves, theta, t, y, 0.3, precision=1)
+            assert rel(e[k], ld[k]) <= max(tol, 4 * rel(o[k], ld[k])), k
+
+
+@pytest.mark.parametrize("m0", [0, 2, 4])
+def test_eq_against_long_double_arbiter(m0):
+    """EQ is ill-conditioned in fp64: the device algorithm must be at
+    least as close to the long-double evaluation of the reference formulas as the fp64
+    oracle itself (x4), or within 1e-9."""
+    t, y = series(5, 120)
+    lv, th = [(O.EQ, 6)], [1.1, 1.4]
+    e = E.evaluate(lv, th, t, y, 0.3, m0=m0)
+    o = O.evaluate(lv, th, t, y, 0.3)
+    ld = O.evaluate(lv, th, t, y, 0.3, precision=1)
+    for k in ("loglik", "grad", "mean", "var"):
+        assert rel(e[k], ld[k]) <= max(1e-9, 4 * rel(o[k], ld[k])), k
+
+
+def test_batched_series_match_individual_oracle_runs():
+    rng = np.random.default_rng(3)
+    S, n = 6, 50
+    t = np.cumsum(rng.uniform(0.5, 1.5, (S, n)) * 0.01, axis=1)
+    y = rng.standard_normal((S, n))
+    theta = np.stack([np.exp(rng.uniform(np.log(0.5), np.log(2), S)), np.exp(rng.uniform(np.log(0.5), np.log(5), S))], 1)
+    sig = np.full(S, 0.1)
+    e = E.evaluate([O.MATERN52], theta, t, y, sig, var=False, mean=False)
+    for s in range(S):
+        o = O.evaluate([O.MATERN52], theta[s], t[s], y[s], 0.1, mean=False, var=False)
+        assert rel(e["loglik"][s], o["loglik"]) < 1e-10
+        assert rel(e["grad"][s], o["grad"]) < 1e-9
+
+
+def test_duplicate_time_reported_with_index():
+    with pytest.raises(E.EmuError) as ex:
+        E.evaluate([O.MATERN32], [1.0, 1.0], [0.0, 0.5, 0.5, 1.0], [0.0] * 4, 0.3)
+    assert ex.value.status == 6 and ex.value.block == 2
+
+
+@pytest.mark.parametrize("n,b", [(1, 1), (2, 1), (3, 2), (17, 2), (100, 3), (33, 4), (50, 6), (20, 16), (129, 5)])
+@pytest.mark.parametrize("m0", [0, 2, 3])
+def test_btd_operators_match_thomas(n, b, m0):
+    rng = np.random.default_rng(n * b + m0)
+    A = rng.standard_normal((n, b, b))
+    diag = np.einsum("nij,nkj->nik", A, A) + 4 * b * np.eye(b)
+    upper = rng.standard_normal((max(n - 1, 0), b, b))
+    rhs = rng.standard_normal((n * b, 2))
+    xo, ldo = O.btd_solve(diag, upper, rhs)
+    cdo, cuo, _ = O.btd_selinv(diag, upper)
+    r = E.btd(diag, upper, rhs, selinv=True, m0=m0)
+    assert rel(r["x"], xo) < 1e-12
+    assert abs(r["logdet"] - ldo) <= 1e-12 * max(1.0, abs(ldo))
+    assert rel(r["cdiag"], cdo) < 1e-12
+    if n > 1:
+        assert rel(r["cupper"], cuo) < 1e-12
