@@ -106,9 +106,9 @@ inline BTDFactor factorize(const SymBTD& m, Device& dev = default_device()) {
     detail::pack(m, d, u);
     BTDFactor f{m, 0.0};
     int64_t fb = -1;
-    Device::check(spingp_btd_cr_solve(dev.get(), m.n_blocks, static_cast<int32_t>(m.block_dim), d.data(),
-                                      u.data(), nullptr, 0, nullptr, &f.logdet, &fb),
-                  fb);
+    const int st_ = spingp_btd_cr_solve(dev.get(), m.n_blocks, static_cast<int32_t>(m.block_dim), d.data(),
+                                      u.data(), nullptr, 0, nullptr, &f.logdet, &fb);
+    Device::check(st_, fb);
     return f;
 }
 
@@ -123,9 +123,9 @@ inline Matrix solve(const BTDFactor& f, const Matrix& rhs, Device& dev = default
     Matrix x(rhs.rows(), rhs.cols());
     double ld = 0.0;
     int64_t fb = -1;
-    Device::check(spingp_btd_cr_solve(dev.get(), n, static_cast<int32_t>(b), d.data(), u.data(), rhs.data(),
-                                      static_cast<int32_t>(rhs.cols()), x.data(), &ld, &fb),
-                  fb);
+    const int st_ = spingp_btd_cr_solve(dev.get(), n, static_cast<int32_t>(b), d.data(), u.data(), rhs.data(),
+                                      static_cast<int32_t>(rhs.cols()), x.data(), &ld, &fb);
+    Device::check(st_, fb);
     return x;
 }
 
@@ -147,9 +147,9 @@ inline SymBTD selective_inverse(const BTDFactor& f, Device& dev = default_device
     detail::pack(f.matrix, d, u);
     double ld = 0.0;
     int64_t fb = -1;
-    Device::check(spingp_btd_selinv(dev.get(), n, static_cast<int32_t>(b), d.data(), u.data(), cd.data(),
-                                    n > 1 ? cu.data() : nullptr, &ld, &fb),
-                  fb);
+    const int st_ = spingp_btd_selinv(dev.get(), n, static_cast<int32_t>(b), d.data(), u.data(), cd.data(),
+                                    n > 1 ? cu.data() : nullptr, &ld, &fb);
+    Device::check(st_, fb);
     SymBTD out(n, b);
     for (Index i = 0; i < n; ++i) std::copy(cd.begin() + i * b * b, cd.begin() + (i + 1) * b * b, out.diag[i].data());
     for (Index i = 0; i + 1 < n; ++i)
@@ -173,8 +173,8 @@ inline Matrix matvec(const SymBTD& m, const Matrix& v, Device& dev = default_dev
     std::vector<double> d, u;
     detail::pack(m, d, u);
     Matrix out(v.rows(), v.cols());
-    Device::check(spingp_btd_matvec(dev.get(), n, static_cast<int32_t>(b), d.data(), u.data(), v.data(), out.data()),
-                  -1);
+    const int st_ = spingp_btd_matvec(dev.get(), n, static_cast<int32_t>(b), d.data(), u.data(), v.data(), out.data());
+    Device::check(st_, -1);
     return out;
 }
 

@@ -78,12 +78,12 @@ inline EvalOut eval(const Dataset& d, const KernelSpec& spec, const Hyperparamet
     if (flags & SPINGP_WANT_MEAN) o.mean.resize(n);
     if (flags & SPINGP_WANT_VAR) o.var.resize(n);
     int64_t fb = -1;
-    Device::check(spingp_eval(dev.get(), lv.data(), static_cast<int32_t>(lv.size()), theta.data(),
+    const int st_ = spingp_eval(dev.get(), lv.data(), static_cast<int32_t>(lv.size()), theta.data(),
                               static_cast<int32_t>(theta.size()), d.times.data(), d.values.data(),
                               static_cast<int64_t>(n), std::sqrt(noise.sigma_n2), flags, &o.loglik,
                               o.grad.empty() ? nullptr : o.grad.data(), o.mean.empty() ? nullptr : o.mean.data(),
-                              o.var.empty() ? nullptr : o.var.data(), &fb),
-                  fb);
+                              o.var.empty() ? nullptr : o.var.data(), &fb);
+    Device::check(st_, fb);
     return o;
 }
 
@@ -99,11 +99,11 @@ inline SymBTD assemble_prior_precision(const std::vector<double>& times, const K
     if (n < 1) throw std::invalid_argument("need at least one time");
     std::vector<double> d(static_cast<size_t>(n) * b * b), u(static_cast<size_t>(n - 1) * b * b), y(n, 0.0);
     int64_t fb = -1;
-    Device::check(spingp_assemble(dev.get(), lv.data(), static_cast<int32_t>(lv.size()), theta.data(),
+    const int st_ = spingp_assemble(dev.get(), lv.data(), static_cast<int32_t>(lv.size()), theta.data(),
                                   static_cast<int32_t>(theta.size()), times.data(), y.data(), n,
                                   std::numeric_limits<double>::infinity(), d.data(), n > 1 ? u.data() : nullptr,
-                                  nullptr, &fb),
-                  fb);
+                                  nullptr, &fb);
+    Device::check(st_, fb);
     SymBTD m(n, b);
     for (int64_t i = 0; i < n; ++i) std::copy(d.begin() + i * b * b, d.begin() + (i + 1) * b * b, m.diag[i].data());
     for (int64_t i = 0; i + 1 < n; ++i) std::copy(u.begin() + i * b * b, u.begin() + (i + 1) * b * b, m.upper[i].data());

@@ -28,7 +28,7 @@ int take_status(spingp_ctx* ctx, int64_t* fail_block) {
     CUDA_OK(cudaMemcpy(&h, ctx->d_status, sizeof h, cudaMemcpyDeviceToHost));
     CUDA_OK(cudaMemset(ctx->d_status, 0xFF, sizeof(unsigned long long)));
     if (h == ~0ULL) return SPINGP_OK;
-    if (fail_block) *fail_block = static_cast<int64_t>(h >> 4);
+    if (fail_block) *fail_block = static_cast<int64_t>((h >> 4) & ((1ULL << 56) - 1));
     const int code = static_cast<int>(h & 15ULL);
     static const char* what[] = {"", "pivot block is not positive definite",
                                  "process noise block singular after jitter", "invalid input value",

@@ -344,4 +344,52 @@ SP_UNROLL
         }
 }
 
+// Triangular solves with the Cholesky factor L (lower): forward L X = A, backward L^T X = A.
+template <int B>
+SP_DEV void lsolve(double* X, const double* L, const double* A, int ncol = B) {
+SP_UNROLL
+    for (int c = 0; c < B; ++c) {
+        if (c >= ncol) break;
+SP_UNROLL
+        for (int i = 0; i < B; ++i) {
+            double s = A[i * B + c];
+SP_UNROLL
+            for (int k = 0; k < i; ++k) s = fma(-L[i * B + k], X[k * B + c], s);
+            X[i * B + c] = s / L[i * B + i];
+        }
+    }
+}
+template <int B>
+SP_DEV void lsolve_v(double* x, const double* L, const double* a) {
+SP_UNROLL
+    for (int i = 0; i < B; ++i) {
+        double s = a[i];
+SP_UNROLL
+        for (int k = 0; k < i; ++k) s = fma(-L[i * B + k], x[k], s);
+        x[i] = s / L[i * B + i];
+    }
+}
+template <int B>
+SP_DEV void ltsolve(double* X, const double* L, const double* A) {
+SP_UNROLL
+    for (int c = 0; c < B; ++c)
+SP_UNROLL
+        for (int i = B - 1; i >= 0; --i) {
+            double s = A[i * B + c];
+SP_UNROLL
+            for (int k = i + 1; k < B; ++k) s = fma(-L[k * B + i], X[k * B + c], s);
+            X[i * B + c] = s / L[i * B + i];
+        }
+}
+template <int B>
+SP_DEV void ltsolve_v(double* x, const double* L, const double* a) {
+SP_UNROLL
+    for (int i = B - 1; i >= 0; --i) {
+        double s = a[i];
+SP_UNROLL
+        for (int k = i + 1; k < B; ++k) s = fma(-L[k * B + i], x[k], s);
+        x[i] = s / L[i * B + i];
+    }
+}
+
 }  // namespace spingp_dev

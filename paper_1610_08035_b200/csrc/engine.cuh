@@ -41,15 +41,19 @@
 
 namespace spingp_dev {
 
-// status word: min over (index << 4 | code) of every failure seen on the device
+// status word: min over every failure seen on the device of
+//   (priority << 60) | (index << 4) | code,
+// priority 0 for invalid input (bad value, duplicate time) so that it is reported
+// ahead of the numerical failures it may cause, 1 for numerical failures.
 enum DevStatus {
     ST_NOT_PD = 1, ST_SINGULAR_Q = 2, ST_BAD_ARG = 3, ST_DUPLICATE = 6, ST_NEG_VAR = 8
 };
 
 SP_DEV void report(unsigned long long* st, long long idx, int code) {
-    atomicMin(st, (static_cast<unsigned long long>(idx) << 4) | static_cast<unsigned long long>(code));
+    const unsigned long long prio = (code == ST_BAD_ARG || code == ST_DUPLICATE) ? 0ULL : 1ULL;
+    atomicMin(st, (prio << 60) | (static_cast<unsigned long long>(idx) << 4) |
+                      static_cast<unsigned long long>(code));
 }
-
 
 // level-l block k -> level-0 block index (the separator chain)
 SP_DEV long long to_global(const Geom& g, int lev, long long k) {
@@ -72,7 +76,8 @@ struct Rec {
     static constexpr int N = 3 * B * B + 2 * B + 1;
 };
 // per-step factor layout: fac[(jj * NF + comp) * SK + chunk]
-//   LI: L_j^{-1} packed lower (row-major), Y: L_j^{-1} W_j, Z: L_j^{-1} r_j
+//   LI: the Cholesky factor L_j of S_j, packed lower (row-major),
+//   Y: L_j^{-1} W_j, Z: L_j^{-1} r_j  (triangular solves, never explicit inverses)
 template <int B>
 struct Fac {
     static constexpr int NLI = B * (B + 1) / 2;
@@ -113,10 +118,10 @@ SP_DEV void elim_init(ElimState<B>& es) {
 }
 
 // Eliminate one interior block j with diagonal D, coupling U (to j+1) and rhs.
-// With S = D - T = L L^T and Li = L^{-1}:  X = Li U, Y = Li W, z = Li r.
+// With S = D - T = L L^T:  X = L^{-1} U, Y = L^{-1} W, z = L^{-1} r (forward solves).
 // Schur updates in Gram form (symmetric PSD by construction):
 //   T' = X^T X,  rc' = X^T z,  W' = -X^T Y,  accLL -= Y^T Y,  accrL -= Y^T z.
-// Stores Li (packed), Y and z at fp[comp * SK] for the reverse sweep.
+// Stores L (packed), Y and z at fp[comp * SK] for the reverse sweep.
 template <int B>
 SP_DEV bool elim_block(ElimState<B>& es, const double* D, const double* U, const double* rhs,
                        bool hasL, double* fp, long long SK) {
@@ -127,17 +132,15 @@ SP_UNROLL
     double L[B * B], ld;
     if (!chol<B>(L, S, ld)) return false;
     es.logdet += ld;
-    double Li[B * B];
-    tri_inverse<B>(Li, L);
     double r[B], z[B];
 SP_UNROLL
     for (int i = 0; i < B; ++i) r[i] = rhs[i] - es.rc[i];
-    lmv<B>(z, Li, r);
+    lsolve_v<B>(z, L, r);
     double X[B * B];
-    lmul<B>(X, Li, U);
+    lsolve<B>(X, L, U);
     if (hasL) {
         double Y[B * B], G[B * B];
-        lmul<B>(Y, Li, es.W);
+        lsolve<B>(Y, L, es.W);
         mtm_sym<B>(G, Y, Y);
 SP_UNROLL
         for (int i = 0; i < B * B; ++i) es.accLL[i] -= G[i];
@@ -157,7 +160,7 @@ SP_UNROLL
 SP_UNROLL
     for (int i = 0; i < B; ++i)
 SP_UNROLL
-        for (int j = 0; j <= i; ++j) fp[(Fac<B>::LI + q++) * SK] = Li[i * B + j];
+        for (int j = 0; j <= i; ++j) fp[(Fac<B>::LI + q++) * SK] = L[i * B + j];
 SP_UNROLL
     for (int i = 0; i < B; ++i) fp[(Fac<B>::Z + i) * SK] = z[i];
     return true;
@@ -183,10 +186,10 @@ SP_UNROLL
     r[Rec<B>::LOGDET * SK] = es.logdet;
 }
 
-// Q̃ = Q + jit I = L_Q L_Q^T  ->  Mq = L_Q^{-1} (and log det Q̃).
+// Q̃ = Q + jit I = L_Q L_Q^T  ->  L_Q (and log det Q̃).
 template <int B>
-SP_DEV bool qt_factor(const double* Q, double jit, int breal, double* Mq, double* ldq) {
-    double Qt[B * B], L[B * B];
+SP_DEV bool qt_factor(const double* Q, double jit, int breal, double* L, double* ldq) {
+    double Qt[B * B];
 SP_UNROLL
     for (int i = 0; i < B * B; ++i) Qt[i] = Q[i];
 SP_UNROLL
@@ -195,28 +198,32 @@ SP_UNROLL
     bool ok;
     if (ldq) ok = chol<B>(L, Qt, *ldq);
     else ok = chol_nolog<B>(L, Qt);
-    if (!ok) return false;
-    tri_inverse<B>(Mq, L);
-    return true;
+    return ok;
 }
 
-// Assembly pieces from one step: with Z = Mq Φ,
-//   Φ^T Q̃^{-1} Φ = Z^T Z  and  U = -Φ^T Q̃^{-1} = -Z^T Mq.
+// Q̃^{-1} from its Cholesky factor by substitution (as the oracle's chol_solve(L, I)).
 template <int B>
-SP_DEV void step_assembly(const double* Phi, const double* Mq, double* PQP, double* U) {
-    double Z[B * B];
-    lmul<B>(Z, Mq, Phi);
+SP_DEV void chol_inv_solve(double* Qinv, const double* L) {
+    double I[B * B], X[B * B];
+SP_UNROLL
+    for (int i = 0; i < B * B; ++i) I[i] = (i % (B + 1) == 0) ? 1.0 : 0.0;
+    lsolve<B>(X, L, I);
+    ltsolve<B>(Qinv, L, X);
+    msym<B>(Qinv);
+}
+
+// Assembly pieces from one step: with Z = L_Q^{-1} Φ (forward solve),
+//   Φ^T Q̃^{-1} Φ = Z^T Z  and  U = -Φ^T Q̃^{-1} = -(L_Q^{-T} Z)^T.
+template <int B>
+SP_DEV void step_assembly(const double* Phi, const double* LQ, double* PQP, double* U) {
+    double Z[B * B], W[B * B];
+    lsolve<B>(Z, LQ, Phi);
     mtm_sym<B>(PQP, Z, Z);
-    // U = -Z^T Mq
+    ltsolve<B>(W, LQ, Z);
 SP_UNROLL
     for (int i = 0; i < B; ++i)
 SP_UNROLL
-        for (int j = 0; j < B; ++j) {
-            double s = 0.0;
-SP_UNROLL
-            for (int k = j; k < B; ++k) s = fma(Z[k * B + i], Mq[k * B + j], s);
-            U[i * B + j] = -s;
-        }
+        for (int j = 0; j < B; ++j) U[i * B + j] = -W[j * B + i];
 }
 
 // ======================================================= level 0 (fused) ======
@@ -259,7 +266,7 @@ __global__ void __launch_bounds__(128) k_fwd0(ModelDesc md, const double* __rest
         return;
     }
     double Qinv[B * B];  // Q̃_j^{-1} of the current block
-    ltl<B>(Qinv, Mq);
+    chol_inv_solve<B>(Qinv, Mq);
     ElimState<B> es;
     elim_init<B>(es);
     if (hasL) {  // P_{s, s-1} = U_{s-1}^T
@@ -304,7 +311,7 @@ SP_UNROLL
             report(status, gbase + j, ST_NOT_PD);
             return;
         }
-        ltl<B>(Qinv, Mqn);
+        chol_inv_solve<B>(Qinv, Mqn);
     }
     // separator R = en - 1
     double D[B * B], Rr[B];
@@ -452,10 +459,10 @@ SP_UNROLL
         report(status, static_cast<long long>(s) * geo.n[0] + to_global(geo, L, 0), ST_NOT_PD);
         return;
     }
-    tri_inverse<B>(Li, Lc);
-    ltl<B>(C, Li);
-    lmv<B>(z, Li, r);
-    ltmv<B>(x, Li, z);
+    chol_inv_solve<B>(C, Lc);
+    lsolve_v<B>(z, Lc, r);
+    ltsolve_v<B>(x, Lc, z);
+    (void)Li;
     const long long Sn = geo.S;
 SP_UNROLL
     for (int q = 0; q < B; ++q) sol[(Sol<B>::X + q) * Sn + s] = x[q];
@@ -497,13 +504,13 @@ SP_UNROLL
     mzero<B>(sd.CLR);
 }
 
-// One step of the reverse sweep.  With x_j = L^{-T}(z - X x_n - Y x_L) + ε_j,
-// Cov ε_j = S_j^{-1} = L^{-T} L^{-1}:
+// One step of the reverse sweep (all L^{-1}, L^{-T} by substitution).  With
+// x_j = L^{-T}(z - X x_n - Y x_L) + ε_j,  Cov ε_j = S_j^{-1} = L^{-T} L^{-1}:
 //   P1 = X C_nL + Y C_LL,   C_jL = -L^{-T} P1
 //   P2 = X C_nn + Y C_Ln,   C_jn = -L^{-T} P2
 //   C_jj = L^{-T} (I + P2 X^T + P1 Y^T) L^{-1}
 template <int B>
-SP_DEV void back_step(const double* Li, const double* Y, const double* z, const double* X,
+SP_DEV void back_step(const double* L, const double* Y, const double* z, const double* X,
                       bool hasL, bool needC, const SepData<B>& sd, const double* xn,
                       const double* Cnn, const double* CnL, double* xj, double* CjL, double* Cjn,
                       double* Cjj) {
@@ -516,7 +523,7 @@ SP_UNROLL
 SP_UNROLL
         for (int i = 0; i < B; ++i) a[i] -= tmp[i];
     }
-    ltmv<B>(xj, Li, a);
+    ltsolve_v<B>(xj, L, a);
     if (!needC) return;
     double P1[B * B], P2[B * B], M[B * B], N[B * B];
     mm<B>(P1, X, CnL);
@@ -529,8 +536,8 @@ SP_UNROLL
 SP_UNROLL
         for (int i = 0; i < B * B; ++i) P2[i] += M[i];
     }
-    ltmul<B>(CjL, Li, P1);
-    ltmul<B>(Cjn, Li, P2);
+    ltsolve<B>(CjL, L, P1);
+    ltsolve<B>(Cjn, L, P2);
 SP_UNROLL
     for (int i = 0; i < B * B; ++i) {
         CjL[i] = -CjL[i];
@@ -545,12 +552,23 @@ SP_UNROLL
 SP_UNROLL
     for (int i = 0; i < B; ++i) M[i * B + i] += 1.0;
     msym<B>(M);
-    sandwich<B>(Cjj, Li, M);
+    // Cjj = L^{-T} M L^{-1} = L^{-T} (L^{-T} M)^T
+    ltsolve<B>(N, L, M);
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j < i; ++j) {
+            const double tmp2 = N[i * B + j];
+            N[i * B + j] = N[j * B + i];
+            N[j * B + i] = tmp2;
+        }
+    ltsolve<B>(Cjj, L, N);
+    msym<B>(Cjj);
 }
 
 template <int B>
 SP_DEV void load_fac(const double* fp, long long SK, bool hasL, double* Li, double* Y, double* z) {
-    int q = 0;
+    int q = 0;  // Li receives the packed Cholesky factor L_j
 SP_UNROLL
     for (int i = 0; i < B; ++i)
 SP_UNROLL
@@ -630,7 +648,7 @@ SP_UNROLL
         double Li[B * B], Y[B * B], z[B], U[B * B], X[B * B];
         load_fac<B>(fac + (j - st) * Fac<B>::N * SK + g, SK, hasL, Li, Y, z);
         src.upper(s, j, U);
-        lmul<B>(X, Li, U);
+        lsolve<B>(X, Li, U);
         double xj[B], CjL[B * B], Cjn[B * B], Cjj[B * B];
         back_step<B>(Li, Y, z, X, hasL, needC, sd, xn, Cnn, CnL, xj, CjL, Cjn, Cjj);
         sink.put(s, j, xj, Cjj, needC);
@@ -689,15 +707,31 @@ SP_UNROLL
 }
 
 // Likelihood / gradient terms of step i with transition Φ
-// (Φ := 0 at the anchor), Mq = L_Q̃^{-1}, previous block (xp, Cpp) and
+// (Φ := 0 at the anchor), L_Q = chol(Q̃), previous block (xp, Cpp) and
 // cross-covariance Cpc = C_{i-1,i}:
-//   ē = x_c - Φ x_p,  fe += |Mq ē|²
+//   ē = x_c - Φ x_p,  fe += |L_Q^{-1} ē|²
 //   E = C_cc - Φ C_pc - (Φ C_pc)^T + Φ C_pp Φ^T + ē ē^T
 //   Zc = C_pc - C_pp Φ^T + x_p ē^T
 //   M = Q̃^{-1}(E - Q̃)Q̃^{-1},  Bm = Zc Q̃^{-1};  T::grad adds ½Tr(M dQ̃) + Tr(dΦ Bm).
+// Every Q̃^{-1} is applied by forward/backward substitution with L_Q.
+template <int B>
+SP_DEV void qinv_apply_right(double* out, const double* LQ, const double* A) {  // out = A Q̃^{-1}
+    double At[B * B], X[B * B], Y[B * B];
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j < B; ++j) At[i * B + j] = A[j * B + i];
+    lsolve<B>(X, LQ, At);
+    ltsolve<B>(Y, LQ, X);  // Q̃^{-1} A^T
+SP_UNROLL
+    for (int i = 0; i < B; ++i)
+SP_UNROLL
+        for (int j = 0; j < B; ++j) out[i * B + j] = Y[j * B + i];
+}
+
 template <class T>
 SP_DEV void step_terms(const ModelDesc& md, const double* rp, double dt, const double* Phi,
-                       const double* Qraw, const double* Mq, const double* xc, const double* Ccc,
+                       const double* Qraw, const double* LQ, const double* xc, const double* Ccc,
                        const double* xp, const double* Cpp, const double* Cpc, bool anchor,
                        bool grad, double& fe, double* g) {
     constexpr int B = T::B;
@@ -710,7 +744,7 @@ SP_UNROLL
 SP_UNROLL
         for (int i = 0; i < B; ++i) e[i] = xc[i] - tmp[i];
     }
-    lmv<B>(tmp, Mq, e);
+    lsolve_v<B>(tmp, LQ, e);
     double q = 0.0;
 SP_UNROLL
     for (int i = 0; i < B; ++i) q += tmp[i] * tmp[i];
@@ -739,49 +773,21 @@ SP_UNROLL
         for (int i = 0; i < B; ++i)
 SP_UNROLL
             for (int j = 0; j < B; ++j) Z[i * B + j] = Cpc[i * B + j] - Y[i * B + j] + xp[i] * e[j];
-        // Bm = Zc Q̃^{-1} = (Zc Mq^T) Mq
-        double ZM[B * B];
-SP_UNROLL
-        for (int i = 0; i < B; ++i)
-SP_UNROLL
-            for (int j = 0; j < B; ++j) {
-                double s = 0.0;
-SP_UNROLL
-                for (int k = 0; k <= j; ++k) s = fma(Z[i * B + k], Mq[j * B + k], s);
-                ZM[i * B + j] = s;
-            }
-SP_UNROLL
-        for (int i = 0; i < B; ++i)
-SP_UNROLL
-            for (int j = 0; j < B; ++j) {
-                double s = 0.0;
-SP_UNROLL
-                for (int k = j; k < B; ++k) s = fma(ZM[i * B + k], Mq[k * B + j], s);
-                Bm[i * B + j] = s;
-            }
+        qinv_apply_right<B>(Bm, LQ, Z);
     }
-    // E - Q̃ (padding states: Q̃ = 1 there and E = 0, but their M rows are unused)
+    // E - Q̃ (padding states have Q̃ = 1 and E = 0; their rows of M are never read)
 SP_UNROLL
     for (int i = 0; i < B * B; ++i) E[i] -= Qraw[i];
 SP_UNROLL
     for (int i = 0; i < B; ++i)
         if (i < md.b) E[i * B + i] -= jit;
     msym<B>(E);
-    // M = Mq^T Mq (E - Q̃) Mq^T Mq = Mq^T [Mq (E - Q̃) Mq^T] Mq
-    double Inner[B * B];
-    lmul<B>(X, Mq, E);  // Mq (E - Q̃)
-SP_UNROLL
-    for (int i = 0; i < B; ++i)
-SP_UNROLL
-        for (int j = 0; j <= i; ++j) {
-            double s = 0.0;
-SP_UNROLL
-            for (int k = 0; k <= j; ++k) s = fma(X[i * B + k], Mq[j * B + k], s);
-            Inner[i * B + j] = s;
-            Inner[j * B + i] = s;
-        }
-    sandwich<B>(Y, Mq, Inner);
-    T::grad(md, rp, dt, Phi, Qraw, Y, Bm, g);
+    // M = Q̃^{-1} (E - Q̃) Q̃^{-1}
+    lsolve<B>(X, LQ, E);
+    ltsolve<B>(Y, LQ, X);         // Q̃^{-1}(E - Q̃)
+    qinv_apply_right<B>(X, LQ, Y);
+    msym<B>(X);
+    T::grad(md, rp, dt, Phi, Qraw, X, Bm, g);
 }
 
 template <class T>
@@ -833,7 +839,7 @@ SP_UNROLL
         double Li[B * B], Y[B * B], z[B], U[B * B], X[B * B], PQP[B * B];
         load_fac<B>(fac + (j - st) * Fac<B>::N * SK + g, SK, hasL, Li, Y, z);
         step_assembly<B>(Phn, Mqn, PQP, U);
-        lmul<B>(X, Li, U);
+        lsolve<B>(X, Li, U);
         double xj[B], CjL[B * B], Cjn[B * B], Cjj[B * B];
         back_step<B>(Li, Y, z, X, hasL, needC, sd, xn, Cnn, CnL, xj, CjL, Cjn, Cjj);
         point_out<T>(md, outs, gbase + nb, ys[nb], is2, sig, xn, Cnn, fy, noise, status);
@@ -1022,7 +1028,7 @@ __global__ void __launch_bounds__(128) k_assemble(ModelDesc md, const double* __
         report(status, i, ST_SINGULAR_Q);
         return;
     }
-    ltl<B>(D, Mq);
+    chol_inv_solve<B>(D, Mq);
     if (i + 1 < n) {
         const double dtn = t[i + 1] - t[i];
         if (!(dtn > 0.0) || !isfinite(dtn)) {

@@ -4,7 +4,9 @@
 // C++ API of include/spingp/kernels.hpp for the reference's state_space_of.
 #include "host_model.hpp"
 
+#include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstring>
 #include <numbers>
 #include <stdexcept>
@@ -16,6 +18,113 @@ using namespace spingp_dev;
 namespace spingp_host {
 
 namespace {
+// Device constants of the modal EQ realisation (kernels.hpp:202-321), computed in
+// x87 long double and rounded once: the spectral-factor roots (a_p, c_p) at unit
+// lengthscale, the unit-variance Pinf = s0 G(inf) and s0 = 1/k0.  G(inf) =
+// ∫_0^inf e^{Au} g g^T e^{A^T u} du in closed form (2x2 blocks
+// ½ [[C- + C+, S- - S+], [-(S+ + S-), C- - C+]], C± + i S± = -1/(α + iβ±),
+// α = a_p + a_q, β± = c_p ± c_q) — the exact solution of the reference's Lyapunov
+// equation (matexp.hpp:37-52).  The EQ Pinf is ill-conditioned (cond ~1e6 at order 6)
+// and k0 = H G H^T cancels by ~1e4, so double-precision constants would perturb the
+// small eigen-directions of every Q̃ well above the fp64 floor of the reference.
+struct EqConst {
+    std::vector<double> H;   // emission row (partial-fraction residues)
+    std::vector<double> ac;  // a_0, c_0, a_1, c_1, ...
+    std::vector<double> P1;  // J x J
+    double s0 = 0.0;
+};
+EqConst eq_constants(int J) {
+    using R = long double;
+    using C = std::complex<R>;
+    // roots of T_J(J z) J!/J^J (Weierstrass iteration), then 4+ Newton steps on T_J
+    std::vector<R> c(J);
+    for (int k = 0; k < J; ++k) {
+        R v = 1;
+        for (int i = k + 1; i <= J; ++i) v *= R(i);
+        c[k] = v / std::pow(R(J), R(J - k));
+    }
+    auto poly = [&](C z) {
+        C s = 1;
+        for (int k = J - 1; k >= 0; --k) s = s * z + c[k];
+        return s;
+    };
+    std::vector<C> z(J);
+    for (int k = 0; k < J; ++k) z[k] = std::pow(C(0.4L, 0.9L), k);
+    for (int it = 0; it < 2000; ++it) {
+        R ch = 0;
+        for (int k = 0; k < J; ++k) {
+            C den = 1;
+            for (int m = 0; m < J; ++m)
+                if (m != k) den *= (z[k] - z[m]);
+            const C st = poly(z[k]) / den;
+            z[k] -= st;
+            ch = std::max(ch, std::abs(st));
+        }
+        if (ch < 1e-19L) break;
+    }
+    std::vector<C> roots;
+    for (int k = 0; k < J; ++k) {
+        C y = z[k] * R(J);
+        for (int it = 0; it < 8; ++it) {
+            C t = 1, tp = 0, term = 1;
+            for (int i = 1; i <= J; ++i) {
+                tp += term;
+                term *= y / R(i);
+                t += term;
+            }
+            if (std::abs(tp) == 0) break;
+            y -= t / tp;
+        }
+        C r = std::sqrt(R(-2) * y);
+        if (r.real() > 0) r = -r;
+        roots.push_back(r);
+    }
+    std::vector<C> up;
+    for (C r : roots)
+        if (r.imag() > 0) up.push_back(r);
+    if (2 * up.size() != roots.size()) throw std::runtime_error("eq kernel: roots did not split into conjugate pairs");
+    std::sort(up.begin(), up.end(),
+              [](C a, C b) { return a.real() != b.real() ? a.real() < b.real() : a.imag() < b.imag(); });
+    std::vector<R> H(J), G(static_cast<size_t>(J) * J);
+    for (size_t p = 0; p < up.size(); ++p) {
+        C den = 1;
+        for (C o : roots)
+            if (std::abs(o - up[p]) > 1e-12L) den *= (up[p] - o);
+        const C res = C(1) / den;
+        H[2 * p] = 2 * res.real();
+        H[2 * p + 1] = 2 * res.imag();
+    }
+    auto inv = [](R a, R b, R& re, R& im) {
+        const R d = a * a + b * b;
+        re = -a / d;
+        im = b / d;
+    };
+    for (int p = 0; p < J / 2; ++p)
+        for (int q = 0; q < J / 2; ++q) {
+            const R al = up[p].real() + up[q].real();
+            R cm, sm, cp, sp;
+            inv(al, up[p].imag() - up[q].imag(), cm, sm);
+            inv(al, up[p].imag() + up[q].imag(), cp, sp);
+            G[(2 * p) * J + 2 * q] = (cm + cp) / 2;
+            G[(2 * p) * J + 2 * q + 1] = (sm - sp) / 2;
+            G[(2 * p + 1) * J + 2 * q] = -(sp + sm) / 2;
+            G[(2 * p + 1) * J + 2 * q + 1] = (cm - cp) / 2;
+        }
+    R k0 = 0;
+    for (int i = 0; i < J; ++i)
+        for (int j = 0; j < J; ++j) k0 += H[i] * G[i * J + j] * H[j];
+    EqConst out;
+    for (R v : H) out.H.push_back(static_cast<double>(v));
+    for (const C& r : up) {
+        out.ac.push_back(static_cast<double>(r.real()));
+        out.ac.push_back(static_cast<double>(r.imag()));
+    }
+    const R s0 = R(1) / k0;
+    for (R v : G) out.P1.push_back(static_cast<double>(v * s0));
+    out.s0 = static_cast<double>(s0);
+    return out;
+}
+
 int leaf_dim(const spingp_leaf& l) {
     switch (l.type) {
         case SPINGP_MATERN12: return 1;
@@ -75,6 +184,7 @@ HostModel build_model(const spingp_leaf* leaves, int32_t n_leaves, int32_t n_the
     d.b = off;
     d.nleaves = n_leaves;
     d.nt = th;
+    std::vector<std::pair<int, std::vector<double>>> eq_h;
     rec = 2 + th;
     for (int l = 0; l < n_leaves; ++l) {
         d.rec[l] = rec;
@@ -87,14 +197,12 @@ HostModel build_model(const spingp_leaf* leaves, int32_t n_leaves, int32_t n_the
         if (leaves[l].type == SPINGP_EQ) {
             // unit variance / unit lengthscale model: roots (a, c) and P1
             const int J = leaves[l].order;
-            const auto m = spingp::eq_approx_ss(1.0, 1.0, J);
+            const EqConst ec = eq_constants(J);
+            eq_h.emplace_back(l, ec.H);
             d.eqc[l] = static_cast<int>(hm.eqconst.size());
-            for (int p = 0; p < J / 2; ++p) {
-                hm.eqconst.push_back(m.F(2 * p, 2 * p));
-                hm.eqconst.push_back(m.F(2 * p, 2 * p + 1));
-            }
-            for (int i = 0; i < J; ++i)
-                for (int j = 0; j < J; ++j) hm.eqconst.push_back(m.Pinf(i, j));
+            hm.eqconst.insert(hm.eqconst.end(), ec.ac.begin(), ec.ac.end());
+            hm.eqconst.insert(hm.eqconst.end(), ec.P1.begin(), ec.P1.end());
+            hm.eqconst.push_back(ec.s0);
         }
     }
     hm.rec_stride = rec;
@@ -102,6 +210,8 @@ HostModel build_model(const spingp_leaf* leaves, int32_t n_leaves, int32_t n_the
     // emission row
     const auto ssm = spingp::state_space_of(spec_of(leaves, n_leaves), spingp::default_theta(spec_of(leaves, n_leaves)));
     for (int i = 0; i < kMaxB; ++i) d.H[i] = i < hm.b ? ssm.H(i) : 0.0;
+    for (const auto& [l, Hl] : eq_h)  // EQ emission rows from the extended-precision constants
+        for (size_t i = 0; i < Hl.size(); ++i) d.H[d.off[l] + i] = Hl[i];
     hm.single_matern = n_leaves == 1 && leaves[0].type <= SPINGP_MATERN52;
     return hm;
 }

@@ -29,7 +29,71 @@
 
 namespace spingp_dev {
 
+// ------------------------------------------------------------ accurate Q --
+// The reference evaluates Q = Pinf - Φ Pinf Φ^T (kernels.hpp:402), which cancels
+// catastrophically when Δt is small against the lengthscale (Q ~ Δt^{2b-1} while
+// Pinf ~ 1): its fp64 error is ~eps·|Pinf|, far above the small eigenvalues of Q
+// (SURVEY.md App. A).  The device evaluates the SAME matrix through its integral
+// form Q(Δt) = ∫_0^Δt e^{Fs} L q L^T e^{F^T s} ds in closed form, entry by entry,
+// with no cancellation; its θ-derivatives follow from the same form.
+
+// R_m(x) = e^{-x} Σ_{j>m} x^j / j!  (= 1 - e^{-x} Σ_{j<=m} x^j/j!), m = 0..M, x >= 0.
+template <int M>
+SP_DEV void exp_tails(double x, double* R) {
+    const double ex = exp(-x);
+    double pw[M + 1];  // x^m / m!
+    pw[0] = 1.0;
+#pragma unroll
+    for (int m = 1; m <= M; ++m) pw[m] = pw[m - 1] * x / double(m);
+    if (x < 6.0) {
+        double term = pw[M] * x / double(M + 1), s = 0.0;
+#pragma unroll 4
+        for (int k = 0; k < 48; ++k) {
+            s += term;
+            term *= x / double(M + 2 + k);
+        }
+        R[M] = ex * s;
+#pragma unroll
+        for (int m = M; m >= 1; --m) R[m - 1] = R[m] + ex * pw[m];
+    } else {
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m <= M; ++m) {
+            acc += pw[m];
+            R[m] = 1.0 - ex * acc;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ Matérn --
+// Unit-λ companion model F1 = F(λ=1) (kernels.hpp:137-200) with F(λ) = λ T F1 T^{-1},
+// T = diag(1, λ, λ², ...).  The noise column e^{F1 s} e_b = e^{-s} Σ_k c_k s^k and the
+// unit spectral density q1 (F1 P1 + P1 F1^T + q1 e_b e_b^T = 0 with the unit-variance Pinf):
+//   Matérn-1/2: c0 = [1];                                   q1 = 2
+//   Matérn-3/2: c0 = [0,1], c1 = [1,-1];                    q1 = 4
+//   Matérn-5/2: c0 = [0,0,1], c1 = [0,1,-2], c2 = ½[1,-1,1];  q1 = 16/3
+// Then Q(Δt) = var T Q1(λΔt) T,  Q1(u)_ij = q1 Σ_kl c_k[i] c_l[j] I_{k+l}(u),
+// I_m(u) = ∫_0^u s^m e^{-2s} ds = m!/2^{m+1} R_m(2u),
+// and dQ/dλ = ((i+j)/λ) Q_ij + var Δt q1 (T v(u))(T v(u))^T, v(u) = e^{-u} Σ_k c_k u^k.
+template <int D>
+SP_DEV double matern_c(int k, int i) {
+    if constexpr (D == 1) {
+        return 1.0;
+    } else if constexpr (D == 2) {
+        return k == 0 ? (i == 1 ? 1.0 : 0.0) : (i == 0 ? 1.0 : -1.0);
+    } else {
+        if (k == 0) return i == 2 ? 1.0 : 0.0;
+        if (k == 1) return i == 0 ? 0.0 : (i == 1 ? 1.0 : -2.0);
+        return i == 1 ? -0.5 : 0.5;
+    }
+}
+template <int D>
+SP_DEV double matern_q1() {
+    if constexpr (D == 1) return 2.0;
+    else if constexpr (D == 2) return 4.0;
+    else return 16.0 / 3.0;
+}
+
 // Block of dimension D at offset o inside LD x LD arrays.
 template <int D, int LD>
 SP_DEV void matern_block(const double* lr, double dt, int o, double* Phi, double* Q) {
@@ -56,18 +120,16 @@ SP_DEV void matern_block(const double* lr, double dt, int o, double* Phi, double
             }
         return;
     }
-    // Φ = e^{-λΔt} (I + NΔt + N²Δt²/2), N = F + λI
+    // Φ = e^{-λΔt} (I + NΔt + N²Δt²/2), N = F + λI nilpotent
     const double e = exp(-lam * dt);
     double ph[D * D];
     if constexpr (D == 1) {
         ph[0] = e;
     } else if constexpr (D == 2) {
-        // N = [[λ, 1], [-λ², -λ]]
         const double x = lam * dt;
         ph[0] = e * (1.0 + x); ph[1] = e * dt;
         ph[2] = -e * lam * x; ph[3] = e * (1.0 - x);
     } else {
-        // N = [[λ,1,0],[0,λ,1],[-λ³,-3λ²,-2λ]]; N² = [[λ²,2λ,1],[-λ³,-2λ²,-λ],[λ⁴,λ³,λ²]]... computed generically
         const double l2 = lam * lam, l3 = l2 * lam;
         const double N[9] = {lam, 1.0, 0.0, 0.0, lam, 1.0, -l3, -3.0 * l2, -2.0 * lam};
         double N2[9];
@@ -76,18 +138,42 @@ SP_DEV void matern_block(const double* lr, double dt, int o, double* Phi, double
 #pragma unroll
         for (int k = 0; k < 9; ++k) ph[k] = e * ((k % 4 == 0 ? 1.0 : 0.0) + dt * N[k] + h * N2[k]);
     }
-    // Q = Pinf - Φ Pinf Φ^T (symmetrised)
-    double X[D * D], Y[D * D];
-    mm<D>(X, ph, P);
-    mmt<D>(Y, X, ph);
+    // Q = var T Q1(λΔt) T (cancellation-free integral form)
+    constexpr int M = 2 * (D - 1);
+    double R[M + 1];
+    const double u = lam * dt;
+    exp_tails<M>(2.0 * u, R);
+    double I[M + 1];
+    {
+        double f = 0.5;  // m! / 2^{m+1}
+#pragma unroll
+        for (int m = 0; m <= M; ++m) {
+            I[m] = f * R[m];
+            f *= double(m + 1) * 0.5;
+        }
+    }
+    double tp[D];
+    tp[0] = 1.0;
+#pragma unroll
+    for (int i = 1; i < D; ++i) tp[i] = tp[i - 1] * lam;
+    const double q1 = matern_q1<D>();
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-            Phi[(o + i) * LD + o + j] = ph[i * D + j];
-            Q[(o + i) * LD + o + j] =
-                0.5 * ((P[i * D + j] - Y[i * D + j]) + (P[j * D + i] - Y[j * D + i]));
+        for (int j = 0; j <= i; ++j) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k)
+#pragma unroll
+                for (int l = 0; l < D; ++l) s += matern_c<D>(k, i) * matern_c<D>(l, j) * I[k + l];
+            const double v = var * q1 * s * tp[i] * tp[j];
+            Q[(o + i) * LD + o + j] = v;
+            Q[(o + j) * LD + o + i] = v;
         }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) Phi[(o + i) * LD + o + j] = ph[i * D + j];
 }
 
 // g[var] += ½Tr(M dQ̃_var) ; g[len] += ½Tr(M dQ̃_len) + Tr(dΦ_len Bm)
@@ -96,7 +182,7 @@ template <int D, int LD>
 SP_DEV void matern_grad(const double* lr, double dt, int o, const double* Phi, const double* Q,
                         const double* M, const double* Bm, double& gvar, double& glen) {
     const double var = lr[0], len = lr[1], lam = lr[2];
-    double P[D * D], dP[D * D], ph[D * D], Mb[D * D], Bb[D * D], Qb[D * D];
+    double ph[D * D], Mb[D * D], Bb[D * D], Qb[D * D];
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
@@ -106,26 +192,43 @@ SP_DEV void matern_grad(const double* lr, double dt, int o, const double* Phi, c
             Bb[i * D + j] = Bm[(o + i) * LD + o + j];
             Qb[i * D + j] = Q[(o + i) * LD + o + j];
         }
-    if constexpr (D == 1) {
-        P[0] = var;
-    } else if constexpr (D == 2) {
-        P[0] = var; P[1] = 0.0; P[2] = 0.0; P[3] = var * lam * lam;
-    } else {
-        const double kap = lam * lam / 3.0;
-        P[0] = var; P[1] = 0.0; P[2] = -var * kap;
-        P[3] = 0.0; P[4] = var * kap; P[5] = 0.0;
-        P[6] = -var * kap; P[7] = 0.0; P[8] = var * lam * lam * lam * lam;
-    }
     // d/dvar: dΦ = 0, dQ = Q / var (also at the anchor, where Q = Pinf)
     gvar += 0.5 * mtrprod<D>(Mb, Qb) / var;
-    // d/dlen: dPinf_ij = -(i+j)/ℓ Pinf_ij
+    // d/dℓ = -(λ/ℓ) d/dλ.  dQ/dλ_ij = ((i+j)/λ) Q_ij + var Δt q1 (T v)_i (T v)_j
+    double dQ[D * D];
+    const double c = -lam / len;
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
-        for (int j = 0; j < D; ++j) dP[i * D + j] = -double(i + j) / len * P[i * D + j];
-    if (dt < 0.0) {
-        glen += 0.5 * mtrprod<D>(Mb, dP);
+        for (int j = 0; j < D; ++j) dQ[i * D + j] = c * double(i + j) / lam * Qb[i * D + j];
+    if (dt < 0.0) {  // anchor: dPinf/dℓ_ij = -(i+j)/ℓ Pinf_ij
+        glen += 0.5 * mtrprod<D>(Mb, dQ);
         return;
+    }
+    {
+        const double u = lam * dt, eu = exp(-u);
+        double v[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double s = 0.0, pw = 1.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                s += matern_c<D>(k, i) * pw;  // c_k already carries the 1/k!
+                pw *= u;
+            }
+            v[i] = eu * s;
+        }
+        double tp = 1.0, tv[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            tv[i] = tp * v[i];
+            tp *= lam;
+        }
+        const double w = c * var * dt * matern_q1<D>();
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) dQ[i * D + j] += w * tv[i] * tv[j];
     }
     // dΦ = -(1/ℓ)[K, Φ] - (Δt/ℓ) F Φ
     double F[D * D];
@@ -145,31 +248,38 @@ SP_DEV void matern_grad(const double* lr, double dt, int o, const double* Phi, c
 #pragma unroll
         for (int j = 0; j < D; ++j)
             dph[i * D + j] = c1 * double(i - j) * ph[i * D + j] + c2 * FP[i * D + j];
-    // dQ = dP - dΦ P Φ^T - Φ dP Φ^T - Φ P dΦ^T   (symmetrised)
-    double X[D * D], Y[D * D], dQ[D * D];
-    mm<D>(X, dph, P);     // dΦ P
-    mmt<D>(Y, X, ph);     // dΦ P Φ^T
-    double Z[D * D], W[D * D];
-    mm<D>(Z, ph, dP);     // Φ dP
-    mmt<D>(W, Z, ph);     // Φ dP Φ^T
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-#pragma unroll
-        for (int j = 0; j < D; ++j)
-            dQ[i * D + j] = dP[i * D + j] - Y[i * D + j] - W[i * D + j] - Y[j * D + i];
-    msym<D>(dQ);
     glen += 0.5 * mtrprod<D>(Mb, dQ) + mtrprod<D>(dph, Bb);
 }
 
 // ---------------------------------------------------------------------- EQ --
-// Generic-path only (dynamic offsets, LD = padded B).
+// Modal EQ (kernels.hpp:286-306): F = A/ℓ with 2x2 blocks A_p = [[a_p, c_p], [-c_p, a_p]],
+// noise gain g = e_first of every pair, Pinf = var s0 p1 (s0 = 1/k0, kernels.hpp:310-315).
+// Q(Δt) = var s0 G(Δt/ℓ),  G(τ) = ∫_0^τ e^{Au} g g^T e^{A^T u} du, block (p,q):
+//   ½ [[C- + C+, S- - S+], [-(S+ + S-), C- - C+]],  C± + i S± = ∫_0^τ e^{(α + iβ±)u} du,
+//   α = a_p + a_q, β± = c_p ± c_q  — evaluated with a complex expm1 (no cancellation).
+// dQ/dℓ = -var s0 (Δt/ℓ²) e^{Aτ} g g^T e^{A^T τ}; dQ/dvar = Q/var.
+// Constants at desc.eqconst + eqc[l]: (a_p, c_p) pairs, P1 = s0 p1 (J*J), s0.
+SP_DEV void phi1_int(double a, double b, double tau, double& re, double& im) {
+    // (e^{(a+ib)τ} - 1) / (a + ib)
+    const double x = a * tau, y = b * tau;
+    double sy, cy;
+    sincos(y, &sy, &cy);
+    const double sh = sin(0.5 * y);
+    const double er = expm1(x) * cy - 2.0 * sh * sh;  // Re(e^w - 1)
+    const double ei = exp(x) * sy;                     // Im(e^w - 1)
+    const double den = a * a + b * b;
+    re = (er * a + ei * b) / den;
+    im = (ei * a - er * b) / den;
+}
+
 template <int LD>
 SP_DEV void eq_block(const ModelDesc& md, int l, const double* lr, double dt, double* Phi,
                      double* Q) {
     const int o = md.off[l], J = md.dim[l];
     const double var = lr[0], len = lr[1];
     const double* ac = md.eqconst + md.eqc[l];
-    const double* P1 = ac + J;  // J/2 pairs of (a, c), then P1
+    const double* P1 = ac + J;  // J/2 pairs of (a, c), then P1, then s0
+    const double s0 = P1[J * J];
     if (dt < 0.0) {
         for (int i = 0; i < J; ++i)
             for (int j = 0; j < J; ++j) {
@@ -180,31 +290,35 @@ SP_DEV void eq_block(const ModelDesc& md, int l, const double* lr, double dt, do
     }
     for (int i = 0; i < J; ++i)
         for (int j = 0; j < J; ++j) Phi[(o + i) * LD + o + j] = 0.0;
+    const double tau = dt / len;
     for (int p = 0; p < J / 2; ++p) {
         const double a = ac[2 * p], c = ac[2 * p + 1];
-        const double rho = exp(a * dt / len);
+        const double rho = exp(a * tau);
         double sn, cs;
-        sincos(c * dt / len, &sn, &cs);
+        sincos(c * tau, &sn, &cs);
         const int k = o + 2 * p;
         Phi[k * LD + k] = rho * cs;
         Phi[k * LD + k + 1] = rho * sn;
         Phi[(k + 1) * LD + k] = -rho * sn;
         Phi[(k + 1) * LD + k + 1] = rho * cs;
     }
-    // Q = var (P1 - Φ P1 Φ^T), Φ 2x2-block diagonal
-    for (int i = 0; i < J; ++i)
-        for (int j = 0; j <= i; ++j) {
-            const int pi = i & ~1, pj = j & ~1;
-            double s = 0.0;
-            for (int u = 0; u < 2; ++u)
-                for (int v = 0; v < 2; ++v)
-                    s += Phi[(o + i) * LD + o + pi + u] * P1[(pi + u) * J + pj + v] *
-                         Phi[(o + j) * LD + o + pj + v];
-            const double qij = var * (P1[i * J + j] - s);
-            const double qji = var * (P1[j * J + i] - s);
-            const double v = 0.5 * (qij + qji);
-            Q[(o + i) * LD + o + j] = v;
-            Q[(o + j) * LD + o + i] = v;
+    const double w = 0.5 * var * s0;
+    for (int p = 0; p < J / 2; ++p)
+        for (int q = 0; q <= p; ++q) {
+            const double al = ac[2 * p] + ac[2 * q];
+            double cm, sm, cp, sp;
+            phi1_int(al, ac[2 * p + 1] - ac[2 * q + 1], tau, cm, sm);
+            phi1_int(al, ac[2 * p + 1] + ac[2 * q + 1], tau, cp, sp);
+            const double g00 = w * (cm + cp), g01 = w * (sm - sp), g10 = -w * (sp + sm), g11 = w * (cm - cp);
+            const int r = o + 2 * p, s = o + 2 * q;
+            Q[r * LD + s] = g00;
+            Q[r * LD + s + 1] = g01;
+            Q[(r + 1) * LD + s] = g10;
+            Q[(r + 1) * LD + s + 1] = g11;
+            Q[s * LD + r] = g00;
+            Q[(s + 1) * LD + r] = g01;
+            Q[s * LD + r + 1] = g10;
+            Q[(s + 1) * LD + r + 1] = g11;
         }
 }
 
@@ -215,18 +329,34 @@ SP_DEV void eq_grad(const ModelDesc& md, int l, const double* lr, double dt, con
     const int o = md.off[l], J = md.dim[l];
     const double var = lr[0], len = lr[1];
     const double* ac = md.eqconst + md.eqc[l];
-    const double* P1 = ac + J;
+    const double s0 = ac[J + J * J];
     // var: dQ = Q / var
     double s = 0.0;
     for (int i = 0; i < J; ++i)
         for (int k = 0; k < J; ++k) s += M[(o + i) * LD + o + k] * Q[(o + k) * LD + o + i];
     gvar += 0.5 * s / var;
-    if (dt < 0.0) return;  // dPinf/dlen = 0 and dΦ = 0 at the anchor
-    // len: dΦ = -(Δt/ℓ) F Φ (2x2 blocks), dQ = -(dΦ P Φ^T + Φ P dΦ^T)
+    if (dt < 0.0) return;  // dPinf/dℓ = 0 and dΦ = 0 at the anchor
+    const double tau = dt / len;
+    // dQ/dℓ = -var s0 (Δt/ℓ²) z z^T with z = e^{Aτ} g: pair p -> e^{a τ} [cos(cτ), -sin(cτ)]
     double tq = 0.0, tb = 0.0;
     for (int p = 0; p < J / 2; ++p) {
         const double a = ac[2 * p], c = ac[2 * p + 1];
         const int k = o + 2 * p;
+        const double rho = exp(a * tau);
+        double sn, cs;
+        sincos(c * tau, &sn, &cs);
+        const double zp0 = rho * cs, zp1 = -rho * sn;
+        for (int q = 0; q < J / 2; ++q) {
+            const double aq = ac[2 * q], cq = ac[2 * q + 1];
+            const int kq = o + 2 * q;
+            const double rq = exp(aq * tau);
+            double snq, csq;
+            sincos(cq * tau, &snq, &csq);
+            const double zq0 = rq * csq, zq1 = -rq * snq;
+            tq += M[kq * LD + k] * zp0 * zq0 + M[(kq + 1) * LD + k] * zp0 * zq1 +
+                  M[kq * LD + k + 1] * zp1 * zq0 + M[(kq + 1) * LD + k + 1] * zp1 * zq1;
+        }
+        // dΦ = -(Δt/ℓ) F Φ on the 2x2 block
         const double f00 = a / len, f01 = c / len, f10 = -c / len, f11 = a / len;
         const double p00 = Phi[k * LD + k], p01 = Phi[k * LD + k + 1];
         const double p10 = Phi[(k + 1) * LD + k], p11 = Phi[(k + 1) * LD + k + 1];
@@ -236,27 +366,7 @@ SP_DEV void eq_grad(const ModelDesc& md, int l, const double* lr, double dt, con
         tb += d00 * Bm[k * LD + k] + d01 * Bm[(k + 1) * LD + k] + d10 * Bm[k * LD + k + 1] +
               d11 * Bm[(k + 1) * LD + k + 1];
     }
-    // Tr(M dQ) with dQ = -var (dΦ P1 Φ^T + Φ P1 dΦ^T): both terms have equal trace
-    // against the symmetric M, so Tr(M dQ) = -2 var Tr(M dΦ P1 Φ^T).
-    for (int i = 0; i < J; ++i) {
-        const int pi = i & ~1;
-        for (int j = 0; j < J; ++j) {
-            const int pj = j & ~1;
-            // (dΦ P1 Φ^T)_{ij}
-            double v = 0.0;
-            for (int u = 0; u < 2; ++u) {
-                const int ku = o + pi + u;
-                const double a = ac[pi], c = ac[pi + 1];
-                const double fr0 = (i - pi == 0) ? a / len : -c / len;
-                const double fr1 = (i - pi == 0) ? c / len : a / len;
-                const double dph = -dt / len * (fr0 * Phi[(o + pi) * LD + ku] + fr1 * Phi[(o + pi + 1) * LD + ku]);
-                for (int w = 0; w < 2; ++w)
-                    v += dph * P1[(pi + u) * J + pj + w] * Phi[(o + j) * LD + o + pj + w];
-            }
-            tq += M[(o + j) * LD + o + i] * v;
-        }
-    }
-    glen += 0.5 * (-2.0 * var * tq) + tb;
+    glen += 0.5 * (-var * s0 * dt / (len * len)) * tq + tb;
 }
 
 // ---------------------------------------------------------------------- QP --

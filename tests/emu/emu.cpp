@@ -20,6 +20,7 @@ namespace {
 
 std::string g_err;
 unsigned long long g_status;
+double g_diag[4];  // logdetP, logdetQ, fit_y, fit_e of the last series evaluated
 
 unsigned nblocks(long long n, int tpb) { return static_cast<unsigned>((n + tpb - 1) / tpb); }
 
@@ -73,6 +74,10 @@ void emu_eval(const HostModel& hm, const Plan& plan, std::vector<double>& params
         double ld = acc[P_LOGDET] + top[s];
         for (int l = 1; l < g.nlev; ++l)
             for (long long k = 0; k < g.K[l]; ++k) ld += rec[l][Rec<B>::LOGDET * g.K[l] * g.S + s * g.K[l] + k];
+        g_diag[0] = ld;
+        g_diag[1] = acc[P_LDQ];
+        g_diag[2] = acc[P_FITY];
+        g_diag[3] = acc[P_FITE];
         const double* rp = params.data() + static_cast<size_t>(s) * hm.rec_stride;
         const double sig = rp[0], s2 = sig * sig, nn = static_cast<double>(g.n[0]);
         loglik[s] = -0.5 * (acc[P_FITY] + acc[P_FITE]) - 0.5 * (ld + acc[P_LDQ] + nn * std::log(s2)) -
@@ -134,6 +139,9 @@ int finish() {
 extern "C" {
 
 const char* emu_last_error(void) { return g_err.c_str(); }
+void emu_last_diag(double* out) {
+    for (int i = 0; i < 4; ++i) out[i] = g_diag[i];
+}
 
 int emu_eval_batched(const spingp_leaf* leaves, int32_t n_leaves, const double* theta, int32_t n_theta,
                      int64_t S, int64_t n, const double* t, const double* y, const double* sigma,
@@ -170,7 +178,7 @@ int emu_eval_batched(const spingp_leaf* leaves, int32_t n_leaves, const double* 
         g_err = e.what();
         return SPINGP_BAD_ARG;
     }
-    if (fail_block) *fail_block = g_status == ~0ULL ? -1 : static_cast<int64_t>(g_status >> 4);
+    if (fail_block) *fail_block = g_status == ~0ULL ? -1 : static_cast<int64_t>((g_status >> 4) & ((1ULL << 56) - 1));
     return finish();
 }
 
