@@ -144,36 +144,10 @@ SP_UNROLL
     return s;
 }
 
-// Cholesky A = L L^T (L lower, stored full with zero upper); returns false on a
-// non-positive / non-finite pivot.  logdet accumulates 2 sum ln L_kk.
-template <int B>
-SP_DEV bool chol(double* L, const double* A, double& logdet) {
-    bool ok = true;
-    double ld = 0.0;
-SP_UNROLL
-    for (int j = 0; j < B; ++j) {
-        double d = A[j * B + j];
-SP_UNROLL
-        for (int k = 0; k < j; ++k) d = fma(-L[j * B + k], L[j * B + k], d);
-        ok = ok && (d > 0.0) && isfinite(d);
-        const double ljj = sqrt(d);
-        const double inv = 1.0 / ljj;
-        L[j * B + j] = ljj;
-        ld += log(ljj);
-SP_UNROLL
-        for (int i = j + 1; i < B; ++i) {
-            double s = A[i * B + j];
-SP_UNROLL
-            for (int k = 0; k < j; ++k) s = fma(-L[i * B + k], L[j * B + k], s);
-            L[i * B + j] = s * inv;
-        }
-SP_UNROLL
-        for (int i = 0; i < j; ++i) L[i * B + j] = 0.0;
-    }
-    logdet = 2.0 * ld;
-    return ok;
-}
-// same without the logarithms
+// Cholesky A = L L^T with INVERTED pivots: the returned lower-triangular L holds
+// 1/l_jj on its diagonal (all substitutions below multiply by it; one rsqrt per
+// pivot and no divisions).  Returns false on a non-positive / non-finite pivot.
+// logdet = log det A = -2 log prod_j (1/l_jj), taken in groups of 4 pivots.
 template <int B>
 SP_DEV bool chol_nolog(double* L, const double* A) {
     bool ok = true;
@@ -183,9 +157,8 @@ SP_UNROLL
 SP_UNROLL
         for (int k = 0; k < j; ++k) d = fma(-L[j * B + k], L[j * B + k], d);
         ok = ok && (d > 0.0) && isfinite(d);
-        const double ljj = sqrt(d);
-        const double inv = 1.0 / ljj;
-        L[j * B + j] = ljj;
+        const double inv = rsqrt(d);
+        L[j * B + j] = inv;
 SP_UNROLL
         for (int i = j + 1; i < B; ++i) {
             double s = A[i * B + j];
@@ -202,8 +175,19 @@ template <int B>
 SP_DEV double chol_logdet(const double* L) {
     double ld = 0.0;
 SP_UNROLL
-    for (int j = 0; j < B; ++j) ld += log(L[j * B + j]);
-    return 2.0 * ld;
+    for (int j0 = 0; j0 < B; j0 += 4) {
+        double p = 1.0;
+SP_UNROLL
+        for (int j = j0; j < j0 + 4 && j < B; ++j) p *= L[j * B + j];
+        ld += log(p);
+    }
+    return -2.0 * ld;
+}
+template <int B>
+SP_DEV bool chol(double* L, const double* A, double& logdet) {
+    const bool ok = chol_nolog<B>(L, A);
+    logdet = ok ? chol_logdet<B>(L) : 0.0;
+    return ok;
 }
 
 // Ainv = (L L^T)^{-1} = L^{-T} L^{-1}, symmetric.
@@ -212,7 +196,7 @@ SP_DEV void chol_inverse(double* Ainv, const double* L) {
     double Li[B * B];  // L^{-1}, lower
 SP_UNROLL
     for (int j = 0; j < B; ++j) {
-        const double dj = 1.0 / L[j * B + j];
+        const double dj = L[j * B + j];  // inverted pivot
 SP_UNROLL
         for (int i = 0; i < B; ++i) {
             if (i < j) { Li[i * B + j] = 0.0; continue; }
@@ -220,7 +204,7 @@ SP_UNROLL
             double s = 0.0;
 SP_UNROLL
             for (int k = j; k < i; ++k) s = fma(L[i * B + k], (k == j ? dj : Li[k * B + j]), s);
-            Li[i * B + j] = -s / L[i * B + i];
+            Li[i * B + j] = -s * L[i * B + i];
         }
     }
 SP_UNROLL
@@ -241,7 +225,7 @@ template <int B>
 SP_DEV void tri_inverse(double* Li, const double* L) {
 SP_UNROLL
     for (int j = 0; j < B; ++j) {
-        const double dj = 1.0 / L[j * B + j];
+        const double dj = L[j * B + j];  // inverted pivot
 SP_UNROLL
         for (int i = 0; i < B; ++i) {
             if (i < j) {
@@ -252,7 +236,7 @@ SP_UNROLL
                 double s = L[i * B + j] * dj;
 SP_UNROLL
                 for (int k = j + 1; k < i; ++k) s = fma(L[i * B + k], Li[k * B + j], s);
-                Li[i * B + j] = -s / L[i * B + i];
+                Li[i * B + j] = -s * L[i * B + i];
             }
         }
     }
@@ -344,7 +328,8 @@ SP_UNROLL
         }
 }
 
-// Triangular solves with the Cholesky factor L (lower): forward L X = A, backward L^T X = A.
+// Triangular solves with the inverted-pivot Cholesky factor L (lower):
+// forward L X = A, backward L^T X = A.
 template <int B>
 SP_DEV void lsolve(double* X, const double* L, const double* A, int ncol = B) {
 SP_UNROLL
@@ -355,7 +340,7 @@ SP_UNROLL
             double s = A[i * B + c];
 SP_UNROLL
             for (int k = 0; k < i; ++k) s = fma(-L[i * B + k], X[k * B + c], s);
-            X[i * B + c] = s / L[i * B + i];
+            X[i * B + c] = s * L[i * B + i];
         }
     }
 }
@@ -366,7 +351,7 @@ SP_UNROLL
         double s = a[i];
 SP_UNROLL
         for (int k = 0; k < i; ++k) s = fma(-L[i * B + k], x[k], s);
-        x[i] = s / L[i * B + i];
+        x[i] = s * L[i * B + i];
     }
 }
 template <int B>
@@ -378,7 +363,7 @@ SP_UNROLL
             double s = A[i * B + c];
 SP_UNROLL
             for (int k = i + 1; k < B; ++k) s = fma(-L[k * B + i], X[k * B + c], s);
-            X[i * B + c] = s / L[i * B + i];
+            X[i * B + c] = s * L[i * B + i];
         }
 }
 template <int B>
@@ -388,7 +373,7 @@ SP_UNROLL
         double s = a[i];
 SP_UNROLL
         for (int k = i + 1; k < B; ++k) s = fma(-L[k * B + i], x[k], s);
-        x[i] = s / L[i * B + i];
+        x[i] = s * L[i * B + i];
     }
 }
 

@@ -229,7 +229,7 @@ SP_UNROLL
 // ======================================================= level 0 (fused) ======
 
 template <class T>
-__global__ void __launch_bounds__(128) k_fwd0(ModelDesc md, const double* __restrict__ params,
+__global__ void __launch_bounds__(128, 3) k_fwd0(ModelDesc md, const double* __restrict__ params,
                                               const double* __restrict__ t,
                                               const double* __restrict__ y, Geom geo,
                                               double* __restrict__ fac, double* __restrict__ rec,
@@ -423,16 +423,23 @@ SP_UNROLL
 SP_UNROLL
             for (int j = 0; j < B; ++j) es.W[i * B + j] = U[j * B + i];
     }
+    // software-pipelined: the next block's (L2-resident) record is loaded while the
+    // current block is eliminated — the upper levels are latency-bound chains
+    double D[B * B], U[B * B], r[B];
+    if (st < en - 1) src.block(s, st, D, U, r, true);
     for (long long j = st; j < en - 1; ++j) {
-        double D[B * B], U[B * B], r[B];
-        src.block(s, j, D, U, r, true);
+        double Dn[B * B], Un[B * B], rn[B];
+        if (j + 1 < en - 1) src.block(s, j + 1, Dn, Un, rn, true);
         double* fp = fac + (j - st) * Fac<B>::N * SK + g;
         if (!elim_block<B>(es, D, U, r, hasL, fp, SK)) {
             report(status, gbase + to_global(geo, lev, j), ST_NOT_PD);
             return;
         }
+        mcopy<B>(D, Dn);
+        mcopy<B>(U, Un);
+SP_UNROLL
+        for (int q = 0; q < B; ++q) r[q] = rn[q];
     }
-    double D[B * B], U[B * B], r[B];
     src.block(s, en - 1, D, U, r, false);
 SP_UNROLL
     for (int i = 0; i < B * B; ++i) D[i] -= es.T[i];
@@ -644,10 +651,17 @@ SP_UNROLL
 SP_UNROLL
         for (int j = 0; j < B; ++j) CnL[i * B + j] = sd.CLR[j * B + i];
     sink.put(s, en - 1, xn, Cnn, needC);
+    double Li[B * B], Y[B * B], z[B], U[B * B];
+    if (en - 2 >= st) {
+        load_fac<B>(fac + (en - 2 - st) * Fac<B>::N * SK + g, SK, hasL, Li, Y, z);
+        src.upper(s, en - 2, U);
+    }
     for (long long j = en - 2; j >= st; --j) {
-        double Li[B * B], Y[B * B], z[B], U[B * B], X[B * B];
-        load_fac<B>(fac + (j - st) * Fac<B>::N * SK + g, SK, hasL, Li, Y, z);
-        src.upper(s, j, U);
+        double X[B * B], Lin[B * B], Yn[B * B], zn[B], Un[B * B];
+        if (j - 1 >= st) {  // prefetch the next (lower) block of the reverse sweep
+            load_fac<B>(fac + (j - 1 - st) * Fac<B>::N * SK + g, SK, hasL, Lin, Yn, zn);
+            src.upper(s, j - 1, Un);
+        }
         lsolve<B>(X, Li, U);
         double xj[B], CjL[B * B], Cjn[B * B], Cjj[B * B];
         back_step<B>(Li, Y, z, X, hasL, needC, sd, xn, Cnn, CnL, xj, CjL, Cjn, Cjj);
@@ -658,6 +672,13 @@ SP_UNROLL
         if (needC) {
             mcopy<B>(Cnn, Cjj);
             mcopy<B>(CnL, CjL);
+        }
+        if (j - 1 >= st) {
+            mcopy<B>(Li, Lin);
+            if (hasL) mcopy<B>(Y, Yn);
+            mcopy<B>(U, Un);
+SP_UNROLL
+            for (int q = 0; q < B; ++q) z[q] = zn[q];
         }
     }
     if (hasL && needC) {  // C_{st-1, st} = C_{st, L}^T

@@ -314,7 +314,7 @@ Plan make_plan(int64_t n, int64_t S, int Bsz, int64_t m0_override) {
     int64_t cur = n, m = m0;
     while (true) {
         if (lev >= kMaxLev) throw ApiError{SPINGP_UNSUPPORTED, -1, "too many reduction levels"};
-        if (lev > 0) m = cur <= 16 ? cur : 8;
+        if (lev > 0) m = cur <= 8 ? cur : 4;
         if (m < 2 && cur > 1) m = 2;
         g.n[lev] = cur;
         g.m[lev] = static_cast<int>(m);

@@ -47,10 +47,10 @@ SP_DEV void exp_tails(double x, double* R) {
     for (int m = 1; m <= M; ++m) pw[m] = pw[m - 1] * x / double(m);
     if (x < 6.0) {
         double term = pw[M] * x / double(M + 1), s = 0.0;
-#pragma unroll 4
-        for (int k = 0; k < 48; ++k) {
+        for (int k = 0; k < 64; ++k) {  // terms decrease monotonically once j > x
             s += term;
             term *= x / double(M + 2 + k);
+            if (term <= 1e-17 * s) break;
         }
         R[M] = ex * s;
 #pragma unroll

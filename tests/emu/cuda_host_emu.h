@@ -13,7 +13,7 @@
 #define __host__
 #define __forceinline__ inline
 #define __global__
-#define __launch_bounds__(x)
+#define __launch_bounds__(...)
 #define __shared__ static
 #define __restrict__ __restrict
 
@@ -30,6 +30,7 @@ inline unsigned long long atomicMin(unsigned long long* p, unsigned long long v)
     return o;
 }
 using std::isfinite;
+inline double rsqrt(double x) { return 1.0 / std::sqrt(x); }
 using std::max;
 using std::min;
 
