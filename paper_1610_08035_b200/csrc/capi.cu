@@ -78,6 +78,13 @@ void dispatch_eval(spingp_ctx* ctx, const EvalArgs& a) {
             case 3: return eval_matern_3(ctx, a);
         }
     }
+    switch (static_model(hm)) {
+        case SM_EQ6: return eval_s_eq6(ctx, a);
+        case SM_EQ10: return eval_s_eq10(ctx, a);
+        case SM_M32_QP6: return eval_s_m32qp6(ctx, a);
+        case SM_M32_EQ10: return eval_s_m32eq10(ctx, a);
+        default: break;
+    }
     switch (pad_b(hm.b)) {
         case 1: case 2: case 3: return eval_generic_3(ctx, a);
         case 4: return eval_generic_4(ctx, a);
@@ -89,7 +96,9 @@ void dispatch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     throw ApiError{SPINGP_UNSUPPORTED, -1, "no kernel instantiation for this state dimension"};
 }
 
-int plan_bsize(const HostModel& hm) { return hm.single_matern ? hm.b : std::max(3, pad_b(hm.b)); }
+int plan_bsize(const HostModel& hm) {
+    return (hm.single_matern || static_model(hm) != SM_NONE) ? hm.b : std::max(3, pad_b(hm.b));
+}
 
 void btd_dispatch(spingp_ctx* ctx, int64_t n, int b, const double* diag, const double* upper,
                   const double* rhs, int k, int col, double* x, double* cdiag, double* cupper,

@@ -182,6 +182,10 @@ void eval_generic_6(spingp_ctx* ctx, const EvalArgs& a);
 void eval_generic_8(spingp_ctx* ctx, const EvalArgs& a);
 void eval_generic_12(spingp_ctx* ctx, const EvalArgs& a);
 void eval_generic_16(spingp_ctx* ctx, const EvalArgs& a);
+void eval_s_eq6(spingp_ctx* ctx, const EvalArgs& a);       // inst_s_eq6.cu
+void eval_s_eq10(spingp_ctx* ctx, const EvalArgs& a);      // inst_s_eq10.cu
+void eval_s_m32qp6(spingp_ctx* ctx, const EvalArgs& a);    // inst_s_m32qp6.cu
+void eval_s_m32eq10(spingp_ctx* ctx, const EvalArgs& a);   // inst_s_m32eq10.cu
 #define SPINGP_BTD_DECL(B)                                                                          \
     void btd_run_##B(spingp_ctx* ctx, int64_t n, int b, const double* diag, const double* upper, \
                      const double* rhs, int k, int col, double* x, double* cdiag, double* cupper, \

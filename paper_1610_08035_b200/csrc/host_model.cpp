@@ -302,6 +302,15 @@ int pad_b(int b) {
 // Level 0: enough chunks to give every one of the 148 SMs ~256 resident threads
 // (b <= 3) or ~128 (larger blocks); upper levels: chunks of 8 blocks until one
 // block is left.
+StaticModel static_model(const HostModel& hm) {
+    const spingp_dev::ModelDesc& d = hm.desc;
+    if (d.nleaves == 1 && d.type[0] == EQ && d.order[0] == 6) return SM_EQ6;
+    if (d.nleaves == 1 && d.type[0] == EQ && d.order[0] == 10) return SM_EQ10;
+    if (d.nleaves == 2 && d.type[0] == MATERN32 && d.type[1] == QP && d.order[1] == 6) return SM_M32_QP6;
+    if (d.nleaves == 2 && d.type[0] == MATERN32 && d.type[1] == EQ && d.order[1] == 10) return SM_M32_EQ10;
+    return SM_NONE;
+}
+
 Plan make_plan(int64_t n, int64_t S, int Bsz, int64_t m0_override) {
     if (n < 1 || S < 1) throw std::invalid_argument("need at least one point and one series");
     Plan p;

@@ -42,4 +42,8 @@ Plan make_plan(int64_t n, int64_t S, int Bsz, int64_t m0_override = 0);
 // Padded block size with a kernel instantiation (1, 2, 3, 4, 6, 8, 12, 16).
 int pad_b(int b);
 
+// Models with a static-structure (compile-time offsets) instantiation.
+enum StaticModel { SM_NONE = 0, SM_EQ6 = 1, SM_EQ10 = 2, SM_M32_QP6 = 3, SM_M32_EQ10 = 4 };
+StaticModel static_model(const HostModel& hm);
+
 }  // namespace spingp_host

@@ -273,11 +273,9 @@ SP_DEV void phi1_int(double a, double b, double tau, double& re, double& im) {
 }
 
 template <int LD>
-SP_DEV void eq_block(const ModelDesc& md, int l, const double* lr, double dt, double* Phi,
+SP_DEV void eq_block(int o, int J, const double* ac, const double* lr, double dt, double* Phi,
                      double* Q) {
-    const int o = md.off[l], J = md.dim[l];
     const double var = lr[0], len = lr[1];
-    const double* ac = md.eqconst + md.eqc[l];
     const double* P1 = ac + J;  // J/2 pairs of (a, c), then P1, then s0
     const double s0 = P1[J * J];
     if (dt < 0.0) {
@@ -323,12 +321,10 @@ SP_DEV void eq_block(const ModelDesc& md, int l, const double* lr, double dt, do
 }
 
 template <int LD>
-SP_DEV void eq_grad(const ModelDesc& md, int l, const double* lr, double dt, const double* Phi,
+SP_DEV void eq_grad(int o, int J, const double* ac, const double* lr, double dt, const double* Phi,
                     const double* Q, const double* M, const double* Bm, double& gvar,
                     double& glen) {
-    const int o = md.off[l], J = md.dim[l];
     const double var = lr[0], len = lr[1];
-    const double* ac = md.eqconst + md.eqc[l];
     const double s0 = ac[J + J * J];
     // var: dQ = Q / var
     double s = 0.0;
@@ -371,9 +367,8 @@ SP_DEV void eq_grad(const ModelDesc& md, int l, const double* lr, double dt, con
 
 // ---------------------------------------------------------------------- QP --
 template <int LD>
-SP_DEV void qp_block(const ModelDesc& md, int l, const double* lr, double dt, double* Phi,
-                     double* Q) {
-    const int o = md.off[l], J = md.order[l], d = md.dim[l];
+SP_DEV void qp_block(int o, int J, const double* lr, double dt, double* Phi, double* Q) {
+    const int d = 2 * (J + 1);
     const double var = lr[0], env = lr[3], w0 = lr[4];
     const double* q2 = lr + 5;
     for (int i = 0; i < d; ++i)
@@ -401,9 +396,8 @@ SP_DEV void qp_block(const ModelDesc& md, int l, const double* lr, double dt, do
 
 // gradients w.r.t. (var, len, period, env) of one QP leaf
 template <int LD>
-SP_DEV void qp_grad(const ModelDesc& md, int l, const double* lr, double dt, const double* Phi,
-                    const double* M, const double* Bm, double* g4) {
-    const int o = md.off[l], J = md.order[l];
+SP_DEV void qp_grad(int o, int J, const double* lr, double dt, const double* Phi, const double* M,
+                    const double* Bm, double* g4) {
     const double var = lr[0], period = lr[2], env = lr[3], w0 = lr[4];
     const double* q2 = lr + 5;
     const double* dq2 = lr + 5 + (J + 1);
@@ -477,8 +471,8 @@ struct GenericTraits {
                 case MATERN12: matern_block<1, BB>(lr, dt, md.off[l], Phi, Q); break;
                 case MATERN32: matern_block<2, BB>(lr, dt, md.off[l], Phi, Q); break;
                 case MATERN52: matern_block<3, BB>(lr, dt, md.off[l], Phi, Q); break;
-                case EQ: eq_block<BB>(md, l, lr, dt, Phi, Q); break;
-                case QP: qp_block<BB>(md, l, lr, dt, Phi, Q); break;
+                case EQ: eq_block<BB>(md.off[l], md.dim[l], md.eqconst + md.eqc[l], lr, dt, Phi, Q); break;
+                case QP: qp_block<BB>(md.off[l], md.order[l], lr, dt, Phi, Q); break;
             }
         }
     }
@@ -495,10 +489,12 @@ struct GenericTraits {
                 case MATERN12: matern_grad<1, BB>(lr, dt, md.off[l], Phi, Q, M, Bm, gv, gl); break;
                 case MATERN32: matern_grad<2, BB>(lr, dt, md.off[l], Phi, Q, M, Bm, gv, gl); break;
                 case MATERN52: matern_grad<3, BB>(lr, dt, md.off[l], Phi, Q, M, Bm, gv, gl); break;
-                case EQ: eq_grad<BB>(md, l, lr, dt, Phi, Q, M, Bm, gv, gl); break;
+                case EQ:
+                    eq_grad<BB>(md.off[l], md.dim[l], md.eqconst + md.eqc[l], lr, dt, Phi, Q, M, Bm, gv, gl);
+                    break;
                 case QP: {
                     double g4[4] = {0.0, 0.0, 0.0, 0.0};
-                    qp_grad<BB>(md, l, lr, dt, Phi, M, Bm, g4);
+                    qp_grad<BB>(md.off[l], md.order[l], lr, dt, Phi, M, Bm, g4);
                     g[t0 + 2] += g4[2];
                     g[t0 + 3] += g4[3];
                     gv = g4[0];
@@ -510,6 +506,91 @@ struct GenericTraits {
             g[t0 + 1] += gl;
         }
         for (int p = 0; p < md.nt; ++p) g[p] += hm * rec[2 + p];
+    }
+};
+
+// Static-structure models: leaf types and offsets are template constants, so every
+// block index is a compile-time constant after inlining (the fast, fully optimised
+// path for the BASELINE models; GenericTraits above is the any-sum fallback).
+template <int D>
+struct SMatern {
+    static constexpr int dim = D, np = 2;
+    template <int O, int LD>
+    SP_DEV static void step(const ModelDesc&, int, const double* lr, double dt, double* Phi, double* Q) {
+        matern_block<D, LD>(lr, dt, O, Phi, Q);
+    }
+    template <int O, int LD>
+    SP_DEV static void grad(const ModelDesc&, int, const double* lr, double dt, const double* Phi,
+                            const double* Q, const double* M, const double* Bm, double* g) {
+        matern_grad<D, LD>(lr, dt, O, Phi, Q, M, Bm, g[0], g[1]);
+    }
+};
+template <int J>
+struct SEQ {
+    static constexpr int dim = J, np = 2;
+    template <int O, int LD>
+    SP_DEV static void step(const ModelDesc& md, int l, const double* lr, double dt, double* Phi, double* Q) {
+        eq_block<LD>(O, J, md.eqconst + md.eqc[l], lr, dt, Phi, Q);
+    }
+    template <int O, int LD>
+    SP_DEV static void grad(const ModelDesc& md, int l, const double* lr, double dt, const double* Phi,
+                            const double* Q, const double* M, const double* Bm, double* g) {
+        eq_grad<LD>(O, J, md.eqconst + md.eqc[l], lr, dt, Phi, Q, M, Bm, g[0], g[1]);
+    }
+};
+template <int J>
+struct SQP {
+    static constexpr int dim = 2 * (J + 1), np = 4;
+    template <int O, int LD>
+    SP_DEV static void step(const ModelDesc&, int, const double* lr, double dt, double* Phi, double* Q) {
+        qp_block<LD>(O, J, lr, dt, Phi, Q);
+    }
+    template <int O, int LD>
+    SP_DEV static void grad(const ModelDesc&, int, const double* lr, double dt, const double* Phi,
+                            const double*, const double* M, const double* Bm, double* g) {
+        qp_grad<LD>(O, J, lr, dt, Phi, M, Bm, g);
+    }
+};
+
+// One or two static leaves (the second at offset dim of the first).
+template <class L0, class L1 = void>
+struct StaticTraits {
+    static constexpr int B = L0::dim + L1::dim;
+    SP_DEV static double H(const ModelDesc& md, int i) { return md.H[i]; }
+    SP_DEV static void step(const ModelDesc& md, const double* rec, double dt, double* Phi, double* Q) {
+        mzero<B>(Phi);
+        mzero<B>(Q);
+        L0::template step<0, B>(md, 0, rec + md.rec[0], dt, Phi, Q);
+        L1::template step<L0::dim, B>(md, 1, rec + md.rec[1], dt, Phi, Q);
+    }
+    SP_DEV static void grad(const ModelDesc& md, const double* rec, double dt, const double* Phi,
+                            const double* Q, const double* M, const double* Bm, double* g) {
+        double g0[4] = {0.0, 0.0, 0.0, 0.0}, g1[4] = {0.0, 0.0, 0.0, 0.0};
+        L0::template grad<0, B>(md, 0, rec + md.rec[0], dt, Phi, Q, M, Bm, g0);
+        L1::template grad<L0::dim, B>(md, 1, rec + md.rec[1], dt, Phi, Q, M, Bm, g1);
+        const double hm = 0.5 * mtrace<B>(M);
+#pragma unroll
+        for (int p = 0; p < L0::np; ++p) g[p] += g0[p] + hm * rec[2 + p];
+#pragma unroll
+        for (int p = 0; p < L1::np; ++p) g[L0::np + p] += g1[p] + hm * rec[2 + L0::np + p];
+    }
+};
+template <class L0>
+struct StaticTraits<L0, void> {
+    static constexpr int B = L0::dim;
+    SP_DEV static double H(const ModelDesc& md, int i) { return md.H[i]; }
+    SP_DEV static void step(const ModelDesc& md, const double* rec, double dt, double* Phi, double* Q) {
+        mzero<B>(Phi);
+        mzero<B>(Q);
+        L0::template step<0, B>(md, 0, rec + md.rec[0], dt, Phi, Q);
+    }
+    SP_DEV static void grad(const ModelDesc& md, const double* rec, double dt, const double* Phi,
+                            const double* Q, const double* M, const double* Bm, double* g) {
+        double g0[4] = {0.0, 0.0, 0.0, 0.0};
+        L0::template grad<0, B>(md, 0, rec + md.rec[0], dt, Phi, Q, M, Bm, g0);
+        const double hm = 0.5 * mtrace<B>(M);
+#pragma unroll
+        for (int p = 0; p < L0::np; ++p) g[p] += g0[p] + hm * rec[2 + p];
     }
 };
 

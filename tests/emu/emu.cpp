@@ -151,12 +151,17 @@ int emu_eval_batched(const spingp_leaf* leaves, int32_t n_leaves, const double* 
     try {
         const HostModel hm = build_model(leaves, n_leaves, n_theta);
         const bool matern = hm.single_matern && !force_generic;
-        const int Bsz = matern ? hm.b : std::max(3, pad_b(hm.b));
+        const StaticModel sm = force_generic ? SM_NONE : static_model(hm);
+        const int Bsz = (matern || sm != SM_NONE) ? hm.b : std::max(3, pad_b(hm.b));
         const Plan plan = make_plan(n, S, Bsz, m0);
         std::vector<double> params(static_cast<size_t>(S) * hm.rec_stride, 0.0);
         for (int64_t s = 0; s < S; ++s) fill_record(hm, theta + s * n_theta, sigma[s], params.data() + s * hm.rec_stride);
-#define E(T) emu_eval<T>(hm, plan, params, t, y, flags, loglik, grad, mean, var)
-        if (matern) {
+#define E(...) emu_eval<__VA_ARGS__>(hm, plan, params, t, y, flags, loglik, grad, mean, var)
+        if (sm == SM_EQ6) E(StaticTraits<SEQ<6>>);
+        else if (sm == SM_EQ10) E(StaticTraits<SEQ<10>>);
+        else if (sm == SM_M32_QP6) E(StaticTraits<SMatern<2>, SQP<6>>);
+        else if (sm == SM_M32_EQ10) E(StaticTraits<SMatern<2>, SEQ<10>>);
+        else if (matern) {
             if (hm.b == 1) E(MaternTraits<1>);
             else if (hm.b == 2) E(MaternTraits<2>);
             else E(MaternTraits<3>);
