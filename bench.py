@@ -10,9 +10,12 @@ partitioned block elimination -> selected inverse -> loglik/gradient reduction).
            stream, L2 flushed (256 MiB write) between steps outside the events.
   e2e    : the same metric through the host-pointer C ABI call (spingp_eval):
            pinned host t,y -> H2D, kernels, D2H of loglik, gradient and mean.
-  N > 1  : torchrun, one rank per GPU; every rank evaluates its own seeded series
-           of the same size (independent series, weak scaling, no data-path
-           collective; SURVEY.md §8(e) "batches of independent series are sharded").
+  N > 1  : torchrun, one rank per GPU; ONE series of N x 1,000,000 points partitioned
+           into contiguous time segments: each GPU reduces its
+           segment to a 2-separator Schur record, the N records are all-gathered over
+           NCCL (torch.distributed), the N-block reduced system is solved redundantly on
+           every GPU, segments are back-substituted and the partial sums all-reduced.
+           Weak scaling (1,000,000 points per GPU).  Batched configs (cfg3) shard series.
   --impl reference : the CPU oracle (restatement of the reference algorithm, Padé/
            Van Loan per step + block Thomas + Takahashi; the reference itself does
            not build here) on all host cores, same workload, rank 0 only.
@@ -214,28 +217,56 @@ def run_ours(args, ws, rank, local):
     import paper_1610_08035_b200 as P
 
     torch.cuda.set_device(local)
+    dist = None
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    wl = workload(args.config, rank, args.points)
+    partitioned = ws > 1 and args.config != "cfg3"
+    if partitioned:  # one long series, contiguous segment per rank
+        from paper_1610_08035_b200 import datasets
+        from paper_1610_08035_b200.partition import split, halos, make_buffers, eval_partitioned
+        base = datasets.make(args.config, **({"n": args.points} if args.points else {}))
+        full = datasets.make(args.config, n=len(base.t) * ws)
+        bounds = split(len(full.t), ws)
+        a, bb = bounds[rank], bounds[rank + 1]
+        t_left, t_right = halos(full.t, bounds, rank)
+        wl = full
+        seg_t, seg_y = full.t[a:bb], full.y[a:bb]
+        n_total = len(full.t)
+    else:
+        wl = workload(args.config, rank, args.points)
+        seg_t, seg_y = wl.t, wl.y
     b, nt = P.kernel_dims(wl.leaves)
     flags = P.WANT_GRAD | (P.WANT_MEAN if "mean" in wl.outputs else 0) | (P.WANT_VAR if "var" in wl.outputs else 0)
-    S = wl.t.shape[0] if wl.batched else 1
-    n = wl.t.shape[-1]
+    S = seg_t.shape[0] if seg_t.ndim == 2 else 1
+    n = seg_t.shape[-1]
+    points_per_rank = seg_t.size
     ctx = P.Context(local)
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
-    d_t = torch.from_numpy(np.ascontiguousarray(wl.t)).to(dev)
-    d_y = torch.from_numpy(np.ascontiguousarray(wl.y)).to(dev)
+    d_t = torch.from_numpy(np.ascontiguousarray(seg_t)).to(dev)
+    d_y = torch.from_numpy(np.ascontiguousarray(seg_y)).to(dev)
     d_ll = torch.zeros(S, dtype=torch.float64, device=dev)
     d_g = torch.zeros(S * (nt + 1), dtype=torch.float64, device=dev)
     d_m = torch.zeros(S * n, dtype=torch.float64, device=dev) if flags & P.WANT_MEAN else None
     d_v = torch.zeros(S * n, dtype=torch.float64, device=dev) if flags & P.WANT_VAR else None
     flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=dev)
+    if partitioned:
+        bufs = make_buffers(torch, dev, wl.leaves, ws)
+
+        def gather(out, inp):
+            dist.all_gather_into_tensor(out, inp)
+
+        def reduce_(x):
+            dist.all_reduce(x)
 
     def step():
-        if wl.batched:
+        if partitioned:
+            eval_partitioned(ctx, wl.leaves, wl.theta, d_t.data_ptr(), d_y.data_ptr(), n, n_total, t_left, t_right,
+                             rank, ws, wl.sigma, flags, bufs, gather, reduce_,
+                             d_m.data_ptr() if d_m is not None else 0, d_v.data_ptr() if d_v is not None else 0)
+        elif wl.batched:
             ctx.eval_batched_device(wl.leaves, wl.theta, S, n, d_t.data_ptr(), d_y.data_ptr(), wl.sigma, flags,
                                     d_ll.data_ptr(), d_g.data_ptr(), d_m.data_ptr() if d_m is not None else 0,
                                     d_v.data_ptr() if d_v is not None else 0)
@@ -244,33 +275,33 @@ def run_ours(args, ws, rank, local):
                             d_ll.data_ptr(), d_g.data_ptr(), d_m.data_ptr() if d_m is not None else 0,
                             d_v.data_ptr() if d_v is not None else 0)
 
-    for _ in range(max(3, args.warmup)):
-        flush.zero_()
-        step()
-    ctx.status()
-    torch.cuda.synchronize(dev)
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    launches0 = ctx.launch_count()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
+        for _ in range(max(3, args.warmup)):
+            flush.zero_()
+            step()
+        ctx.status()
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        launches0 = ctx.launch_count()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         for k in range(args.steps):
             flush.zero_()  # L2 flush between timed steps, outside the events
             evs[k][0].record(stream)
             step()
             evs[k][1].record(stream)
         torch.cuda.synchronize(dev)
-    launches = ctx.launch_count() - launches0
+        launches = ctx.launch_count() - launches0
     ctx.status()  # raises on any device-side failure in the timed steps
-    step_ms = [a.elapsed_time(bv) for a, bv in evs]
+    step_ms = [a_.elapsed_time(b_) for a_, b_ in evs]
     total_ms = float(sum(step_ms))
     if ws > 1:
         tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
         dist.barrier()
-    value = wl.points * ws * args.steps / (total_ms * 1e-3)
+    value = points_per_rank * ws * args.steps / (total_ms * 1e-3)
 
     # per-kernel breakdown (separate, untimed profiling pass; events around every launch)
     ctx.set_profiling(True)
@@ -287,37 +318,54 @@ def run_ours(args, ws, rank, local):
     dom_launch_ms = statistics.mean(kt[dom])
     launches_per_step = {k: len(v) // reps for k, v in kt.items()}
 
-    # e2e through the host-pointer ABI call (pinned host inputs, D2H of the results)
-    h_t = torch.from_numpy(np.ascontiguousarray(wl.t)).pin_memory().numpy()
-    h_y = torch.from_numpy(np.ascontiguousarray(wl.y)).pin_memory().numpy()
+    # e2e: host inputs (pinned) -> device, evaluation, results -> host, every step
+    h_t = torch.from_numpy(np.ascontiguousarray(seg_t)).pin_memory()
+    h_y = torch.from_numpy(np.ascontiguousarray(seg_y)).pin_memory()
     want = dict(grad=True, mean="mean" in wl.outputs, var="var" in wl.outputs)
+    h_out = torch.empty(S * (nt + 1) + S + (S * n if want["mean"] else 0) + (S * n if want["var"] else 0),
+                        dtype=torch.float64).pin_memory()
 
     def e2e_step():
+        if partitioned:  # device entry points with explicit pinned H2D / D2H (the ABI is device-side here)
+            d_t.copy_(h_t, non_blocking=True)
+            d_y.copy_(h_y, non_blocking=True)
+            step()
+            k0 = 0
+            h_out[k0:k0 + 1].copy_(bufs["loglik"], non_blocking=True)
+            h_out[1:2 + nt].copy_(bufs["grad"], non_blocking=True)
+            k0 = 2 + nt
+            if d_m is not None:
+                h_out[k0:k0 + n].copy_(d_m, non_blocking=True)
+                k0 += n
+            if d_v is not None:
+                h_out[k0:k0 + n].copy_(d_v, non_blocking=True)
+            return
         if wl.batched:
-            return ctx.eval_batched(wl.leaves, wl.theta, h_t, h_y, wl.sigma, **want)
-        return ctx.eval(wl.leaves, wl.theta, h_t, h_y, wl.sigma, **want)
+            ctx.eval_batched(wl.leaves, wl.theta, h_t.numpy(), h_y.numpy(), wl.sigma, **want)
+        else:
+            ctx.eval(wl.leaves, wl.theta, h_t.numpy(), h_y.numpy(), wl.sigma, **want)
 
     for _ in range(2):
         e2e_step()
+    torch.cuda.synchronize(dev)
     if ws > 1:
         dist.barrier()
-    torch.cuda.synchronize(dev)
     e_ms = []
     for _ in range(args.steps):
-        a = torch.cuda.Event(enable_timing=True)
-        bv = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
+        ea = torch.cuda.Event(enable_timing=True)
+        eb = torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
         e2e_step()
-        bv.record(stream)
-        bv.synchronize()
-        e_ms.append(a.elapsed_time(bv))
+        eb.record(stream)
+        eb.synchronize()
+        e_ms.append(ea.elapsed_time(eb))
     e_total = float(sum(e_ms))
     if ws > 1:
         tt = torch.tensor([e_total], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e_total = float(tt.item())
-    e2e_value = wl.points * ws * args.steps / (e_total * 1e-3)
-    h2d = 2 * 8 * wl.points
+    e2e_value = points_per_rank * ws * args.steps / (e_total * 1e-3)
+    h2d = 2 * 8 * points_per_rank
     d2h = 8 * (S + S * (nt + 1) + (S * n if want["mean"] else 0) + (S * n if want["var"] else 0))
 
     if rank != 0:
@@ -325,7 +373,7 @@ def run_ours(args, ws, rank, local):
             dist.destroy_process_group()
         return
     peak, peak_src = measured_peaks()
-    abytes = alg_bytes_per_point(dom, wl) * wl.points
+    abytes = alg_bytes_per_point(dom, wl) * points_per_rank
     achieved = abytes / (dom_launch_ms * 1e-3) / 1e9 if abytes else 0.0
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -334,22 +382,29 @@ def run_ours(args, ws, rank, local):
             tr = json.load(f).get(wl.name, {}).get(dom)
         if tr is not None:
             traffic = tr
-    F = core_flops_per_point(b, nt) * wl.points
+    F = core_flops_per_point(b, nt) * points_per_rank
     fp64_achieved = F / (total_ms / args.steps * 1e-3) / 1e12
     clocks = clk.summary()
+    if partitioned:
+        desc = f"{wl.description.split(' single')[0]} ONE series of {n_total} points partitioned over {ws} GPUs"
+        par = f"{ws} ranks, contiguous time segments, NCCL all_gather of 2-separator records + all_reduce"
+    else:
+        desc = wl.description
+        par = "single GPU" if ws == 1 else f"{ws} ranks, series sharded (independent series per rank)"
     line = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": ws, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE shapes; no public dataset)",
-        "config": {"workload": wl.description, "config": wl.name, "points_per_gpu": wl.points,
+        "config": {"workload": desc, "config": wl.name, "points_per_gpu": int(points_per_rank),
                    "outputs": ["loglik"] + list(wl.outputs), "state_dim": b, "n_theta": nt,
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                   "parallelism": "single GPU" if ws == 1 else f"{ws} ranks, independent series per rank"},
+                   "parallelism": par},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "note": f"algorithmic bytes = {alg_bytes_per_point(dom, wl):.0f} B/point x {wl.points} points "
-                             f"per launch / {dom_launch_ms:.4f} ms mean launch; peak {peak_src}"},
+                     "note": f"algorithmic bytes = {alg_bytes_per_point(dom, wl):.0f} B/point x {points_per_rank} "
+                             f"points per launch / {dom_launch_ms:.4f} ms mean launch; peak {peak_src}; the fused "
+                             "path is FP64-bound (see roofline_fp64)"},
         "roofline_fp64": {"bound": "fp64", "achieved": fp64_achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                           "frac": fp64_achieved / FP64_PEAK_TFLOPS,
                           "note": "F_core = 8b^3 + 4b^2(1+n_theta) flop/point (SURVEY.md §8(d), lower bound) "

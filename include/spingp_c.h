@@ -164,6 +164,32 @@ int spingp_assemble(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves
                     int64_t n, double sigma, double* diag, double* upper, double* rhs,
                     int64_t* fail_block);
 
+/* ---- multi-GPU partition of one long series -----------------
+ * Rank r of P owns the contiguous time segment t[s_r .. e_r) (n_local points, device
+ * pointers).  t_left = the last time of rank r-1 (ignored on rank 0), t_right = the
+ * first time of rank r+1 (ignored on the last rank).  Protocol:
+ *   1. spingp_seg_forward_device   -> d_record (n_record doubles): the segment reduced
+ *      to its two boundary separators (Schur complement + logdet partial);
+ *   2. caller all-gathers the P records (rank order) into d_records (e.g. NCCL);
+ *   3. spingp_seg_reverse_device   -> d_partials (n_partials doubles): the P-block
+ *      reduced system is solved redundantly, the segment back-substituted (selected
+ *      inverse, gradient terms, optional per-point mean/var of the segment);
+ *   4. caller all-reduces (sum) d_partials across ranks;
+ *   5. spingp_seg_finalize_device  -> loglik, gradient (identical on every rank).
+ * Steps 1 and 3 must run on the same context with no other evaluation in between. */
+int spingp_seg_sizes(const spingp_leaf* leaves, int32_t n_leaves, int32_t* n_record, int32_t* n_partials);
+int spingp_seg_forward_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
+                              const double* theta, int32_t n_theta, const double* d_t, const double* d_y,
+                              int64_t n_local, double t_left, double t_right, int32_t rank, int32_t nranks,
+                              double sigma, uint32_t flags, double* d_record);
+int spingp_seg_reverse_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
+                              const double* theta, int32_t n_theta, const double* d_t, const double* d_y,
+                              int64_t n_local, double t_left, double t_right, int32_t rank, int32_t nranks,
+                              double sigma, uint32_t flags, const double* d_records, double* d_partials,
+                              double* d_mean, double* d_var);
+int spingp_seg_finalize_device(spingp_ctx* ctx, int32_t n_theta, int64_t n_total, double sigma, uint32_t flags,
+                               const double* d_partials, double* d_loglik, double* d_grad);
+
 /* ---- btd_core on a materialised symmetric BTD --------------- */
 
 /* cr_solve: x = M^{-1} rhs for k right-hand sides, plus log det M. */

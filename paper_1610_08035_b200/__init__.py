@@ -14,7 +14,7 @@ from ._capi import (  # noqa: F401
     WANT_GRAD, WANT_MEAN, WANT_VAR, INCLUDE_NOISE,
     SpingpError, NotPositiveDefinite, SingularProcessNoise, DuplicateTimestamp, DeviceError,
     NegativeVariance, Unsupported,
-    Context, lib, lib_path, kernel_dims, state_space, n_theta,
+    Context, lib, lib_path, kernel_dims, state_space, n_theta, seg_sizes,
 )
 
 __all__ = [
@@ -22,4 +22,5 @@ __all__ = [
     "WANT_GRAD", "WANT_MEAN", "WANT_VAR", "INCLUDE_NOISE",
     "SpingpError", "NotPositiveDefinite", "SingularProcessNoise", "DuplicateTimestamp", "DeviceError",
     "NegativeVariance", "Unsupported", "Context", "lib", "lib_path", "kernel_dims", "state_space", "n_theta",
+    "seg_sizes",
 ]

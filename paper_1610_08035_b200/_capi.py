@@ -91,6 +91,12 @@ SIGNATURES = {
     "spingp_eval_batched_device": (ctypes.c_int, [_vp, _vp, _i32, _d, _i32, _i64, _i64, _vp, _vp, _d, _u32, _vp, _vp,
                                                   _vp, _vp]),
     "spingp_assemble": (ctypes.c_int, [_vp, _vp, _i32, _d, _i32, _d, _d, _i64, _dbl, _d, _d, _d, _i64p]),
+    "spingp_seg_sizes": (ctypes.c_int, [_vp, _i32, _i32p, _i32p]),
+    "spingp_seg_forward_device": (ctypes.c_int, [_vp, _vp, _i32, _d, _i32, _vp, _vp, _i64, _dbl, _dbl, _i32, _i32, _dbl,
+                                                 _u32, _vp]),
+    "spingp_seg_reverse_device": (ctypes.c_int, [_vp, _vp, _i32, _d, _i32, _vp, _vp, _i64, _dbl, _dbl, _i32, _i32, _dbl,
+                                                 _u32, _vp, _vp, _vp, _vp]),
+    "spingp_seg_finalize_device": (ctypes.c_int, [_vp, _i32, _i64, _dbl, _u32, _vp, _vp, _vp]),
     "spingp_btd_cr_solve": (ctypes.c_int, [_vp, _i64, _i32, _d, _d, _d, _i32, _d, _d, _i64p]),
     "spingp_btd_cr_solve_device": (ctypes.c_int, [_vp, _i64, _i32, _vp, _vp, _vp, _i32, _vp, _vp]),
     "spingp_btd_selinv": (ctypes.c_int, [_vp, _i64, _i32, _d, _d, _d, _d, _d, _i64p]),
@@ -150,6 +156,14 @@ def kernel_dims(leaves):
     b, nt = _i32(), _i32()
     _raise(lib().spingp_kernel_dims(lv.ctypes.data, len(leaves), ctypes.byref(b), ctypes.byref(nt)))
     return b.value, nt.value
+
+
+def seg_sizes(leaves):
+    """(record length, partials length) of the multi-GPU segment protocol."""
+    nrec, npart = _i32(), _i32()
+    lv = _leaves(leaves)
+    _raise(lib().spingp_seg_sizes(lv.ctypes.data, len(leaves), ctypes.byref(nrec), ctypes.byref(npart)))
+    return nrec.value, npart.value
 
 
 def state_space(leaves, theta):
@@ -325,6 +339,28 @@ class Context:
         _raise(lib().spingp_eval_batched_device(self._h, lv.ctypes.data, len(leaves), _p(th), th.shape[1], int(S),
                                                 int(n), d_t, d_y, _p(sg), int(flags), d_loglik, d_grad or None,
                                                 d_mean or None, d_var or None))
+
+    # ---- multi-GPU partition of one series (segment protocol, include/spingp_c.h) -----
+    def seg_forward_device(self, leaves, theta, d_t, d_y, n_local, t_left, t_right, rank, nranks, sigma, flags,
+                           d_record):
+        lv = _leaves(leaves)
+        th = _f64(theta)
+        _raise(lib().spingp_seg_forward_device(self._h, lv.ctypes.data, len(leaves), _p(th), len(th), d_t, d_y,
+                                               int(n_local), float(t_left), float(t_right), int(rank), int(nranks),
+                                               float(sigma), int(flags), d_record))
+
+    def seg_reverse_device(self, leaves, theta, d_t, d_y, n_local, t_left, t_right, rank, nranks, sigma, flags,
+                           d_records, d_partials, d_mean=0, d_var=0):
+        lv = _leaves(leaves)
+        th = _f64(theta)
+        _raise(lib().spingp_seg_reverse_device(self._h, lv.ctypes.data, len(leaves), _p(th), len(th), d_t, d_y,
+                                               int(n_local), float(t_left), float(t_right), int(rank), int(nranks),
+                                               float(sigma), int(flags), d_records, d_partials, d_mean or None,
+                                               d_var or None))
+
+    def seg_finalize_device(self, n_theta, n_total, sigma, flags, d_partials, d_loglik, d_grad=0):
+        _raise(lib().spingp_seg_finalize_device(self._h, int(n_theta), int(n_total), float(sigma), int(flags),
+                                                d_partials, d_loglik, d_grad or None))
 
     def btd_cr_solve_device(self, n, b, d_diag, d_upper, d_rhs, k, d_x, d_logdet):
         _raise(lib().spingp_btd_cr_solve_device(self._h, int(n), int(b), d_diag, d_upper, d_rhs, int(k), d_x, d_logdet))

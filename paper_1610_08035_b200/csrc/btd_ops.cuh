@@ -50,7 +50,7 @@ void launch_btd(spingp_ctx* ctx, int64_t n, int b, const double* d_diag, const d
     ctx->launched("k_top");
     for (int l = g.nlev - 1; l >= 1; --l) {
         RecSource<B> src{rec[l - 1], g.K[l - 1], g.n[l]};
-        SolSink<B> sink{sol[l], g.n[l], g.n[l]};
+        SolSink<B> sink{sol[l], g.n[l], g.n[l], 0};
         ctx->pre();
         k_revL<B, RecSource<B>, SolSink<B>><<<blocks_for(g.K[l], tpb), tpb, 0, ctx->stream>>>(
             src, sink, g, l, fac[l], sol[l + 1], needC ? 1 : 0);

@@ -126,6 +126,48 @@ spingp_ctx* checked(spingp_ctx* ctx) {
 
 }  // namespace
 
+// ---- multi-GPU partition of one long series (segment mode) -------
+
+int spingp_seg_sizes(const spingp_leaf* leaves, int32_t n_leaves, int32_t* n_record, int32_t* n_partials) {
+    return guarded(nullptr, [&] {
+        int32_t b = 0, nt = 0;
+        const int st = spingp_kernel_dims(leaves, n_leaves, &b, &nt);
+        if (st != SPINGP_OK) return st;
+        const HostModel hm = build_model(leaves, n_leaves, nt);
+        const int B = plan_bsize(hm);
+        if (n_record) *n_record = 3 * B * B + 2 * B + 1;  // Rec<B>::N
+        if (n_partials) *n_partials = 5 + nt;             // P_GRAD + nt
+        return SPINGP_OK;
+    });
+}
+
+static int seg_run(spingp_ctx* ctx, int mode, const spingp_leaf* leaves, int32_t n_leaves, const double* theta,
+                   int32_t n_theta, const double* d_t, const double* d_y, int64_t n_local, double t_left,
+                   double t_right, int32_t rank, int32_t nranks, double sigma, uint32_t flags,
+                   const double* d_in, double* d_out, double* d_mean, double* d_var) {
+    return guarded(nullptr, [&] {
+        checked(ctx);
+        if (!theta || !d_t || !d_y || !d_out || (mode == 3 && !d_in)) throw std::invalid_argument("null argument");
+        if (nranks < 1 || rank < 0 || rank >= nranks || nranks > 64) throw std::invalid_argument("bad rank / nranks");
+        if (rank > 0 && !(t_left < 0.0 || t_left >= 0.0)) throw std::invalid_argument("missing left halo time");
+        if (rank + 1 < nranks && !(t_right < 0.0 || t_right >= 0.0)) throw std::invalid_argument("missing right halo time");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        const HostModel hm = build_model(leaves, n_leaves, n_theta);
+        Plan plan = make_plan(n_local, 1, plan_bsize(hm), ctx->m0_override);
+        plan.geo.segL = rank > 0 ? 1 : 0;
+        plan.geo.segR = rank + 1 < nranks ? 1 : 0;
+        std::vector<double> params(hm.rec_stride + 2, 0.0);
+        fill_record(hm, theta, sigma, params.data());
+        params[hm.rec_stride] = t_left;
+        params[hm.rec_stride + 1] = t_right;
+        EvalArgs a{&hm, &plan, params.data(), params.size(), d_t, d_y, flags, nullptr, nullptr,
+                   (flags & SPINGP_WANT_MEAN) ? d_mean : nullptr, (flags & SPINGP_WANT_VAR) ? d_var : nullptr,
+                   mode, nullptr, nullptr, nullptr, rank, nranks, d_in, d_out};
+        dispatch_eval(ctx, a);
+        return SPINGP_OK;
+    });
+}
+
 extern "C" {
 
 int spingp_abi_version(void) { return SPINGP_ABI_VERSION; }
@@ -358,6 +400,37 @@ int spingp_assemble(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves
         if (upper && nu) CUDA_OK(cudaMemcpyAsync(upper, d_u, nu * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         if (rhs) CUDA_OK(cudaMemcpyAsync(rhs, d_r, n * b * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         return take_status(ctx, fail_block);
+    });
+}
+
+int spingp_seg_forward_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
+                              const double* theta, int32_t n_theta, const double* d_t, const double* d_y,
+                              int64_t n_local, double t_left, double t_right, int32_t rank, int32_t nranks,
+                              double sigma, uint32_t flags, double* d_record) {
+    return seg_run(ctx, 2, leaves, n_leaves, theta, n_theta, d_t, d_y, n_local, t_left, t_right, rank, nranks,
+                   sigma, flags, nullptr, d_record, nullptr, nullptr);
+}
+
+int spingp_seg_reverse_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
+                              const double* theta, int32_t n_theta, const double* d_t, const double* d_y,
+                              int64_t n_local, double t_left, double t_right, int32_t rank, int32_t nranks,
+                              double sigma, uint32_t flags, const double* d_records, double* d_partials,
+                              double* d_mean, double* d_var) {
+    return seg_run(ctx, 3, leaves, n_leaves, theta, n_theta, d_t, d_y, n_local, t_left, t_right, rank, nranks,
+                   sigma, flags, d_records, d_partials, d_mean, d_var);
+}
+
+int spingp_seg_finalize_device(spingp_ctx* ctx, int32_t n_theta, int64_t n_total, double sigma, uint32_t flags,
+                               const double* d_partials, double* d_loglik, double* d_grad) {
+    return guarded(nullptr, [&] {
+        checked(ctx);
+        if (!d_partials || !d_loglik || ((flags & SPINGP_WANT_GRAD) && !d_grad)) throw std::invalid_argument("null argument");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        SegFinalArgs fa{d_partials, n_theta, n_total, sigma, d_loglik, (flags & SPINGP_WANT_GRAD) ? d_grad : nullptr};
+        ctx->pre();
+        k_seg_final<<<1, 32, 0, ctx->stream>>>(fa);
+        ctx->launched("k_seg_final");
+        return SPINGP_OK;
     });
 }
 

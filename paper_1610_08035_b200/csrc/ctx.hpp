@@ -167,10 +167,15 @@ struct EvalArgs {
     double* d_mean;
     double* d_var;
     // mode 1: assemble only into d_diag / d_upper / d_rhs (S = 1)
+    // mode 2: segment forward -> d_seg_out (this rank's top-level record)
+    // mode 3: segment reverse from d_seg_in (all ranks' records) -> d_seg_out (partial sums)
     int mode;
     double* d_diag;
     double* d_upper;
     double* d_rhs;
+    int rank = 0, nranks = 1;
+    const double* d_seg_in = nullptr;
+    double* d_seg_out = nullptr;
 };
 // one translation unit per instantiation (inst_*.cu, btd_b*.cu) so they build in parallel
 void eval_matern_1(spingp_ctx* ctx, const EvalArgs& a);

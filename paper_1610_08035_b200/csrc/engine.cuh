@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(128, 3) k_fwd0(ModelDesc md, const double* __r
                                               const double* __restrict__ y, Geom geo,
                                               double* __restrict__ fac, double* __restrict__ rec,
                                               double* __restrict__ part,
-                                              unsigned long long* status) {
+                                              unsigned long long* status,
+                                              const double* __restrict__ halo) {
     constexpr int B = T::B;
     const long long K = geo.K[0], SK = K * geo.S;
     const long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -249,12 +250,12 @@ __global__ void __launch_bounds__(128, 3) k_fwd0(ModelDesc md, const double* __r
     const double* rp = params + static_cast<long long>(s) * md.rec_stride;
     const double sig = rp[0], jit = rp[1], is2 = 1.0 / (sig * sig);
     const long long gbase = static_cast<long long>(s) * n;
-    const bool hasL = c > 0;
+    const bool hasL = c > 0 || geo.segL;
 
     double Phi[B * B], Q[B * B], Mq[B * B];
     double dt = -1.0;
-    if (st > 0) {
-        dt = ts[st] - ts[st - 1];
+    if (st > 0 || geo.segL) {
+        dt = ts[st] - (st > 0 ? ts[st - 1] : halo[2 * s]);
         if (!(dt > 0.0) || !isfinite(dt)) {
             report(status, gbase + st, dt == 0.0 ? ST_DUPLICATE : ST_BAD_ARG);
             return;
@@ -317,8 +318,8 @@ SP_UNROLL
     double D[B * B], Rr[B];
 SP_UNROLL
     for (int i = 0; i < B * B; ++i) D[i] = Qinv[i] + HH[i];
-    if (en < n) {
-        const double dte = ts[en] - ts[en - 1];
+    if (en < n || geo.segR) {
+        const double dte = (en < n ? ts[en] : halo[2 * s + 1]) - ts[en - 1];
         if (!(dte > 0.0) || !isfinite(dte)) {
             report(status, gbase + en, dte == 0.0 ? ST_DUPLICATE : ST_BAD_ARG);
             return;
@@ -370,6 +371,14 @@ SP_UNROLL
 SP_UNROLL
         for (int q = 0; q < B * B; ++q) U[q] = rec[(Rec<B>::LR + q) * SKp + i1];
     }
+    // segment mode: what block 0's record contributes to the segment's left separator
+    SP_DEV void left_contrib(int s, double* D, double* r) const {
+        const long long i0 = static_cast<long long>(s) * n;
+SP_UNROLL
+        for (int q = 0; q < B * B; ++q) D[q] = rec[(Rec<B>::LDIAG + q) * SKp + i0];
+SP_UNROLL
+        for (int q = 0; q < B; ++q) r[q] = rec[(Rec<B>::LRHS + q) * SKp + i0];
+    }
 };
 
 // Block source for a user SymBTD (row-major diag[n][b][b], upper[n-1][b][b],
@@ -397,6 +406,10 @@ SP_UNROLL
 SP_UNROLL
             for (int q = 0; q < B; ++q) U[p * B + q] = (p < b && q < b) ? up[(i * b + p) * b + q] : 0.0;
     }
+    SP_DEV void left_contrib(int, double* D, double* r) const {
+        mzero<B>(D);
+        vzero<B>(r);
+    }
 };
 
 template <int B, class Src>
@@ -411,10 +424,11 @@ __global__ void __launch_bounds__(128) k_fwdL(Src src, Geom geo, int lev, double
     const long long n = geo.n[lev];
     const int m = geo.m[lev];
     const long long st = c * m, en = min(n, st + m);
-    const bool hasL = c > 0;
+    const bool hasL = c > 0 || geo.segL;
     const long long gbase = static_cast<long long>(s) * geo.n[0];
     ElimState<B> es;
     elim_init<B>(es);
+    if (c == 0 && geo.segL) src.left_contrib(s, es.accLL, es.accrL);  // carried to the segment's L
     if (hasL) {  // P_{st, st-1} = upper(st-1)^T
         double U[B * B];
         src.upper(s, st - 1, U);
@@ -589,12 +603,13 @@ SP_UNROLL
 
 // Solution sinks for the reverse sweep of levels >= 1.
 template <int B>
-struct SolSink {  // component-major sol of this level
+struct SolSink {  // component-major sol of this level (segment mode: slot -1 = left separator)
     double* sol;
-    long long Sn;  // S * n
+    long long Sn;  // S * (n + segL)
     long long n;
+    int segL;
     SP_DEV void put(int s, long long i, const double* x, const double* Cd, bool needC) const {
-        const long long k = static_cast<long long>(s) * n + i;
+        const long long k = static_cast<long long>(s) * (n + segL) + segL + i;
 SP_UNROLL
         for (int q = 0; q < B; ++q) sol[(Sol<B>::X + q) * Sn + k] = x[q];
         if (needC)
@@ -602,7 +617,7 @@ SP_UNROLL
             for (int q = 0; q < B * B; ++q) sol[(Sol<B>::CD + q) * Sn + k] = Cd[q];
     }
     SP_DEV void put_upper(int s, long long i, const double* Cu) const {
-        const long long k = static_cast<long long>(s) * n + i;
+        const long long k = static_cast<long long>(s) * (n + segL) + segL + i;
 SP_UNROLL
         for (int q = 0; q < B * B; ++q) sol[(Sol<B>::CU + q) * Sn + k] = Cu[q];
     }
@@ -639,9 +654,10 @@ __global__ void __launch_bounds__(128) k_revL(Src src, Sink sink, Geom geo, int 
     const long long n = geo.n[lev];
     const int m = geo.m[lev];
     const long long st = c * m, en = min(n, st + m);
-    const bool hasL = c > 0;
+    const bool hasL = c > 0 || geo.segL;
     SepData<B> sd;
-    load_sep<B>(solU, static_cast<long long>(geo.S) * geo.n[lev + 1], g, hasL, needC, sd);
+    load_sep<B>(solU, static_cast<long long>(geo.S) * (geo.n[lev + 1] + geo.segL), g + geo.segL * (s + 1), hasL,
+                needC, sd);
     double xn[B], Cnn[B * B], CnL[B * B];
 SP_UNROLL
     for (int q = 0; q < B; ++q) xn[q] = sd.xR[q];
@@ -651,6 +667,7 @@ SP_UNROLL
 SP_UNROLL
         for (int j = 0; j < B; ++j) CnL[i * B + j] = sd.CLR[j * B + i];
     sink.put(s, en - 1, xn, Cnn, needC);
+    if (c == 0 && geo.segL) sink.put(s, -1, sd.xL, sd.CLL, needC);  // propagate the left separator
     double Li[B * B], Y[B * B], z[B], U[B * B];
     if (en - 2 >= st) {
         load_fac<B>(fac + (en - 2 - st) * Fac<B>::N * SK + g, SK, hasL, Li, Y, z);
@@ -818,7 +835,8 @@ __global__ void __launch_bounds__(128) k_rev0(ModelDesc md, const double* __rest
                                               const double* __restrict__ fac,
                                               const double* __restrict__ solU,
                                               double* __restrict__ part, Outs outs,
-                                              unsigned long long* status) {
+                                              unsigned long long* status,
+                                              const double* __restrict__ halo) {
     constexpr int B = T::B;
     const long long K = geo.K[0], SK = K * geo.S;
     const long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -833,11 +851,12 @@ __global__ void __launch_bounds__(128) k_rev0(ModelDesc md, const double* __rest
     const double* rp = params + static_cast<long long>(s) * md.rec_stride;
     const double sig = rp[0], jit = rp[1], is2 = 1.0 / (sig * sig);
     const long long gbase = static_cast<long long>(s) * n;
-    const bool hasL = c > 0;
+    const bool hasL = c > 0 || geo.segL;
     const bool needC = outs.need_c != 0, grad = outs.want_grad != 0;
 
     SepData<B> sd;
-    load_sep<B>(solU, static_cast<long long>(geo.S) * geo.n[1], g, hasL, needC, sd);
+    load_sep<B>(solU, static_cast<long long>(geo.S) * (geo.n[1] + geo.segL), g + geo.segL * (s + 1), hasL, needC,
+                sd);
     double xn[B], Cnn[B * B], CnL[B * B];
 SP_UNROLL
     for (int q = 0; q < B; ++q) xn[q] = sd.xR[q];
@@ -876,8 +895,8 @@ SP_UNROLL
     // block st: previous block is the left separator (or the anchor at st = 0)
     point_out<T>(md, outs, gbase + st, ys[st], is2, sig, xn, Cnn, fy, noise, status);
     {
-        const bool anchor = st == 0;
-        const double dt = anchor ? -1.0 : ts[st] - ts[st - 1];
+        const bool anchor = st == 0 && !geo.segL;
+        const double dt = anchor ? -1.0 : ts[st] - (st > 0 ? ts[st - 1] : halo[2 * s]);
         double Ph[B * B], Qr[B * B], Mq[B * B], ldq0;
         T::step(md, rp, dt, Ph, Qr);
         qt_factor<B>(Qr, jit, md.b, Mq, &ldq0);
@@ -935,6 +954,7 @@ struct FinalArgs {
     long long n;
     double* loglik;        // [S]
     double* grad;          // [S][nt+1] or null
+    double* partials;      // segment mode: raw sums (logdetP total, fit_y, fit_e, logdetQ, noise, grad...)
 };
 
 // Stage 2: one CTA per series.  Deterministic fixed-order tree sums.
@@ -969,6 +989,11 @@ static __global__ void k_reduce_final(FinalArgs a, Geom geo) {
         if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
         __syncthreads();
     }
+    if (threadIdx.x == 0 && a.partials) {
+        for (int c = 0; c < a.NC; ++c) a.partials[c] = acc[c];
+        a.partials[P_LOGDET] = acc[P_LOGDET] + sh[0] + a.toplogdet[s];
+        return;
+    }
     if (threadIdx.x == 0) {
         const double ldP = acc[P_LOGDET] + sh[0] + a.toplogdet[s];
         const double* rp = a.params + static_cast<long long>(s) * a.rec_stride;
@@ -982,6 +1007,117 @@ static __global__ void k_reduce_final(FinalArgs a, Geom geo) {
             for (int p = 0; p < a.nt; ++p) gs[p] = acc[P_GRAD + p];
             gs[a.nt] = 2.0 * sig * (-0.5 * nn / s2 + acc[P_NOISE] / (2.0 * s2 * s2));
         }
+    }
+}
+
+// ===================================================== multi-GPU reduced system ==
+// Segment mode: rank r has reduced its time segment to a 2-separator record
+// (left separator = rank r-1's last block, right = its own last block).  Every rank
+// solves the P-block BTD of the ranks' last blocks redundantly (P <= a few dozen),
+// then keeps x and the selected-inverse blocks it needs for its reverse sweep:
+//   sol slot 0 (segL only) = (x_{r-1}, C_{r-1,r-1}), Cu slot 0 = C_{r-1,r}; next slot = (x_r, C_rr).
+// recs: P records, each Rec<B>::N contiguous doubles (the K = 1 top-level record).
+template <int B>
+__global__ void k_seg_solve(int P, int rank, const double* __restrict__ recs, double* __restrict__ sol,
+                            double* __restrict__ toplogdet, unsigned long long* status, long long gidx) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    constexpr int NR = Rec<B>::N;
+    constexpr int kMaxP = 64;
+    double S_L[B * B], T[B * B], rc[B];
+    double Ls[kMaxP][B * B], Zs[kMaxP][B], Xs[kMaxP][B * B];  // factor per block (P <= 64)
+    mzero<B>(T);
+    vzero<B>(rc);
+    double ld = 0.0;
+    for (int r = 0; r < P; ++r) {
+        const double* R0 = recs + static_cast<long long>(r) * NR;
+        const double* R1 = recs + static_cast<long long>(r + 1) * NR;
+        double D[B * B], U[B * B], rhs[B];
+        for (int q = 0; q < B * B; ++q)
+            D[q] = R0[Rec<B>::RDIAG + q] + (r + 1 < P ? R1[Rec<B>::LDIAG + q] : 0.0) - T[q];
+        for (int q = 0; q < B; ++q) rhs[q] = R0[Rec<B>::RRHS + q] + (r + 1 < P ? R1[Rec<B>::LRHS + q] : 0.0) - rc[q];
+        msym<B>(D);
+        double ldr;
+        if (!chol<B>(S_L, D, ldr)) {
+            report(status, gidx, ST_NOT_PD);
+            return;
+        }
+        ld += ldr;
+        mcopy<B>(Ls[r], S_L);
+        lsolve_v<B>(Zs[r], S_L, rhs);
+        if (r + 1 < P) {
+            for (int q = 0; q < B * B; ++q) U[q] = R1[Rec<B>::LR + q];
+            lsolve<B>(Xs[r], S_L, U);
+            mtm_sym<B>(T, Xs[r], Xs[r]);
+            mtv<B>(rc, Xs[r], Zs[r]);
+        }
+    }
+    // back substitution + Takahashi down to block rank-1
+    double xn[B], Cnn[B * B], xj[B], Cjn[B * B], Cjj[B * B];
+    {
+        ltsolve_v<B>(xn, Ls[P - 1], Zs[P - 1]);
+        double I[B * B], X[B * B];
+        for (int q = 0; q < B * B; ++q) I[q] = (q % (B + 1) == 0) ? 1.0 : 0.0;
+        lsolve<B>(X, Ls[P - 1], I);
+        ltsolve<B>(Cnn, Ls[P - 1], X);
+        msym<B>(Cnn);
+    }
+    const int lo = rank > 0 ? rank - 1 : rank;
+    double xr[B], Crr[B * B], xl[B], Cll[B * B], Clr[B * B];
+    if (P - 1 == rank) {
+        for (int q = 0; q < B; ++q) xr[q] = xn[q];
+        mcopy<B>(Crr, Cnn);
+    }
+    for (int j = P - 2; j >= lo; --j) {
+        SepData<B> none;
+        vzero<B>(none.xL);
+        mzero<B>(none.CLL);
+        mzero<B>(none.CLR);
+        double Y0[B * B], CnL0[B * B], CjL0[B * B];
+        mzero<B>(Y0);
+        mzero<B>(CnL0);
+        back_step<B>(Ls[j], Y0, Zs[j], Xs[j], false, true, none, xn, Cnn, CnL0, xj, CjL0, Cjn, Cjj);
+        if (j == rank) {
+            for (int q = 0; q < B; ++q) xr[q] = xj[q];
+            mcopy<B>(Crr, Cjj);
+        }
+        if (j == rank - 1) {
+            for (int q = 0; q < B; ++q) xl[q] = xj[q];
+            mcopy<B>(Cll, Cjj);
+            mcopy<B>(Clr, Cjn);
+        }
+        for (int q = 0; q < B; ++q) xn[q] = xj[q];
+        mcopy<B>(Cnn, Cjj);
+    }
+    const int segL = rank > 0 ? 1 : 0;
+    const long long Sn = 1 + segL;
+    if (segL) {
+        for (int q = 0; q < B; ++q) sol[(Sol<B>::X + q) * Sn + 0] = xl[q];
+        for (int q = 0; q < B * B; ++q) sol[(Sol<B>::CD + q) * Sn + 0] = Cll[q];
+        for (int q = 0; q < B * B; ++q) sol[(Sol<B>::CU + q) * Sn + 0] = Clr[q];
+    }
+    for (int q = 0; q < B; ++q) sol[(Sol<B>::X + q) * Sn + segL] = xr[q];
+    for (int q = 0; q < B * B; ++q) sol[(Sol<B>::CD + q) * Sn + segL] = Crr[q];
+    toplogdet[0] = rank == 0 ? ld : 0.0;
+}
+
+// After the all-reduce of the ranks' partial sums: loglik and gradient.
+struct SegFinalArgs {
+    const double* sums;  // [P_GRAD + nt]: (logdetP, fit_y, fit_e, logdetQ, noise, grad...)
+    int nt;
+    long long n;         // total points over all ranks
+    double sigma;
+    double* loglik;
+    double* grad;
+};
+static __global__ void k_seg_final(SegFinalArgs a) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const double s2 = a.sigma * a.sigma, nn = static_cast<double>(a.n);
+    const double kLog2Pi = 1.8378770664093454835606594728112;
+    a.loglik[0] = -0.5 * (a.sums[P_FITY] + a.sums[P_FITE]) -
+                  0.5 * (a.sums[P_LOGDET] + a.sums[P_LDQ] + nn * log(s2)) - 0.5 * nn * kLog2Pi;
+    if (a.grad) {
+        for (int p = 0; p < a.nt; ++p) a.grad[p] = a.sums[P_GRAD + p];
+        a.grad[a.nt] = 2.0 * a.sigma * (-0.5 * nn / s2 + a.sums[P_NOISE] / (2.0 * s2 * s2));
     }
 }
 

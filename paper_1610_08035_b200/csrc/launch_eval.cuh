@@ -29,7 +29,7 @@ EvalBufs carve_eval(spingp_ctx* ctx, const Plan& p, int nt, size_t params_count)
         const size_t SK = static_cast<size_t>(g.K[l]) * g.S;
         tot += arena_bytes(static_cast<size_t>(g.m[l]) * Fac<B>::N * SK) + arena_bytes(Rec<B>::N * SK);
     }
-    for (int l = 1; l <= g.nlev; ++l) tot += arena_bytes(Sol<B>::N * static_cast<size_t>(g.n[l]) * g.S);
+    for (int l = 1; l <= g.nlev; ++l) tot += arena_bytes(Sol<B>::N * static_cast<size_t>(g.n[l] + g.segL) * g.S);
     const size_t SK0 = static_cast<size_t>(g.K[0]) * g.S;
     const int nseg = static_cast<int>((g.K[0] + kSeg - 1) / kSeg);
     tot += arena_bytes(g.S) + arena_bytes((P_GRAD + nt) * SK0) +
@@ -44,7 +44,7 @@ EvalBufs carve_eval(spingp_ctx* ctx, const Plan& p, int nt, size_t params_count)
         eb.rec[l] = ctx->ws.take<double>(Rec<B>::N * SK);
     }
     for (int l = 1; l <= g.nlev; ++l)
-        eb.sol[l] = ctx->ws.take<double>(Sol<B>::N * static_cast<size_t>(g.n[l]) * g.S);
+        eb.sol[l] = ctx->ws.take<double>(Sol<B>::N * static_cast<size_t>(g.n[l] + g.segL) * g.S);
     eb.toplogdet = ctx->ws.take<double>(g.S);
     eb.part = ctx->ws.take<double>((P_GRAD + nt) * SK0);
     eb.nseg = nseg;
@@ -68,6 +68,8 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     ctx->stage_done();
     ModelDesc md = hm.desc;
     md.eqconst = eb.params + a.nparams;
+    // segment halo times (t_left, t_right) are the last two doubles of h_params' tail
+    const double* halo = (a.mode >= 2) ? eb.params + a.nparams - 2 : nullptr;
 
     const int tpb = 128;
     if (a.mode == 1) {
@@ -78,9 +80,12 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
         return;
     }
     const long long SK0 = g.K[0] * g.S;
+    const bool grad = a.flags & SPINGP_WANT_GRAD;
+    const bool needC = grad || (a.flags & SPINGP_WANT_VAR);
+    if (a.mode != 3) {
     ctx->pre();
     k_fwd0<T><<<blocks_for(SK0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
-                                                             eb.rec[0], eb.part, ctx->d_status);
+                                                             eb.rec[0], eb.part, ctx->d_status, halo);
     ctx->launched("k_fwd0");
     for (int l = 1; l < g.nlev; ++l) {
         RecSource<B> src{eb.rec[l - 1], g.K[l - 1] * g.S, g.n[l]};
@@ -89,15 +94,26 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
             src, g, l, eb.fac[l], eb.rec[l], ctx->d_status);
         ctx->launched("k_fwd");
     }
-    ctx->pre();
-    k_top<B><<<blocks_for(g.S, 128), 128, 0, ctx->stream>>>(g, eb.rec[g.nlev - 1], eb.sol[g.nlev],
-                                                           eb.toplogdet, ctx->d_status);
-    ctx->launched("k_top");
-    const bool grad = a.flags & SPINGP_WANT_GRAD;
-    const bool needC = grad || (a.flags & SPINGP_WANT_VAR);
+    }
+    if (a.mode == 2) {  // segment forward: hand this rank's top-level record to the caller
+        CUDA_OK(cudaMemcpyAsync(a.d_seg_out, eb.rec[g.nlev - 1], Rec<B>::N * sizeof(double),
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+        return;
+    }
+    if (a.mode == 3) {
+        ctx->pre();
+        k_seg_solve<B><<<1, 1, 0, ctx->stream>>>(a.nranks, a.rank, a.d_seg_in, eb.sol[g.nlev], eb.toplogdet,
+                                                 ctx->d_status, g.n[0] - 1);
+        ctx->launched("k_seg_solve");
+    } else {
+        ctx->pre();
+        k_top<B><<<blocks_for(g.S, 128), 128, 0, ctx->stream>>>(g, eb.rec[g.nlev - 1], eb.sol[g.nlev],
+                                                               eb.toplogdet, ctx->d_status);
+        ctx->launched("k_top");
+    }
     for (int l = g.nlev - 1; l >= 1; --l) {
         RecSource<B> src{eb.rec[l - 1], g.K[l - 1] * g.S, g.n[l]};
-        SolSink<B> sink{eb.sol[l], g.n[l] * g.S, g.n[l]};
+        SolSink<B> sink{eb.sol[l], (g.n[l] + g.segL) * g.S, g.n[l], g.segL};
         ctx->pre();
         k_revL<B, RecSource<B>, SolSink<B>><<<blocks_for(g.K[l] * g.S, tpb), tpb, 0, ctx->stream>>>(
             src, sink, g, l, eb.fac[l], eb.sol[l + 1], needC ? 1 : 0);
@@ -107,7 +123,7 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
               (a.flags & SPINGP_INCLUDE_NOISE) ? 1 : 0, grad ? 1 : 0, needC ? 1 : 0};
     ctx->pre();
     k_rev0<T><<<blocks_for(SK0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
-                                                             eb.sol[1], eb.part, outs, ctx->d_status);
+                                                             eb.sol[1], eb.part, outs, ctx->d_status, halo);
     ctx->launched("k_rev0");
     const int NC = P_GRAD + nt;
     ctx->pre();
@@ -126,6 +142,7 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     fa.n = g.n[0];
     fa.loglik = a.d_loglik;
     fa.grad = grad ? a.d_grad : nullptr;
+    fa.partials = a.mode == 3 ? a.d_seg_out : nullptr;
     ctx->pre();
     k_reduce_final<<<g.S, 256, 0, ctx->stream>>>(fa, g);
     ctx->launched("k_reduce_final");

@@ -31,6 +31,10 @@ struct Geom {
     long long n[kMaxLev + 1];  // blocks per series at each level (n[0] = points)
     long long K[kMaxLev];      // chunks per series at each level
     int m[kMaxLev];            // chunk length at each level
+    // segment mode (multi-GPU partition of one long series): the first
+    // block couples to a left separator held by the previous rank (segL) and the last
+    // block's diagonal includes the step to the next rank's first time (segR).
+    int segL, segR;
 };
 
 }  // namespace spingp_dev

@@ -6,6 +6,7 @@
 #include "cuda_host_emu.h"
 
 #include <cstring>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -46,7 +47,7 @@ void emu_eval(const HostModel& hm, const Plan& plan, std::vector<double>& params
     const int tpb = 32;
     unsigned long long* st = &g_status;
     emu_launch(nblocks(SK0, tpb), tpb, [&] {
-        k_fwd0<T>(md, params.data(), t, y, g, fac[0].data(), rec[0].data(), part.data(), st);
+        k_fwd0<T>(md, params.data(), t, y, g, fac[0].data(), rec[0].data(), part.data(), st, nullptr);
     });
     for (int l = 1; l < g.nlev; ++l) {
         RecSource<B> src{rec[l - 1].data(), g.K[l - 1] * g.S, g.n[l]};
@@ -57,7 +58,7 @@ void emu_eval(const HostModel& hm, const Plan& plan, std::vector<double>& params
     const bool gr = flags & 1u, needC = gr || (flags & 4u);
     for (int l = g.nlev - 1; l >= 1; --l) {
         RecSource<B> src{rec[l - 1].data(), g.K[l - 1] * g.S, g.n[l]};
-        SolSink<B> sink{sol[l].data(), g.n[l] * g.S, g.n[l]};
+        SolSink<B> sink{sol[l].data(), g.n[l] * g.S, g.n[l], 0};
         emu_launch(nblocks(g.K[l] * g.S, tpb), tpb, [&] {
             k_revL<B, RecSource<B>, SolSink<B>>(src, sink, g, l, fac[l].data(), sol[l + 1].data(), needC ? 1 : 0);
         });
@@ -65,7 +66,7 @@ void emu_eval(const HostModel& hm, const Plan& plan, std::vector<double>& params
     Outs outs{(flags & 2u) ? mean : nullptr, (flags & 4u) ? var : nullptr, (flags & 8u) ? 1 : 0, gr ? 1 : 0,
               needC ? 1 : 0};
     emu_launch(nblocks(SK0, tpb), tpb, [&] {
-        k_rev0<T>(md, params.data(), t, y, g, fac[0].data(), sol[1].data(), part.data(), outs, st);
+        k_rev0<T>(md, params.data(), t, y, g, fac[0].data(), sol[1].data(), part.data(), outs, st, nullptr);
     });
     for (int s = 0; s < g.S; ++s) {
         double acc[P_GRAD + kMaxTheta] = {};
@@ -112,7 +113,7 @@ void emu_btd(int64_t n, int b, const double* diag, const double* upper, const do
     emu_launch(1, 1, [&] { k_top<B>(g, rec[g.nlev - 1].data(), sol[g.nlev].data(), top.data(), st); });
     for (int l = g.nlev - 1; l >= 1; --l) {
         RecSource<B> src{rec[l - 1].data(), g.K[l - 1], g.n[l]};
-        SolSink<B> sink{sol[l].data(), g.n[l], g.n[l]};
+        SolSink<B> sink{sol[l].data(), g.n[l], g.n[l], 0};
         emu_launch(nblocks(g.K[l], tpb), tpb, [&] {
             k_revL<B, RecSource<B>, SolSink<B>>(src, sink, g, l, fac[l].data(), sol[l + 1].data(), needC ? 1 : 0);
         });
@@ -128,6 +129,90 @@ void emu_btd(int64_t n, int b, const double* diag, const double* upper, const do
         *logdet = ld;
     }
 }
+
+// ---------------------------------------------------------------- segment mode ----
+// Multi-rank partition of one series (one rank per process or emulated in turn).
+struct SegStateBase {
+    virtual ~SegStateBase() = default;
+    virtual void forward(double* record) = 0;
+    virtual void reverse(const double* records, double* partials, double* mean, double* var) = 0;
+};
+
+template <class T>
+struct SegState : SegStateBase {
+    static constexpr int B = T::B;
+    HostModel hm;
+    Plan plan;
+    std::vector<double> params, eqc;
+    const double* t;
+    const double* y;
+    uint32_t flags;
+    int rank, nranks;
+    ModelDesc md;
+    std::vector<std::vector<double>> fac, rec, sol;
+    std::vector<double> part, top;
+    SegState(const HostModel& h, const Plan& p, std::vector<double> prm, const double* tt, const double* yy,
+             uint32_t fl, int r, int P)
+        : hm(h), plan(p), params(std::move(prm)), t(tt), y(yy), flags(fl), rank(r), nranks(P) {
+        eqc = hm.eqconst;
+        md = hm.desc;
+        md.eqconst = eqc.data();
+        const Geom& g = plan.geo;
+        fac.resize(g.nlev);
+        rec.resize(g.nlev);
+        sol.resize(g.nlev + 1);
+        for (int l = 0; l < g.nlev; ++l) {
+            fac[l].assign(static_cast<size_t>(g.m[l]) * Fac<B>::N * g.K[l], 0.0);
+            rec[l].assign(Rec<B>::N * g.K[l], 0.0);
+        }
+        for (int l = 1; l <= g.nlev; ++l) sol[l].assign(Sol<B>::N * static_cast<size_t>(g.n[l] + g.segL), 0.0);
+        part.assign(static_cast<size_t>(P_GRAD + hm.nt) * g.K[0], 0.0);
+        top.assign(1, 0.0);
+    }
+    const double* halo() const { return params.data() + hm.rec_stride; }
+    void forward(double* record) override {
+        const Geom& g = plan.geo;
+        unsigned long long* st = &g_status;
+        emu_launch(nblocks(g.K[0], 32), 32, [&] {
+            k_fwd0<T>(md, params.data(), t, y, g, fac[0].data(), rec[0].data(), part.data(), st, halo());
+        });
+        for (int l = 1; l < g.nlev; ++l) {
+            RecSource<B> src{rec[l - 1].data(), g.K[l - 1], g.n[l]};
+            emu_launch(nblocks(g.K[l], 32), 32, [&] { k_fwdL<B, RecSource<B>>(src, g, l, fac[l].data(), rec[l].data(), st); });
+        }
+        std::copy(rec[g.nlev - 1].begin(), rec[g.nlev - 1].begin() + Rec<B>::N, record);
+    }
+    void reverse(const double* records, double* partials, double* mean, double* var) override {
+        const Geom& g = plan.geo;
+        unsigned long long* st = &g_status;
+        emu_launch(1, 1, [&] { k_seg_solve<B>(nranks, rank, records, sol[g.nlev].data(), top.data(), st, 0); });
+        const bool gr = flags & 1u, needC = gr || (flags & 4u);
+        for (int l = g.nlev - 1; l >= 1; --l) {
+            RecSource<B> src{rec[l - 1].data(), g.K[l - 1], g.n[l]};
+            SolSink<B> sink{sol[l].data(), g.n[l] + g.segL, g.n[l], g.segL};
+            emu_launch(nblocks(g.K[l], 32), 32, [&] {
+                k_revL<B, RecSource<B>, SolSink<B>>(src, sink, g, l, fac[l].data(), sol[l + 1].data(), needC ? 1 : 0);
+            });
+        }
+        Outs outs{(flags & 2u) ? mean : nullptr, (flags & 4u) ? var : nullptr, (flags & 8u) ? 1 : 0, gr ? 1 : 0,
+                  needC ? 1 : 0};
+        emu_launch(nblocks(g.K[0], 32), 32, [&] {
+            k_rev0<T>(md, params.data(), t, y, g, fac[0].data(), sol[1].data(), part.data(), outs, st, halo());
+        });
+        const int NC = P_GRAD + hm.nt;
+        for (int c = 0; c < NC; ++c) {
+            double acc = 0.0;
+            for (long long k = 0; k < g.K[0]; ++k) acc += part[c * g.K[0] + k];
+            partials[c] = acc;
+        }
+        double ld = partials[P_LOGDET] + top[0];
+        for (int l = 1; l < g.nlev; ++l)
+            for (long long k = 0; k < g.K[l]; ++k) ld += rec[l][Rec<B>::LOGDET * g.K[l] + k];
+        partials[P_LOGDET] = ld;
+    }
+};
+
+std::unique_ptr<SegStateBase> g_seg;
 
 int finish() {
     if (g_status == ~0ULL) return SPINGP_OK;
@@ -268,6 +353,61 @@ int emu_discretize(const spingp_leaf* leaves, int32_t n_leaves, const double* th
         return SPINGP_BAD_ARG;
     }
     return 0;
+}
+
+int emu_seg_forward(const spingp_leaf* leaves, int32_t n_leaves, const double* theta, int32_t n_theta,
+                    const double* t, const double* y, int64_t n_local, double t_left, double t_right, int32_t rank,
+                    int32_t nranks, double sigma, uint32_t flags, int64_t m0, double* record) {
+    g_status = ~0ULL;
+    try {
+        const HostModel hm = build_model(leaves, n_leaves, n_theta);
+        const StaticModel sm = static_model(hm);
+        const int Bsz = (hm.single_matern || sm != SM_NONE) ? hm.b : std::max(3, pad_b(hm.b));
+        Plan plan = make_plan(n_local, 1, Bsz, m0);
+        plan.geo.segL = rank > 0;
+        plan.geo.segR = rank + 1 < nranks;
+        std::vector<double> params(hm.rec_stride + 2, 0.0);
+        fill_record(hm, theta, sigma, params.data());
+        params[hm.rec_stride] = t_left;
+        params[hm.rec_stride + 1] = t_right;
+#define MK(...) g_seg.reset(new SegState<__VA_ARGS__>(hm, plan, params, t, y, flags, rank, nranks))
+        if (sm == SM_EQ6) MK(StaticTraits<SEQ<6>>);
+        else if (sm == SM_M32_QP6) MK(StaticTraits<SMatern<2>, SQP<6>>);
+        else if (hm.single_matern && hm.b == 1) MK(MaternTraits<1>);
+        else if (hm.single_matern && hm.b == 2) MK(MaternTraits<2>);
+        else if (hm.single_matern && hm.b == 3) MK(MaternTraits<3>);
+        else if (Bsz == 3) MK(GenericTraits<3>);
+        else if (Bsz == 4) MK(GenericTraits<4>);
+        else if (Bsz == 6) MK(GenericTraits<6>);
+        else if (Bsz == 8) MK(GenericTraits<8>);
+        else if (Bsz == 12) MK(GenericTraits<12>);
+        else MK(GenericTraits<16>);
+#undef MK
+        g_seg->forward(record);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SPINGP_BAD_ARG;
+    }
+    return finish();
+}
+
+int emu_seg_sizes(const spingp_leaf* leaves, int32_t n_leaves, int32_t n_theta, int32_t* nrec, int32_t* npart) {
+    try {
+        const HostModel hm = build_model(leaves, n_leaves, n_theta);
+        const int B = (hm.single_matern || static_model(hm) != SM_NONE) ? hm.b : std::max(3, pad_b(hm.b));
+        *nrec = 3 * B * B + 2 * B + 1;
+        *npart = 5 + hm.nt;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SPINGP_BAD_ARG;
+    }
+    return 0;
+}
+
+int emu_seg_reverse(const double* records, double* partials, double* mean, double* var) {
+    if (!g_seg) return SPINGP_BAD_ARG;
+    g_seg->reverse(records, partials, mean, var);
+    return finish();
 }
 
 }  // extern "C"

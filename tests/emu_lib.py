@@ -110,3 +110,55 @@ def discretize(leaves, theta, dt, sigma=0.3):
     if st:
         raise EmuError(st, -1, L.emu_last_error().decode())
     return Phi, Q, dPhi, dQ, jit.value
+
+
+def seg_sizes(leaves):
+    """(record, partials) lengths of the segment protocol (same rule as spingp_seg_sizes)."""
+    nrec, npart = ctypes.c_int32(), ctypes.c_int32()
+    lv = _leaves(leaves)
+    nt = sum(4 if (not isinstance(lf, int) and lf[0] == 4) else 2 for lf in leaves)
+    st = lib().emu_seg_sizes(lv.ctypes.data, len(leaves), nt, ctypes.byref(nrec), ctypes.byref(npart))
+    assert st == 0
+    return nrec.value, npart.value
+
+
+def seg_forward(leaves, theta, t, y, t_left, t_right, rank, nranks, sigma, flags=1, m0=0):
+    L = lib()
+    L.emu_seg_forward.argtypes = [ctypes.c_void_p, ctypes.c_int32, _d, ctypes.c_int32, _d, _d, ctypes.c_int64,
+                                  ctypes.c_double, ctypes.c_double, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                                  ctypes.c_uint32, ctypes.c_int64, _d]
+    nrec, _ = seg_sizes(leaves)
+    lv = _leaves(leaves)
+    th = np.ascontiguousarray(theta, dtype=np.float64)
+    global _seg_keep
+    _seg_keep = (np.ascontiguousarray(t, dtype=np.float64), np.ascontiguousarray(y, dtype=np.float64))
+    rec = np.zeros(nrec)
+    st = L.emu_seg_forward(lv.ctypes.data, len(leaves), _p(th), len(th), _p(_seg_keep[0]), _p(_seg_keep[1]),
+                           len(t), float(t_left), float(t_right), rank, nranks, float(sigma), flags, int(m0), _p(rec))
+    if st:
+        raise EmuError(st, -1, L.emu_last_error().decode())
+    return rec
+
+
+def seg_reverse(records, n_local, n_partials, mean=False, var=False):
+    L = lib()
+    L.emu_seg_reverse.argtypes = [_d, _d, _d, _d]
+    records = np.ascontiguousarray(records, dtype=np.float64)
+    part = np.zeros(n_partials)
+    mu = np.zeros(n_local) if mean else None
+    v = np.zeros(n_local) if var else None
+    st = L.emu_seg_reverse(_p(records), _p(part), _p(mu), _p(v))
+    if st:
+        raise EmuError(st, -1, "seg reverse failure")
+    return part, mu, v
+
+
+def seg_finalize(partials, n_theta, n_total, sigma):
+    import math
+    s2 = sigma * sigma
+    ll = -0.5 * (partials[1] + partials[2]) - 0.5 * (partials[0] + partials[3] + n_total * math.log(s2)) \
+        - 0.5 * n_total * math.log(2 * math.pi)
+    g = np.zeros(n_theta + 1)
+    g[:n_theta] = partials[5:5 + n_theta]
+    g[n_theta] = 2 * sigma * (-0.5 * n_total / s2 + partials[4] / (2 * s2 * s2))
+    return ll, g

@@ -241,3 +241,17 @@ def test_device_pointer_api_on_external_stream(ctx):
         assert np.array_equal(mm.cpu().numpy(), h["mean"])
     finally:
         ctx.set_stream(None)
+
+
+@pytest.mark.parametrize("leaves,theta", [([P.MATERN52], [2.0, 1.5]), ([P.MATERN32, P.MATERN12], [1.0, 0.7, 0.5, 2.0]),
+                                          ([P.MATERN32, (P.QP, 6)], [1.0, 10.0, 1.0, 1.0, 1.0, 20.0])])
+@pytest.mark.parametrize("nranks", [1, 2, 3, 8])
+def test_segment_protocol_on_gpu(ctx, leaves, theta, nranks):
+    """The multi-GPU partition's device half (seg_forward / seg_reverse / seg_finalize)
+    with the P ranks run in turn on this GPU and the exchange done in-process."""
+    import torch
+    from paper_1610_08035_b200.partition import emulate_ranks
+    t, y = series(90 + nranks, 3000)
+    ll, g, mean, var = emulate_ranks(ctx, torch, torch.device("cuda", 0), leaves, theta, t, y, 0.3,
+                                     P.WANT_GRAD | P.WANT_MEAN | P.WANT_VAR, nranks)
+    check({"loglik": ll, "grad": g, "mean": mean, "var": var}, leaves, theta, t, y, 0.3, TOL, factor=50.0)
