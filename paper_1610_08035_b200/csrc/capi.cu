@@ -137,7 +137,7 @@ int spingp_seg_sizes(const spingp_leaf* leaves, int32_t n_leaves, int32_t* n_rec
         const int B = plan_bsize(hm);
         if (n_record) *n_record = 3 * B * B + 2 * B + 1;  // Rec<B>::N
         if (n_partials) *n_partials = 5 + nt;             // P_GRAD + nt
-        return SPINGP_OK;
+        return static_cast<int>(SPINGP_OK);
     });
 }
 
