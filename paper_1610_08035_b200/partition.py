@@ -63,7 +63,17 @@ def make_buffers(torch, device, leaves, nranks):
 
 
 def emulate_ranks(ctx, torch, device, leaves, theta, t, y, sigma, flags, nranks):
-    """Run the P-rank protocol sequentially on one GPU (exchange done in-process)."""
+    """Run the P-rank protocol sequentially on one GPU (exchange done in-process).
+    The library is pointed at torch's current stream so the in-process exchange
+    (torch copies) is ordered after the library's kernels."""
+    ctx.set_stream(torch.cuda.current_stream(device).cuda_stream)
+    try:
+        return _emulate(ctx, torch, device, leaves, theta, t, y, sigma, flags, nranks)
+    finally:
+        ctx.set_stream(None)
+
+
+def _emulate(ctx, torch, device, leaves, theta, t, y, sigma, flags, nranks):
     bounds = split(len(t), nranks)
     bufs = [make_buffers(torch, device, leaves, nranks) for _ in range(nranks)]
     dt = [torch.from_numpy(np.ascontiguousarray(t[bounds[r]:bounds[r + 1]])).to(device) for r in range(nranks)]

@@ -49,7 +49,7 @@ def test_two_ranks_gloo_match_single_series_oracle(leaves, theta):
     n = 600
     t = np.cumsum(rng.uniform(0.05, 0.15, n))
     y = np.sin(0.5 * t) + 0.3 * rng.standard_normal(n)
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()  # a forked manager can deadlock on inherited thread pools
     out = mgr.dict()
     mp.spawn(_worker, args=(2, _free_port(), leaves, theta, t, y, 0.3, out), nprocs=2, join=True)
     o = O.evaluate(leaves, theta, t, y, 0.3)
