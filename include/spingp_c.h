@@ -107,8 +107,11 @@ int spingp_state_space(const spingp_leaf* leaves, int32_t n_leaves, const double
 
 int spingp_ctx_create(int32_t device, spingp_ctx** out);
 int spingp_ctx_destroy(spingp_ctx* ctx);
-/* Use an external CUDA stream (cudaStream_t passed as void*); NULL = own stream. */
+/* Use an external CUDA stream (cudaStream_t passed as void*).  As in the CUDA
+ * runtime, NULL is the legacy default stream (torch's default current stream). */
 int spingp_ctx_set_stream(spingp_ctx* ctx, void* stream);
+/* Go back to the context's own private non-blocking stream. */
+int spingp_ctx_use_own_stream(spingp_ctx* ctx);
 void* spingp_ctx_get_stream(spingp_ctx* ctx);
 /* Synchronise the context's stream and return the first device-side failure of
  * the work enqueued since the previous call (and its block index). */

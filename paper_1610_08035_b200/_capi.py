@@ -78,6 +78,7 @@ SIGNATURES = {
     "spingp_ctx_create": (ctypes.c_int, [_i32, _P(_vp)]),
     "spingp_ctx_destroy": (ctypes.c_int, [_vp]),
     "spingp_ctx_set_stream": (ctypes.c_int, [_vp, _vp]),
+    "spingp_ctx_use_own_stream": (ctypes.c_int, [_vp]),
     "spingp_ctx_get_stream": (_vp, [_vp]),
     "spingp_ctx_status": (ctypes.c_int, [_vp, _i64p]),
     "spingp_ctx_launch_count": (_i64, [_vp]),
@@ -211,7 +212,12 @@ class Context:
         return lib().spingp_ctx_get_stream(self._h)
 
     def set_stream(self, stream_ptr):
-        _raise(lib().spingp_ctx_set_stream(self._h, stream_ptr))
+        """Enqueue on an external cudaStream_t (an int handle; 0 = the legacy default
+        stream, e.g. torch's default current stream).  None = the context's own stream."""
+        if stream_ptr is None:
+            _raise(lib().spingp_ctx_use_own_stream(self._h))
+        else:
+            _raise(lib().spingp_ctx_set_stream(self._h, ctypes.c_void_p(int(stream_ptr))))
 
     def set_chunk(self, m0):
         _raise(lib().spingp_ctx_set_chunk(self._h, int(m0)))

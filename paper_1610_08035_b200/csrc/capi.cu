@@ -233,14 +233,21 @@ int spingp_ctx_set_stream(spingp_ctx* ctx, void* stream) {
         std::lock_guard<std::mutex> lk(ctx->mu);
         CUDA_OK(cudaStreamSynchronize(ctx->stream));
         if (ctx->own_stream) CUDA_OK(cudaStreamDestroy(ctx->stream));
-        if (stream) {
-            ctx->stream = static_cast<cudaStream_t>(stream);
-            ctx->own_stream = false;
-        } else {
-            CUDA_OK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-            ctx->own_stream = true;
-        }
+        ctx->stream = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
+        ctx->own_stream = false;
         return SPINGP_OK;
+    });
+}
+
+int spingp_ctx_use_own_stream(spingp_ctx* ctx) {
+    return guarded(nullptr, [&] {
+        checked(ctx);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        if (ctx->own_stream) return static_cast<int>(SPINGP_OK);
+        CUDA_OK(cudaStreamSynchronize(ctx->stream));
+        CUDA_OK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        ctx->own_stream = true;
+        return static_cast<int>(SPINGP_OK);
     });
 }
 

@@ -1017,14 +1017,19 @@ static __global__ void k_reduce_final(FinalArgs a, Geom geo) {
 // then keeps x and the selected-inverse blocks it needs for its reverse sweep:
 //   sol slot 0 (segL only) = (x_{r-1}, C_{r-1,r-1}), Cu slot 0 = C_{r-1,r}; next slot = (x_r, C_rr).
 // recs: P records, each Rec<B>::N contiguous doubles (the K = 1 top-level record).
+// scratch: P x (2 B^2 + B) doubles of global memory for the per-block factor (kept out of
+// per-thread local arrays: large dynamically indexed local arrays were miscompiled by nvcc
+// 12.9 for sm_100a elsewhere in this code).
 template <int B>
 __global__ void k_seg_solve(int P, int rank, const double* __restrict__ recs, double* __restrict__ sol,
-                            double* __restrict__ toplogdet, unsigned long long* status, long long gidx) {
+                            double* __restrict__ toplogdet, unsigned long long* status, long long gidx,
+                            double* __restrict__ scratch) {
     if (blockIdx.x != 0 || threadIdx.x != 0) return;
     constexpr int NR = Rec<B>::N;
-    constexpr int kMaxP = 64;
     double S_L[B * B], T[B * B], rc[B];
-    double Ls[kMaxP][B * B], Zs[kMaxP][B], Xs[kMaxP][B * B];  // factor per block (P <= 64)
+    auto Ls = [&](int r) { return scratch + static_cast<long long>(r) * (2 * B * B + B); };
+    auto Xs = [&](int r) { return scratch + static_cast<long long>(r) * (2 * B * B + B) + B * B; };
+    auto Zs = [&](int r) { return scratch + static_cast<long long>(r) * (2 * B * B + B) + 2 * B * B; };
     mzero<B>(T);
     vzero<B>(rc);
     double ld = 0.0;
@@ -1042,24 +1047,27 @@ __global__ void k_seg_solve(int P, int rank, const double* __restrict__ recs, do
             return;
         }
         ld += ldr;
-        mcopy<B>(Ls[r], S_L);
-        lsolve_v<B>(Zs[r], S_L, rhs);
+        mcopy<B>(Ls(r), S_L);
+        double z[B];
+        lsolve_v<B>(z, S_L, rhs);
+        for (int q = 0; q < B; ++q) Zs(r)[q] = z[q];
         if (r + 1 < P) {
+            double X[B * B];
             for (int q = 0; q < B * B; ++q) U[q] = R1[Rec<B>::LR + q];
-            lsolve<B>(Xs[r], S_L, U);
-            mtm_sym<B>(T, Xs[r], Xs[r]);
-            mtv<B>(rc, Xs[r], Zs[r]);
+            lsolve<B>(X, S_L, U);
+            mcopy<B>(Xs(r), X);
+            mtm_sym<B>(T, X, X);
+            mtv<B>(rc, X, z);
         }
     }
     // back substitution + Takahashi down to block rank-1
     double xn[B], Cnn[B * B], xj[B], Cjn[B * B], Cjj[B * B];
     {
-        ltsolve_v<B>(xn, Ls[P - 1], Zs[P - 1]);
-        double I[B * B], X[B * B];
-        for (int q = 0; q < B * B; ++q) I[q] = (q % (B + 1) == 0) ? 1.0 : 0.0;
-        lsolve<B>(X, Ls[P - 1], I);
-        ltsolve<B>(Cnn, Ls[P - 1], X);
-        msym<B>(Cnn);
+        double Lq[B * B], z[B];
+        mcopy<B>(Lq, Ls(P - 1));
+        for (int q = 0; q < B; ++q) z[q] = Zs(P - 1)[q];
+        ltsolve_v<B>(xn, Lq, z);
+        chol_inv_solve<B>(Cnn, Lq);
     }
     const int lo = rank > 0 ? rank - 1 : rank;
     double xr[B], Crr[B * B], xl[B], Cll[B * B], Clr[B * B];
@@ -1075,7 +1083,11 @@ __global__ void k_seg_solve(int P, int rank, const double* __restrict__ recs, do
         double Y0[B * B], CnL0[B * B], CjL0[B * B];
         mzero<B>(Y0);
         mzero<B>(CnL0);
-        back_step<B>(Ls[j], Y0, Zs[j], Xs[j], false, true, none, xn, Cnn, CnL0, xj, CjL0, Cjn, Cjj);
+        double Lj[B * B], Xj[B * B], zj[B];
+        mcopy<B>(Lj, Ls(j));
+        mcopy<B>(Xj, Xs(j));
+        for (int q = 0; q < B; ++q) zj[q] = Zs(j)[q];
+        back_step<B>(Lj, Y0, zj, Xj, false, true, none, xn, Cnn, CnL0, xj, CjL0, Cjn, Cjj);
         if (j == rank) {
             for (int q = 0; q < B; ++q) xr[q] = xj[q];
             mcopy<B>(Crr, Cjj);

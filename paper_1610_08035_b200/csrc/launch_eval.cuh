@@ -19,6 +19,7 @@ struct EvalBufs {
     double* part;
     double* seg;
     int nseg;
+    double* segscratch;
 };
 
 template <int B>
@@ -33,7 +34,7 @@ EvalBufs carve_eval(spingp_ctx* ctx, const Plan& p, int nt, size_t params_count)
     const size_t SK0 = static_cast<size_t>(g.K[0]) * g.S;
     const int nseg = static_cast<int>((g.K[0] + kSeg - 1) / kSeg);
     tot += arena_bytes(g.S) + arena_bytes((P_GRAD + nt) * SK0) +
-           arena_bytes(static_cast<size_t>(nseg) * g.S * (P_GRAD + nt));
+           arena_bytes(static_cast<size_t>(nseg) * g.S * (P_GRAD + nt)) + arena_bytes(64 * (2 * B * B + B));
     ctx->ensure_ws(tot);
     ctx->ws.reset();
     EvalBufs eb{};
@@ -49,6 +50,7 @@ EvalBufs carve_eval(spingp_ctx* ctx, const Plan& p, int nt, size_t params_count)
     eb.part = ctx->ws.take<double>((P_GRAD + nt) * SK0);
     eb.nseg = nseg;
     eb.seg = ctx->ws.take<double>(static_cast<size_t>(nseg) * g.S * (P_GRAD + nt));
+    eb.segscratch = ctx->ws.take<double>(64 * (2 * B * B + B));
     return eb;
 }
 
@@ -103,7 +105,7 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     if (a.mode == 3) {
         ctx->pre();
         k_seg_solve<B><<<1, 1, 0, ctx->stream>>>(a.nranks, a.rank, a.d_seg_in, eb.sol[g.nlev], eb.toplogdet,
-                                                 ctx->d_status, g.n[0] - 1);
+                                                 ctx->d_status, g.n[0] - 1, eb.segscratch);
         ctx->launched("k_seg_solve");
     } else {
         ctx->pre();

@@ -185,7 +185,8 @@ struct SegState : SegStateBase {
     void reverse(const double* records, double* partials, double* mean, double* var) override {
         const Geom& g = plan.geo;
         unsigned long long* st = &g_status;
-        emu_launch(1, 1, [&] { k_seg_solve<B>(nranks, rank, records, sol[g.nlev].data(), top.data(), st, 0); });
+        std::vector<double> scratch(64 * (2 * B * B + B));
+        emu_launch(1, 1, [&] { k_seg_solve<B>(nranks, rank, records, sol[g.nlev].data(), top.data(), st, 0, scratch.data()); });
         const bool gr = flags & 1u, needC = gr || (flags & 4u);
         for (int l = g.nlev - 1; l >= 1; --l) {
             RecSource<B> src{rec[l - 1].data(), g.K[l - 1], g.n[l]};
