@@ -24,7 +24,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -80,51 +79,76 @@ FP64_PEAK_TFLOPS = 34.1  # DFMA microbenchmark on this pool's B200 (profiles/r01
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons during the timed region (B200_PROFILING.md)."""
+    """SM clocks and clock-event (throttle) reasons sampled through NVML every ~2 ms
+    while the warm-up and timed steps run (B200_PROFILING.md clocks line).  Samples
+    taken inside the timed region are reported when there are any; otherwise the
+    whole loaded window (warm-up + timed) is, and `window` says which."""
 
-    def __init__(self, index):
-        self.index = index
-        self.rows = []
-        self.proc = None
+    REASONS = [("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown")]
+
+    def __init__(self, torch_device):
+        self.dev = torch_device
+        self.rows = []  # (timed?, sm_mhz, max_mhz, reasons bitmask)
+        self.timed = False
+        self._stop = threading.Event()
+        self.nv = None
+
+    def _handle(self):
+        import pynvml as nv
+        import torch
+        nv.nvmlInit()
+        try:
+            uuid = str(torch.cuda.get_device_properties(self.dev).uuid)
+            return nv, nv.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        except Exception:
+            return nv, nv.nvmlDeviceGetHandleByIndex(self.dev.index or 0)
 
     def __enter__(self):
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except OSError:
-            self.proc = None
+            self.nv, self.h = self._handle()
+        except Exception:
+            self.nv = None
+            return self
+        self.thread = threading.Thread(target=self._poll, daemon=True)
+        self.thread.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+    def _poll(self):
+        nv, h = self.nv, self.h
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((self.timed, sm, mx, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if self.nv is not None:
+            self.thread.join(timeout=2)
 
     def summary(self):
-        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if self.nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "window": "nvml unavailable"}
+        rows = [r for r in self.rows if r[0]]
+        window = "timed region"
+        if not rows:
+            rows, window = self.rows, "warm-up + timed region"
         reasons = set()
-        for r in self.rows:
-            if len(r) >= 9:
-                for k, nm in enumerate(names):
-                    if r[5 + k].lower().startswith("active"):
-                        reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        for r in rows:
+            for nm, attr in self.REASONS:
+                if hasattr(self.nv, attr) and r[3] & getattr(self.nv, attr):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(r[1] for r in rows) if rows else None,
+                "sm_max_mhz": max(r[2] for r in rows) if rows else None,
+                "reasons": sorted(reasons), "samples": len(rows), "window": window}
 
 
 def alg_bytes_per_point(kernel, wl):
@@ -275,7 +299,7 @@ def run_ours(args, ws, rank, local):
                             d_ll.data_ptr(), d_g.data_ptr(), d_m.data_ptr() if d_m is not None else 0,
                             d_v.data_ptr() if d_v is not None else 0)
 
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         for _ in range(max(3, args.warmup)):
             flush.zero_()
             step()
@@ -286,12 +310,14 @@ def run_ours(args, ws, rank, local):
         torch.cuda.synchronize(dev)
         launches0 = ctx.launch_count()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        clk.timed = True
         for k in range(args.steps):
             flush.zero_()  # L2 flush between timed steps, outside the events
             evs[k][0].record(stream)
             step()
             evs[k][1].record(stream)
         torch.cuda.synchronize(dev)
+        clk.timed = False
         launches = ctx.launch_count() - launches0
     ctx.status()  # raises on any device-side failure in the timed steps
     step_ms = [a_.elapsed_time(b_) for a_, b_ in evs]

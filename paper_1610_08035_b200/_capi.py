@@ -10,7 +10,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libspingp_b200.so")
+lib_path = os.environ.get("SPINGP_LIB") or os.path.join(_HERE, "libspingp_b200.so")  # override: experiments only
 
 MATERN12, MATERN32, MATERN52, EQ, QP = 0, 1, 2, 3, 4
 LEAF_NPARAMS = {MATERN12: 2, MATERN32: 2, MATERN52: 2, EQ: 2, QP: 4}

@@ -23,6 +23,11 @@ namespace spingp_dev {
 #ifndef SP_UNROLL
 #define SP_UNROLL
 #endif
+// Compiler-level memory barrier (no instruction emitted): the optimiser may not move
+// local-array loads/stores across it (used around the dynamically offset leaf writes).
+#ifndef SP_MEMFENCE
+#define SP_MEMFENCE() asm volatile("" ::: "memory")
+#endif
 
 template <int B>
 SP_DEV void mzero(double* a) {

@@ -465,8 +465,10 @@ struct GenericTraits {
             Q[i] = 0.0;
         }
         for (int i = md.b; i < BB; ++i) Q[i * BB + i] = 1.0;  // padding
+        SP_MEMFENCE();
         for (int l = 0; l < md.nleaves; ++l) {
             const double* lr = rec + md.rec[l];
+            SP_MEMFENCE();
             switch (md.type[l]) {
                 case MATERN12: matern_block<1, BB>(lr, dt, md.off[l], Phi, Q); break;
                 case MATERN32: matern_block<2, BB>(lr, dt, md.off[l], Phi, Q); break;
@@ -475,15 +477,18 @@ struct GenericTraits {
                 case QP: qp_block<BB>(md.off[l], md.order[l], lr, dt, Phi, Q); break;
             }
         }
+        SP_MEMFENCE();
     }
     SP_DEV static void grad(const ModelDesc& md, const double* rec, double dt, const double* Phi,
                             const double* Q, const double* M, const double* Bm, double* g) {
         double hm = 0.0;
         for (int i = 0; i < md.b; ++i) hm += M[i * BB + i];
         hm *= 0.5;
+        SP_MEMFENCE();
         for (int l = 0; l < md.nleaves; ++l) {
             const double* lr = rec + md.rec[l];
             const int t0 = md.th[l];
+            SP_MEMFENCE();
             double gv = 0.0, gl = 0.0;
             switch (md.type[l]) {
                 case MATERN12: matern_grad<1, BB>(lr, dt, md.off[l], Phi, Q, M, Bm, gv, gl); break;
@@ -560,14 +565,20 @@ struct StaticTraits {
     SP_DEV static void step(const ModelDesc& md, const double* rec, double dt, double* Phi, double* Q) {
         mzero<B>(Phi);
         mzero<B>(Q);
+        SP_MEMFENCE();
         L0::template step<0, B>(md, 0, rec + md.rec[0], dt, Phi, Q);
+        SP_MEMFENCE();
         L1::template step<L0::dim, B>(md, 1, rec + md.rec[1], dt, Phi, Q);
+        SP_MEMFENCE();
     }
     SP_DEV static void grad(const ModelDesc& md, const double* rec, double dt, const double* Phi,
                             const double* Q, const double* M, const double* Bm, double* g) {
         double g0[4] = {0.0, 0.0, 0.0, 0.0}, g1[4] = {0.0, 0.0, 0.0, 0.0};
+        SP_MEMFENCE();
         L0::template grad<0, B>(md, 0, rec + md.rec[0], dt, Phi, Q, M, Bm, g0);
+        SP_MEMFENCE();
         L1::template grad<L0::dim, B>(md, 1, rec + md.rec[1], dt, Phi, Q, M, Bm, g1);
+        SP_MEMFENCE();
         const double hm = 0.5 * mtrace<B>(M);
 #pragma unroll
         for (int p = 0; p < L0::np; ++p) g[p] += g0[p] + hm * rec[2 + p];
@@ -582,12 +593,16 @@ struct StaticTraits<L0, void> {
     SP_DEV static void step(const ModelDesc& md, const double* rec, double dt, double* Phi, double* Q) {
         mzero<B>(Phi);
         mzero<B>(Q);
+        SP_MEMFENCE();
         L0::template step<0, B>(md, 0, rec + md.rec[0], dt, Phi, Q);
+        SP_MEMFENCE();
     }
     SP_DEV static void grad(const ModelDesc& md, const double* rec, double dt, const double* Phi,
                             const double* Q, const double* M, const double* Bm, double* g) {
         double g0[4] = {0.0, 0.0, 0.0, 0.0};
+        SP_MEMFENCE();
         L0::template grad<0, B>(md, 0, rec + md.rec[0], dt, Phi, Q, M, Bm, g0);
+        SP_MEMFENCE();
         const double hm = 0.5 * mtrace<B>(M);
 #pragma unroll
         for (int p = 0; p < L0::np; ++p) g[p] += g0[p] + hm * rec[2 + p];

@@ -11,7 +11,7 @@ import subprocess
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LIB_PATH = os.path.join(ROOT, "tests", "emu", "build", "libspingp_emu.so")
+LIB_PATH = os.environ.get("SPINGP_EMU_LIB") or os.path.join(ROOT, "tests", "emu", "build", "libspingp_emu.so")
 _d = ctypes.POINTER(ctypes.c_double)
 _i64p = ctypes.POINTER(ctypes.c_int64)
 _lib = None
@@ -24,7 +24,8 @@ def build():
 def lib():
     global _lib
     if _lib is None:
-        build()
+        if not os.environ.get("SPINGP_EMU_LIB"):  # a sanitizer build passed in explicitly is used as is
+            build()
         L = ctypes.CDLL(LIB_PATH)
         L.emu_last_error.restype = ctypes.c_char_p
         L.emu_eval_batched.argtypes = [ctypes.c_void_p, ctypes.c_int32, _d, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
@@ -117,6 +118,8 @@ def seg_sizes(leaves):
     nrec, npart = ctypes.c_int32(), ctypes.c_int32()
     lv = _leaves(leaves)
     nt = sum(4 if (not isinstance(lf, int) and lf[0] == 4) else 2 for lf in leaves)
+    lib().emu_seg_sizes.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                    ctypes.POINTER(ctypes.c_int32)]
     st = lib().emu_seg_sizes(lv.ctypes.data, len(leaves), nt, ctypes.byref(nrec), ctypes.byref(npart))
     assert st == 0
     return nrec.value, npart.value
