@@ -9,7 +9,8 @@
  * Which reference interface each entry point replaces (file:line under the
  * read-only reference tree):
  *   spingp_state_space        state_space_of            proj/include/spingp/kernels.hpp:326-381
- *   spingp_discretize         discretize(_with_grad)    proj/include/spingp/kernels.hpp:392-443
+ *   (discretize / discretize_with_grad, kernels.hpp:392-443, stay host-side C++ in
+ *    include/spingp/kernels.hpp; on the device they are fused into spingp_eval)
  *   spingp_eval[_device]      log_marginal_likelihood + mll_gradient + predict (training grid)
  *                                                       SPEC.md:280-306 (assemble :262-279)
  *   spingp_eval_batched[...]  the same over many independent series (BASELINE cfg3)
