@@ -63,16 +63,8 @@ void launch_btd(spingp_ctx* ctx, int64_t n, int b, const double* d_diag, const d
             usrc, usink, g, 0, fac[0], sol[1], needC ? 1 : 0);
         ctx->launched("k_rev");
     }
-    if (d_logdet) {
-        LogdetArgs la{};
-        for (int l = 0; l < g.nlev; ++l) la.recs[l] = rec[l];
-        la.logdet_comp = Rec<B>::LOGDET;
-        la.toplogdet = toplogdet;
-        la.out = d_logdet;
-        ctx->pre();
-        k_logdet_btd<<<1, 256, 0, ctx->stream>>>(g, la);
-        ctx->launched("k_logdet_btd");
-    }
+    if (d_logdet)  // toplogdet is the whole log-determinant (cumulative records)
+        CUDA_OK(cudaMemcpyAsync(d_logdet, toplogdet, sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
 }
 
 }  // namespace spingp_host

@@ -217,6 +217,7 @@ int spingp_ctx_destroy(spingp_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->ws.base) cudaFree(ctx->ws.base);
     if (ctx->d_status) cudaFree(ctx->d_status);
+    if (ctx->d_arrive) cudaFree(ctx->d_arrive);
     for (int k = 0; k < 2; ++k) {
         if (ctx->h_stage[k]) cudaFreeHost(ctx->h_stage[k]);
         if (ctx->stage_ev[k]) cudaEventDestroy(ctx->stage_ev[k]);

@@ -104,6 +104,24 @@ struct spingp_ctx {
         CUDA_OK(cudaEventRecord(pending, stream));
     }
 
+    // self-resetting per-series arrival counters of k_reduce (kept out of the arena so
+    // their zero state survives between calls; grown on demand, zeroed when allocated)
+    unsigned int* d_arrive = nullptr;
+    long long arrive_cap = 0;
+    unsigned int* counters(long long S) {
+        if (S > arrive_cap) {
+            if (d_arrive) {
+                CUDA_OK(cudaStreamSynchronize(stream));
+                CUDA_OK(cudaFree(d_arrive));
+            }
+            const long long cap = std::max<long long>(S, 1024);
+            CUDA_OK(cudaMalloc(&d_arrive, cap * sizeof(unsigned int)));
+            CUDA_OK(cudaMemset(d_arrive, 0, cap * sizeof(unsigned int)));
+            arrive_cap = cap;
+        }
+        return d_arrive;
+    }
+
     void ensure_ws(size_t bytes) {
         if (bytes <= ws.size) return;
         if (ws.base) {

@@ -195,6 +195,50 @@ SP_DEV bool chol(double* L, const double* A, double& logdet) {
     return ok;
 }
 
+// Running log-determinant without a log per factorisation: the product of the
+// inverted pivots is kept as mantissa in [0.5, 1) times 2^e (renormalised by
+// exponent-field arithmetic after every group of <= 4 pivots, so it never leaves the
+// normal range); one log at the end of a chunk.
+struct LogDetAcc {
+    double m;
+    int e;
+    SP_DEV void init() {
+        m = 1.0;
+        e = 0;
+    }
+    SP_DEV void mul(double p) {  // p > 0 finite
+        double x = m * p;
+#ifdef SPINGP_HOST_EMU
+        int ex;
+        x = std::frexp(x, &ex);
+        e += ex;
+#else
+        const int hi = __double2hiint(x);
+        e += ((hi >> 20) & 0x7ff) - 1022;
+        x = __hiloint2double((hi & 0x800fffff) | 0x3fe00000, __double2loint(x));
+#endif
+        m = x;
+    }
+    // log det of the factored matrices = -2 log prod(1/l_jj)
+    SP_DEV double logdet() const { return -2.0 * (log(m) + static_cast<double>(e) * 0.69314718055994530942); }
+};
+template <int B>
+SP_DEV void chol_accum(const double* L, LogDetAcc& acc) {
+SP_UNROLL
+    for (int j0 = 0; j0 < B; j0 += 4) {
+        double p = 1.0;
+SP_UNROLL
+        for (int j = j0; j < j0 + 4 && j < B; ++j) p *= L[j * B + j];
+        acc.mul(p);
+    }
+}
+template <int B>
+SP_DEV bool chol(double* L, const double* A, LogDetAcc& acc) {
+    const bool ok = chol_nolog<B>(L, A);
+    if (ok) chol_accum<B>(L, acc);
+    return ok;
+}
+
 // Ainv = (L L^T)^{-1} = L^{-T} L^{-1}, symmetric.
 template <int B>
 SP_DEV void chol_inverse(double* Ainv, const double* L) {

@@ -38,6 +38,9 @@
 
 #include "devmat.cuh"
 #include "model_dev.cuh"
+#ifndef SPINGP_HOST_EMU
+#include <cooperative_groups.h>
+#endif
 
 namespace spingp_dev {
 
@@ -104,7 +107,9 @@ struct ElimState {
     double W[B * B];    // coupling of the current block with the left separator
     double accLL[B * B];
     double accrL[B];
-    double logdet;
+    double logdet;   // log-dets carried in from child records (upper levels)
+    LogDetAcc piv;   // this chunk's own pivots
+    SP_DEV double total_logdet() const { return logdet + piv.logdet(); }
 };
 
 template <int B>
@@ -115,6 +120,7 @@ SP_DEV void elim_init(ElimState<B>& es) {
     mzero<B>(es.accLL);
     vzero<B>(es.accrL);
     es.logdet = 0.0;
+    es.piv.init();
 }
 
 // Eliminate one interior block j with diagonal D, coupling U (to j+1) and rhs.
@@ -129,9 +135,8 @@ SP_DEV bool elim_block(ElimState<B>& es, const double* D, const double* U, const
 SP_UNROLL
     for (int i = 0; i < B * B; ++i) S[i] = D[i] - es.T[i];
     msym<B>(S);  // pivot symmetrisation
-    double L[B * B], ld;
-    if (!chol<B>(L, S, ld)) return false;
-    es.logdet += ld;
+    double L[B * B];
+    if (!chol<B>(L, S, es.piv)) return false;
     double r[B], z[B];
 SP_UNROLL
     for (int i = 0; i < B; ++i) r[i] = rhs[i] - es.rc[i];
@@ -183,12 +188,12 @@ SP_UNROLL
     for (int i = 0; i < B; ++i) r[(Rec<B>::RRHS + i) * SK] = Rrhs[i];
 SP_UNROLL
     for (int i = 0; i < B; ++i) r[(Rec<B>::LRHS + i) * SK] = es.accrL[i];
-    r[Rec<B>::LOGDET * SK] = es.logdet;
+    r[Rec<B>::LOGDET * SK] = es.total_logdet();
 }
 
 // Q̃ = Q + jit I = L_Q L_Q^T  ->  L_Q (and log det Q̃).
 template <int B>
-SP_DEV bool qt_factor(const double* Q, double jit, int breal, double* L, double* ldq) {
+SP_DEV bool qt_factor(const double* Q, double jit, int breal, double* L, LogDetAcc* ldq) {
     double Qt[B * B];
 SP_UNROLL
     for (int i = 0; i < B * B; ++i) Qt[i] = Q[i];
@@ -344,7 +349,7 @@ SP_UNROLL
 SP_UNROLL
     for (int i = 0; i < B; ++i) Rr[i] = T::H(md, i) * yR * is2 - es.rc[i];
     write_rec<B>(rec, SK, g, es, D, Rr, hasL);
-    part[P_LOGDET * SK + g] = es.logdet;
+    part[P_LOGDET * SK + g] = es.total_logdet();
 }
 
 // ============================================= materialised / upper levels ====
@@ -370,6 +375,10 @@ SP_UNROLL
         const long long i1 = static_cast<long long>(s) * n + k + 1;
 SP_UNROLL
         for (int q = 0; q < B * B; ++q) U[q] = rec[(Rec<B>::LR + q) * SKp + i1];
+    }
+    // cumulative log-determinant carried by child record k
+    SP_DEV double child_logdet(int s, long long k) const {
+        return rec[Rec<B>::LOGDET * SKp + static_cast<long long>(s) * n + k];
     }
     // segment mode: what block 0's record contributes to the segment's left separator
     SP_DEV void left_contrib(int s, double* D, double* r) const {
@@ -406,19 +415,20 @@ SP_UNROLL
 SP_UNROLL
             for (int q = 0; q < B; ++q) U[p * B + q] = (p < b && q < b) ? up[(i * b + p) * b + q] : 0.0;
     }
+    SP_DEV double child_logdet(int, long long) const { return 0.0; }
     SP_DEV void left_contrib(int, double* D, double* r) const {
         mzero<B>(D);
         vzero<B>(r);
     }
 };
 
+// One chunk of level `lev` (global chunk index g = series * K + chunk).  The record's
+// LOGDET is cumulative: this chunk's own pivots plus the LOGDET of every child record
+// it absorbs, so the last level carries the whole log-determinant (no level scans).
 template <int B, class Src>
-__global__ void __launch_bounds__(128) k_fwdL(Src src, Geom geo, int lev, double* __restrict__ fac,
-                                              double* __restrict__ rec,
-                                              unsigned long long* status) {
+SP_DEV void fwdL_item(const Src& src, const Geom& geo, int lev, double* __restrict__ fac,
+                      double* __restrict__ rec, unsigned long long* status, long long g) {
     const long long K = geo.K[lev], SK = K * geo.S;
-    const long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (g >= SK) return;
     const int s = static_cast<int>(g / K);
     const long long c = g - s * K;
     const long long n = geo.n[lev];
@@ -459,15 +469,22 @@ SP_UNROLL
     for (int i = 0; i < B * B; ++i) D[i] -= es.T[i];
 SP_UNROLL
     for (int i = 0; i < B; ++i) r[i] -= es.rc[i];
+    for (long long j = st; j < en; ++j) es.logdet += src.child_logdet(s, j);
     write_rec<B>(rec, SK, g, es, D, r, hasL);
 }
+template <int B, class Src>
+__global__ void __launch_bounds__(128) k_fwdL(Src src, Geom geo, int lev, double* __restrict__ fac,
+                                              double* __restrict__ rec, unsigned long long* status) {
+    const long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (g >= geo.K[lev] * geo.S) return;
+    fwdL_item<B, Src>(src, geo, lev, fac, rec, status, g);
+}
 
-// The single block left per series: invert it.
+// The single block left per series: invert it.  toplogdet = log det of the whole
+// precision (this pivot + the cumulative LOGDET of the last record).
 template <int B>
-__global__ void k_top(Geom geo, const double* __restrict__ rec, double* __restrict__ sol,
-                      double* __restrict__ toplogdet, unsigned long long* status) {
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= geo.S) return;
+SP_DEV void top_item(const Geom& geo, const double* __restrict__ rec, double* __restrict__ sol,
+                     double* __restrict__ toplogdet, unsigned long long* status, int s) {
     const int L = geo.nlev;
     const long long SK = geo.S;  // K = 1 at the last level
     double D[B * B], r[B], Lc[B * B], Li[B * B], C[B * B], x[B], z[B], ld;
@@ -489,7 +506,14 @@ SP_UNROLL
     for (int q = 0; q < B; ++q) sol[(Sol<B>::X + q) * Sn + s] = x[q];
 SP_UNROLL
     for (int q = 0; q < B * B; ++q) sol[(Sol<B>::CD + q) * Sn + s] = C[q];
-    toplogdet[s] = ld;
+    toplogdet[s] = ld + rec[Rec<B>::LOGDET * SK + s];
+}
+template <int B>
+__global__ void k_top(Geom geo, const double* __restrict__ rec, double* __restrict__ sol,
+                      double* __restrict__ toplogdet, unsigned long long* status) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= geo.S) return;
+    top_item<B>(geo, rec, sol, toplogdet, status, s);
 }
 
 // Separator data of chunk c from the level above.
@@ -643,12 +667,9 @@ struct UserSink {  // row-major user outputs (b <= B), any may be null
 };
 
 template <int B, class Src, class Sink>
-__global__ void __launch_bounds__(128) k_revL(Src src, Sink sink, Geom geo, int lev,
-                                              const double* __restrict__ fac,
-                                              const double* __restrict__ solU, int needC) {
+SP_DEV void revL_item(const Src& src, const Sink& sink, const Geom& geo, int lev, const double* __restrict__ fac,
+                      const double* __restrict__ solU, int needC, long long g) {
     const long long K = geo.K[lev], SK = K * geo.S;
-    const long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (g >= SK) return;
     const int s = static_cast<int>(g / K);
     const long long c = g - s * K;
     const long long n = geo.n[lev];
@@ -707,6 +728,60 @@ SP_UNROLL
         sink.put_upper(s, st - 1, X);
     }
 }
+template <int B, class Src, class Sink>
+__global__ void __launch_bounds__(128) k_revL(Src src, Sink sink, Geom geo, int lev,
+                                              const double* __restrict__ fac,
+                                              const double* __restrict__ solU, int needC) {
+    const long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (g >= geo.K[lev] * geo.S) return;
+    revL_item<B, Src, Sink>(src, sink, geo, lev, fac, solU, needC, g);
+}
+
+// ================================================ fused upper levels (1 launch) ==
+// All levels >= 1 in one persistent cooperative kernel: forward levels 1..nlev-1,
+// the top inverse, reverse levels nlev-1..1, a grid-wide barrier between phases.
+// The per-level work items are exactly those of k_fwdL / k_top / k_revL; what goes
+// away is 2(nlev-1)+1 launches of latency-bound chains (the upper
+// levels hold ~1/37888 of the points but cost ~35% of the step as separate kernels).
+#ifndef SPINGP_HOST_EMU
+struct UpperArgs {
+    double* rec[kMaxLev];
+    double* fac[kMaxLev];
+    double* sol[kMaxLev + 1];
+    double* toplogdet;
+    unsigned long long* status;
+    int needC, do_fwd, do_top, do_rev;
+};
+template <int B>
+__global__ void __launch_bounds__(128) k_upper(Geom geo, UpperArgs a) {
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    const long long tid = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    const long long nth = static_cast<long long>(gridDim.x) * blockDim.x;
+    if (a.do_fwd) {
+        for (int l = 1; l < geo.nlev; ++l) {
+            const RecSource<B> src{a.rec[l - 1], geo.K[l - 1] * geo.S, geo.n[l]};
+            const long long SK = geo.K[l] * geo.S;
+            for (long long g = tid; g < SK; g += nth) fwdL_item<B, RecSource<B>>(src, geo, l, a.fac[l], a.rec[l], a.status, g);
+            grid.sync();
+        }
+    }
+    if (a.do_top) {
+        for (long long s = tid; s < geo.S; s += nth)
+            top_item<B>(geo, a.rec[geo.nlev - 1], a.sol[geo.nlev], a.toplogdet, a.status, static_cast<int>(s));
+        grid.sync();
+    }
+    if (a.do_rev) {
+        for (int l = geo.nlev - 1; l >= 1; --l) {
+            const RecSource<B> src{a.rec[l - 1], geo.K[l - 1] * geo.S, geo.n[l]};
+            const SolSink<B> sink{a.sol[l], (geo.n[l] + geo.segL) * geo.S, geo.n[l], geo.segL};
+            const long long SK = geo.K[l] * geo.S;
+            for (long long g = tid; g < SK; g += nth)
+                revL_item<B, RecSource<B>, SolSink<B>>(src, sink, geo, l, a.fac[l], a.sol[l + 1], a.needC, g);
+            if (l > 1) grid.sync();
+        }
+    }
+}
+#endif
 
 // ============================================ level-0 reverse (fused outputs) ==
 
@@ -866,16 +941,18 @@ SP_UNROLL
 SP_UNROLL
         for (int j = 0; j < B; ++j) CnL[i * B + j] = sd.CLR[j * B + i];
 
-    double fy = 0.0, fe = 0.0, ldq = 0.0, noise = 0.0;
+    double fy = 0.0, fe = 0.0, noise = 0.0;
+    LogDetAcc ldq;  // log det of every Q̃ of the chunk
+    ldq.init();
     double gr[kMaxTheta];
     for (int p = 0; p < md.nt; ++p) gr[p] = 0.0;
 
     for (long long j = en - 2; j >= st; --j) {
         const long long nb = j + 1;
         const double dt = ts[nb] - ts[j];
-        double Phn[B * B], Qn[B * B], Mqn[B * B], ldqn;
+        double Phn[B * B], Qn[B * B], Mqn[B * B];
         T::step(md, rp, dt, Phn, Qn);
-        qt_factor<B>(Qn, jit, md.b, Mqn, &ldqn);
+        qt_factor<B>(Qn, jit, md.b, Mqn, &ldq);
         double Li[B * B], Y[B * B], z[B], U[B * B], X[B * B], PQP[B * B];
         load_fac<B>(fac + (j - st) * Fac<B>::N * SK + g, SK, hasL, Li, Y, z);
         step_assembly<B>(Phn, Mqn, PQP, U);
@@ -883,7 +960,6 @@ SP_UNROLL
         double xj[B], CjL[B * B], Cjn[B * B], Cjj[B * B];
         back_step<B>(Li, Y, z, X, hasL, needC, sd, xn, Cnn, CnL, xj, CjL, Cjn, Cjj);
         point_out<T>(md, outs, gbase + nb, ys[nb], is2, sig, xn, Cnn, fy, noise, status);
-        ldq += ldqn;
         step_terms<T>(md, rp, dt, Phn, Qn, Mqn, xn, Cnn, xj, Cjj, Cjn, false, grad, fe, gr);
 SP_UNROLL
         for (int q = 0; q < B; ++q) xn[q] = xj[q];
@@ -897,10 +973,9 @@ SP_UNROLL
     {
         const bool anchor = st == 0 && !geo.segL;
         const double dt = anchor ? -1.0 : ts[st] - (st > 0 ? ts[st - 1] : halo[2 * s]);
-        double Ph[B * B], Qr[B * B], Mq[B * B], ldq0;
+        double Ph[B * B], Qr[B * B], Mq[B * B];
         T::step(md, rp, dt, Ph, Qr);
-        qt_factor<B>(Qr, jit, md.b, Mq, &ldq0);
-        ldq += ldq0;
+        qt_factor<B>(Qr, jit, md.b, Mq, &ldq);
         double CLs[B * B];  // C_{L, st} = C_{st, L}^T
 SP_UNROLL
         for (int i = 0; i < B; ++i)
@@ -910,105 +985,99 @@ SP_UNROLL
     }
     part[P_FITY * SK + g] = fy;
     part[P_FITE * SK + g] = fe;
-    part[P_LDQ * SK + g] = ldq;
+    part[P_LDQ * SK + g] = ldq.logdet();
     part[P_NOISE * SK + g] = noise;
     for (int p = 0; p < md.nt; ++p) part[(P_GRAD + p) * SK + g] = gr[p];
 }
 
 // ================================================================ reductions ==
 
-// Stage 1: per series, per segment of kSeg chunks, fixed-order sums of the
-// level-0 partial components.  out[(s * nseg + seg) * NC + comp]
+// One launch, two fixed-order stages (bit-reproducible):
+//   stage 1  block (seg, s) sums chunks [seg*kSeg, (seg+1)*kSeg) of series s for every
+//            partial component: warp w takes components w, w+8, ...; lane l sums
+//            chunks l, l+32, ... in order, then a fixed shuffle tree -> seg[s][seg][comp];
+//   stage 2  the last block of series s to arrive (per-series counter, self-resetting)
+//            sums seg[s][0..nseg) the same way and writes loglik / gradient (or, in
+//            segment mode, the raw partial sums).
+// The log-determinant of the whole precision is toplogdet[s] (cumulative records).
 constexpr int kSeg = 1024;
-static __global__ void k_reduce_seg(const double* __restrict__ part, long long K, int S, int NC,
-                             double* __restrict__ out) {
-    __shared__ double sh[kSeg / 4];
-    const int s = blockIdx.y, seg = blockIdx.x;
-    const int nseg = gridDim.x;
-    const long long SK = K * S;
-    const long long base = static_cast<long long>(s) * K + static_cast<long long>(seg) * kSeg;
-    const long long lim = min(static_cast<long long>(kSeg), K - static_cast<long long>(seg) * kSeg);
-    for (int comp = 0; comp < NC; ++comp) {
-        double v = 0.0;
-        // thread t sums elements t, t+256, t+512, t+768 in order
-        for (int k = threadIdx.x; k < lim; k += blockDim.x) v += part[comp * SK + base + k];
-        sh[threadIdx.x] = v;
-        __syncthreads();
-        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-            if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) out[(static_cast<long long>(s) * nseg + seg) * NC + comp] = sh[0];
-        __syncthreads();
-    }
-}
+constexpr int kRedThreads = 256;
+constexpr int kMaxNC = P_GRAD + kMaxTheta;
 
 struct FinalArgs {
-    const double* seg;     // [S][nseg][NC]
-    int nseg, NC;
-    const double* recs[kMaxLev];  // records of every level (logdet component)
-    int logdet_comp;       // Rec<B>::LOGDET
+    const double* part;    // [NC][S*K] level-0 per-chunk partial sums
+    long long K;           // chunks per series
+    int NC;
+    double* seg;           // [S][nseg][NC] scratch
+    unsigned int* arrive;  // [S] zero-initialised counters
     const double* toplogdet;
     const double* params;
     int rec_stride, nt;
     long long n;
     double* loglik;        // [S]
     double* grad;          // [S][nt+1] or null
-    double* partials;      // segment mode: raw sums (logdetP total, fit_y, fit_e, logdetQ, noise, grad...)
+    double* partials;      // segment mode: raw sums (logdetP, fit_y, fit_e, logdetQ, noise, grad...)
 };
 
-// Stage 2: one CTA per series.  Deterministic fixed-order tree sums.
-static __global__ void k_reduce_final(FinalArgs a, Geom geo) {
-    __shared__ double sh[256];
-    __shared__ double acc[8 + kMaxTheta];
-    const int s = blockIdx.x;
-    // level-0 partial components from the segments
-    for (int comp = 0; comp < a.NC; ++comp) {
+SP_DEV double warp_sum(double v) {
+#ifndef SPINGP_HOST_EMU
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+#endif
+    return v;
+}
+
+#ifndef SPINGP_HOST_EMU
+static __global__ void __launch_bounds__(kRedThreads) k_reduce(FinalArgs a) {
+    __shared__ double acc[kMaxNC];
+    __shared__ int last;
+    const int s = blockIdx.y, sg = blockIdx.x, nseg = gridDim.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long SK = a.K * gridDim.y;
+    const long long base = static_cast<long long>(s) * a.K + static_cast<long long>(sg) * kSeg;
+    const int lim = static_cast<int>(min(static_cast<long long>(kSeg), a.K - static_cast<long long>(sg) * kSeg));
+    for (int c = warp; c < a.NC; c += kRedThreads / 32) {
+        const double* p = a.part + c * SK + base;
         double v = 0.0;
-        for (int k = threadIdx.x; k < a.nseg; k += blockDim.x)
-            v += a.seg[(static_cast<long long>(s) * a.nseg + k) * a.NC + comp];
-        sh[threadIdx.x] = v;
-        __syncthreads();
-        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-            if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) acc[comp] = sh[0];
-        __syncthreads();
+#pragma unroll 8
+        for (int k = lane; k < lim; k += 32) v += p[k];
+        v = warp_sum(v);
+        if (lane == 0) a.seg[(static_cast<long long>(s) * nseg + sg) * a.NC + c] = v;
     }
-    // logdets of the upper levels
-    double v = 0.0;
-    for (int l = 1; l < geo.nlev; ++l) {
-        const long long K = geo.K[l], SK = K * geo.S;
-        for (long long k = threadIdx.x; k < K; k += blockDim.x)
-            v += a.recs[l][a.logdet_comp * SK + static_cast<long long>(s) * K + k];
-    }
-    sh[threadIdx.x] = v;
+    __threadfence();
     __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-        __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&a.arrive[s], 1u) == static_cast<unsigned>(nseg - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int c = warp; c < a.NC; c += kRedThreads / 32) {
+        double v = 0.0;
+#pragma unroll 8
+        for (int k = lane; k < nseg; k += 32) v += __ldcg(a.seg + (static_cast<long long>(s) * nseg + k) * a.NC + c);
+        v = warp_sum(v);
+        if (lane == 0) acc[c] = v;
     }
-    if (threadIdx.x == 0 && a.partials) {
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    a.arrive[s] = 0u;  // ready for the next launch (stream-ordered)
+    const double ldP = a.toplogdet[s];
+    if (a.partials) {
         for (int c = 0; c < a.NC; ++c) a.partials[c] = acc[c];
-        a.partials[P_LOGDET] = acc[P_LOGDET] + sh[0] + a.toplogdet[s];
+        a.partials[P_LOGDET] = ldP;
         return;
     }
-    if (threadIdx.x == 0) {
-        const double ldP = acc[P_LOGDET] + sh[0] + a.toplogdet[s];
-        const double* rp = a.params + static_cast<long long>(s) * a.rec_stride;
-        const double sig = rp[0], s2 = sig * sig;
-        const double nn = static_cast<double>(a.n);
-        const double kLog2Pi = 1.8378770664093454835606594728112;
-        a.loglik[s] = -0.5 * (acc[P_FITY] + acc[P_FITE]) -
-                      0.5 * (ldP + acc[P_LDQ] + nn * log(s2)) - 0.5 * nn * kLog2Pi;
-        if (a.grad) {
-            double* gs = a.grad + static_cast<long long>(s) * (a.nt + 1);
-            for (int p = 0; p < a.nt; ++p) gs[p] = acc[P_GRAD + p];
-            gs[a.nt] = 2.0 * sig * (-0.5 * nn / s2 + acc[P_NOISE] / (2.0 * s2 * s2));
-        }
+    const double* rp = a.params + static_cast<long long>(s) * a.rec_stride;
+    const double sig = rp[0], s2 = sig * sig;
+    const double nn = static_cast<double>(a.n);
+    const double kLog2Pi = 1.8378770664093454835606594728112;
+    a.loglik[s] = -0.5 * (acc[P_FITY] + acc[P_FITE]) - 0.5 * (ldP + acc[P_LDQ] + nn * log(s2)) - 0.5 * nn * kLog2Pi;
+    if (a.grad) {
+        double* gs = a.grad + static_cast<long long>(s) * (a.nt + 1);
+        for (int p = 0; p < a.nt; ++p) gs[p] = acc[P_GRAD + p];
+        gs[a.nt] = 2.0 * sig * (-0.5 * nn / s2 + acc[P_NOISE] / (2.0 * s2 * s2));
     }
 }
+#endif
 
 // ===================================================== multi-GPU reduced system ==
 // Segment mode: rank r has reduced its time segment to a 2-separator record
@@ -1109,7 +1178,8 @@ __global__ void k_seg_solve(int P, int rank, const double* __restrict__ recs, do
     }
     for (int q = 0; q < B; ++q) sol[(Sol<B>::X + q) * Sn + segL] = xr[q];
     for (int q = 0; q < B * B; ++q) sol[(Sol<B>::CD + q) * Sn + segL] = Crr[q];
-    toplogdet[0] = rank == 0 ? ld : 0.0;
+    // this rank's segment log-det (cumulative record) + the reduced system's (rank 0 only)
+    toplogdet[0] = (rank == 0 ? ld : 0.0) + recs[static_cast<long long>(rank) * NR + Rec<B>::LOGDET];
 }
 
 // After the all-reduce of the ranks' partial sums: loglik and gradient.
@@ -1131,29 +1201,6 @@ static __global__ void k_seg_final(SegFinalArgs a) {
         for (int p = 0; p < a.nt; ++p) a.grad[p] = a.sums[P_GRAD + p];
         a.grad[a.nt] = 2.0 * a.sigma * (-0.5 * nn / s2 + a.sums[P_NOISE] / (2.0 * s2 * s2));
     }
-}
-
-// logdet for the standalone BTD operators: sum of all level records + top.
-struct LogdetArgs {
-    const double* recs[kMaxLev];
-    int logdet_comp;
-    const double* toplogdet;
-    double* out;
-};
-static __global__ void k_logdet_btd(Geom geo, LogdetArgs a) {
-    __shared__ double sh[256];
-    double v = 0.0;
-    for (int l = 0; l < geo.nlev; ++l) {
-        const long long K = geo.K[l];
-        for (long long k = threadIdx.x; k < K; k += blockDim.x) v += a.recs[l][a.logdet_comp * K + k];
-    }
-    sh[threadIdx.x] = v;
-    __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *a.out = sh[0] + a.toplogdet[0];
 }
 
 // y = M v for a user SymBTD (one thread per block row).

@@ -4,6 +4,10 @@
 // deterministic two-stage reduction.  Included by the inst_*.cu files only.
 #pragma once
 
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
 #include "ctx.hpp"
 
 namespace spingp_host {
@@ -20,6 +24,7 @@ struct EvalBufs {
     double* seg;
     int nseg;
     double* segscratch;
+    unsigned int* arrive;  // per-series counters of k_reduce (zeroed at workspace creation)
 };
 
 template <int B>
@@ -51,7 +56,40 @@ EvalBufs carve_eval(spingp_ctx* ctx, const Plan& p, int nt, size_t params_count)
     eb.nseg = nseg;
     eb.seg = ctx->ws.take<double>(static_cast<size_t>(nseg) * g.S * (P_GRAD + nt));
     eb.segscratch = ctx->ws.take<double>(64 * (2 * B * B + B));
+    eb.arrive = ctx->counters(g.S);
     return eb;
+}
+
+// Levels >= 1 as one cooperative launch (default) or as per-level kernels
+// (SPINGP_UPPER=levels: A/B comparison knob).
+inline bool upper_fused() {
+    static const bool f = [] {
+        const char* e = std::getenv("SPINGP_UPPER");
+        return !(e && std::strcmp(e, "levels") == 0);
+    }();
+    return f;
+}
+
+template <int B>
+void launch_upper(spingp_ctx* ctx, const Geom& g, UpperArgs& ua) {
+    constexpr int tpb = 128;
+    static int resident = 0;  // co-resident CTAs of k_upper<B> on this device type
+    if (!resident) {
+        int per = 0, dev = 0, sms = 0;
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_upper<B>, tpb, 0));
+        CUDA_OK(cudaGetDevice(&dev));
+        CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        resident = std::max(1, per) * sms;
+    }
+    long long work = g.S;
+    for (int l = 1; l < g.nlev; ++l) work = std::max(work, g.K[l] * g.S);
+    const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>(resident, (work + tpb - 1) / tpb)));
+    Geom geo = g;
+    void* args[] = {&geo, &ua};
+    ctx->pre();
+    CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_upper<B>), dim3(grid), dim3(tpb), args, 0,
+                                        ctx->stream));
+    ctx->launched("k_upper");
 }
 
 template <class T>
@@ -84,18 +122,21 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     const long long SK0 = g.K[0] * g.S;
     const bool grad = a.flags & SPINGP_WANT_GRAD;
     const bool needC = grad || (a.flags & SPINGP_WANT_VAR);
+    const bool fused = upper_fused();
     if (a.mode != 3) {
-    ctx->pre();
-    k_fwd0<T><<<blocks_for(SK0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
-                                                             eb.rec[0], eb.part, ctx->d_status, halo);
-    ctx->launched("k_fwd0");
-    for (int l = 1; l < g.nlev; ++l) {
-        RecSource<B> src{eb.rec[l - 1], g.K[l - 1] * g.S, g.n[l]};
         ctx->pre();
-        k_fwdL<B, RecSource<B>><<<blocks_for(g.K[l] * g.S, tpb), tpb, 0, ctx->stream>>>(
-            src, g, l, eb.fac[l], eb.rec[l], ctx->d_status);
-        ctx->launched("k_fwd");
-    }
+        k_fwd0<T><<<blocks_for(SK0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
+                                                                 eb.rec[0], eb.part, ctx->d_status, halo);
+        ctx->launched("k_fwd0");
+        if (!fused || a.mode == 2) {
+            for (int l = 1; l < g.nlev; ++l) {
+                RecSource<B> src{eb.rec[l - 1], g.K[l - 1] * g.S, g.n[l]};
+                ctx->pre();
+                k_fwdL<B, RecSource<B>><<<blocks_for(g.K[l] * g.S, tpb), tpb, 0, ctx->stream>>>(
+                    src, g, l, eb.fac[l], eb.rec[l], ctx->d_status);
+                ctx->launched("k_fwd");
+            }
+        }
     }
     if (a.mode == 2) {  // segment forward: hand this rank's top-level record to the caller
         CUDA_OK(cudaMemcpyAsync(a.d_seg_out, eb.rec[g.nlev - 1], Rec<B>::N * sizeof(double),
@@ -107,19 +148,36 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
         k_seg_solve<B><<<1, 1, 0, ctx->stream>>>(a.nranks, a.rank, a.d_seg_in, eb.sol[g.nlev], eb.toplogdet,
                                                  ctx->d_status, g.n[0] - 1, eb.segscratch);
         ctx->launched("k_seg_solve");
-    } else {
-        ctx->pre();
-        k_top<B><<<blocks_for(g.S, 128), 128, 0, ctx->stream>>>(g, eb.rec[g.nlev - 1], eb.sol[g.nlev],
-                                                               eb.toplogdet, ctx->d_status);
-        ctx->launched("k_top");
     }
-    for (int l = g.nlev - 1; l >= 1; --l) {
-        RecSource<B> src{eb.rec[l - 1], g.K[l - 1] * g.S, g.n[l]};
-        SolSink<B> sink{eb.sol[l], (g.n[l] + g.segL) * g.S, g.n[l], g.segL};
-        ctx->pre();
-        k_revL<B, RecSource<B>, SolSink<B>><<<blocks_for(g.K[l] * g.S, tpb), tpb, 0, ctx->stream>>>(
-            src, sink, g, l, eb.fac[l], eb.sol[l + 1], needC ? 1 : 0);
-        ctx->launched("k_rev");
+    if (fused && (a.mode == 0 || g.nlev > 1)) {
+        UpperArgs ua{};
+        for (int l = 0; l < g.nlev; ++l) {
+            ua.rec[l] = eb.rec[l];
+            ua.fac[l] = eb.fac[l];
+        }
+        for (int l = 1; l <= g.nlev; ++l) ua.sol[l] = eb.sol[l];
+        ua.toplogdet = eb.toplogdet;
+        ua.status = ctx->d_status;
+        ua.needC = needC ? 1 : 0;
+        ua.do_fwd = a.mode == 0;
+        ua.do_top = a.mode == 0;
+        ua.do_rev = 1;
+        launch_upper<B>(ctx, g, ua);
+    } else {
+        if (a.mode != 3) {
+            ctx->pre();
+            k_top<B><<<blocks_for(g.S, 128), 128, 0, ctx->stream>>>(g, eb.rec[g.nlev - 1], eb.sol[g.nlev],
+                                                                   eb.toplogdet, ctx->d_status);
+            ctx->launched("k_top");
+        }
+        for (int l = g.nlev - 1; l >= 1; --l) {
+            RecSource<B> src{eb.rec[l - 1], g.K[l - 1] * g.S, g.n[l]};
+            SolSink<B> sink{eb.sol[l], (g.n[l] + g.segL) * g.S, g.n[l], g.segL};
+            ctx->pre();
+            k_revL<B, RecSource<B>, SolSink<B>><<<blocks_for(g.K[l] * g.S, tpb), tpb, 0, ctx->stream>>>(
+                src, sink, g, l, eb.fac[l], eb.sol[l + 1], needC ? 1 : 0);
+            ctx->launched("k_rev");
+        }
     }
     Outs outs{(a.flags & SPINGP_WANT_MEAN) ? a.d_mean : nullptr, (a.flags & SPINGP_WANT_VAR) ? a.d_var : nullptr,
               (a.flags & SPINGP_INCLUDE_NOISE) ? 1 : 0, grad ? 1 : 0, needC ? 1 : 0};
@@ -127,16 +185,12 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     k_rev0<T><<<blocks_for(SK0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
                                                              eb.sol[1], eb.part, outs, ctx->d_status, halo);
     ctx->launched("k_rev0");
-    const int NC = P_GRAD + nt;
-    ctx->pre();
-    k_reduce_seg<<<dim3(eb.nseg, g.S), 256, 0, ctx->stream>>>(eb.part, g.K[0], g.S, NC, eb.seg);
-    ctx->launched("k_reduce_seg");
     FinalArgs fa{};
+    fa.part = eb.part;
+    fa.K = g.K[0];
+    fa.NC = P_GRAD + nt;
     fa.seg = eb.seg;
-    fa.nseg = eb.nseg;
-    fa.NC = NC;
-    for (int l = 0; l < g.nlev; ++l) fa.recs[l] = eb.rec[l];
-    fa.logdet_comp = Rec<B>::LOGDET;
+    fa.arrive = eb.arrive;
     fa.toplogdet = eb.toplogdet;
     fa.params = eb.params;
     fa.rec_stride = hm.rec_stride;
@@ -146,8 +200,8 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     fa.grad = grad ? a.d_grad : nullptr;
     fa.partials = a.mode == 3 ? a.d_seg_out : nullptr;
     ctx->pre();
-    k_reduce_final<<<g.S, 256, 0, ctx->stream>>>(fa, g);
-    ctx->launched("k_reduce_final");
+    k_reduce<<<dim3(eb.nseg, g.S), kRedThreads, 0, ctx->stream>>>(fa);
+    ctx->launched("k_reduce");
 }
 
 }  // namespace spingp_host

@@ -37,20 +37,52 @@ namespace spingp_dev {
 // form Q(Δt) = ∫_0^Δt e^{Fs} L q L^T e^{F^T s} ds in closed form, entry by entry,
 // with no cancellation; its θ-derivatives follow from the same form.
 
+// 1/j for the runtime-length tail series (constant memory: warp-uniform index).
+#ifdef SPINGP_HOST_EMU
+static const double kRecip[96] = {
+#else
+static __constant__ double kRecip[96] = {
+#endif
+    0.0, 1.0 / 1, 1.0 / 2, 1.0 / 3, 1.0 / 4, 1.0 / 5, 1.0 / 6, 1.0 / 7, 1.0 / 8, 1.0 / 9, 1.0 / 10, 1.0 / 11,
+    1.0 / 12, 1.0 / 13, 1.0 / 14, 1.0 / 15, 1.0 / 16, 1.0 / 17, 1.0 / 18, 1.0 / 19, 1.0 / 20, 1.0 / 21, 1.0 / 22,
+    1.0 / 23, 1.0 / 24, 1.0 / 25, 1.0 / 26, 1.0 / 27, 1.0 / 28, 1.0 / 29, 1.0 / 30, 1.0 / 31, 1.0 / 32, 1.0 / 33,
+    1.0 / 34, 1.0 / 35, 1.0 / 36, 1.0 / 37, 1.0 / 38, 1.0 / 39, 1.0 / 40, 1.0 / 41, 1.0 / 42, 1.0 / 43, 1.0 / 44,
+    1.0 / 45, 1.0 / 46, 1.0 / 47, 1.0 / 48, 1.0 / 49, 1.0 / 50, 1.0 / 51, 1.0 / 52, 1.0 / 53, 1.0 / 54, 1.0 / 55,
+    1.0 / 56, 1.0 / 57, 1.0 / 58, 1.0 / 59, 1.0 / 60, 1.0 / 61, 1.0 / 62, 1.0 / 63, 1.0 / 64, 1.0 / 65, 1.0 / 66,
+    1.0 / 67, 1.0 / 68, 1.0 / 69, 1.0 / 70, 1.0 / 71, 1.0 / 72, 1.0 / 73, 1.0 / 74, 1.0 / 75, 1.0 / 76, 1.0 / 77,
+    1.0 / 78, 1.0 / 79, 1.0 / 80, 1.0 / 81, 1.0 / 82, 1.0 / 83, 1.0 / 84, 1.0 / 85, 1.0 / 86, 1.0 / 87, 1.0 / 88,
+    1.0 / 89, 1.0 / 90, 1.0 / 91, 1.0 / 92, 1.0 / 93, 1.0 / 94, 1.0 / 95};
+
 // R_m(x) = e^{-x} Σ_{j>m} x^j / j!  (= 1 - e^{-x} Σ_{j<=m} x^j/j!), m = 0..M, x >= 0.
+// No divisions: reciprocals are compile-time constants (unrolled tiers) or a table.
+// x < 0.25: 14 tail terms by Horner; x < 6: terms until they stop contributing;
+// else the direct form (no cancellation there).
+template <int K, int M>
+SP_DEV double tail_horner(double x) {  // Σ_{k<K} x^k (M+1)!/(M+1+k)!  (nested, smallest term first)
+    double h = 1.0;
+#pragma unroll
+    for (int k = K - 2; k >= 0; --k) h = fma(h, x * (1.0 / double(M + 2 + k)), 1.0);
+    return h;
+}
 template <int M>
-SP_DEV void exp_tails(double x, double* R) {
-    const double ex = exp(-x);
+SP_DEV void exp_tails(double x, double ex, double* R) {  // ex = e^{-x}
     double pw[M + 1];  // x^m / m!
     pw[0] = 1.0;
 #pragma unroll
-    for (int m = 1; m <= M; ++m) pw[m] = pw[m - 1] * x / double(m);
+    for (int m = 1; m <= M; ++m) pw[m] = pw[m - 1] * (x * (1.0 / double(m)));
     if (x < 6.0) {
-        double term = pw[M] * x / double(M + 1), s = 0.0;
-        for (int k = 0; k < 64; ++k) {  // terms decrease monotonically once j > x
-            s += term;
-            term *= x / double(M + 2 + k);
-            if (term <= 1e-17 * s) break;
+        const double t0 = pw[M] * (x * (1.0 / double(M + 1)));
+        double s;
+        if (x < 0.25) {
+            s = t0 * tail_horner<14, M>(x);  // remainder < 0.25^14/14! relative
+        } else {
+            double term = t0;
+            s = 0.0;
+            for (int k = 0; k < 90 - M; ++k) {  // terms decrease monotonically once j > x
+                s += term;
+                term *= x * kRecip[M + 2 + k];
+                if (term <= 1e-17 * s) break;
+            }
         }
         R[M] = ex * s;
 #pragma unroll
@@ -105,7 +137,7 @@ SP_DEV void matern_block(const double* lr, double dt, int o, double* Phi, double
     } else if constexpr (D == 2) {
         P[0] = var; P[1] = 0.0; P[2] = 0.0; P[3] = var * lam * lam;
     } else {
-        const double kap = lam * lam / 3.0;
+        const double kap = lam * lam * (1.0 / 3.0);
         P[0] = var; P[1] = 0.0; P[2] = -var * kap;
         P[3] = 0.0; P[4] = var * kap; P[5] = 0.0;
         P[6] = -var * kap; P[7] = 0.0; P[8] = var * lam * lam * lam * lam;
@@ -142,7 +174,7 @@ SP_DEV void matern_block(const double* lr, double dt, int o, double* Phi, double
     constexpr int M = 2 * (D - 1);
     double R[M + 1];
     const double u = lam * dt;
-    exp_tails<M>(2.0 * u, R);
+    exp_tails<M>(2.0 * u, e * e, R);  // e^{-2λΔt} = (e^{-λΔt})²
     double I[M + 1];
     {
         double f = 0.5;  // m! / 2^{m+1}
@@ -193,14 +225,15 @@ SP_DEV void matern_grad(const double* lr, double dt, int o, const double* Phi, c
             Qb[i * D + j] = Q[(o + i) * LD + o + j];
         }
     // d/dvar: dΦ = 0, dQ = Q / var (also at the anchor, where Q = Pinf)
-    gvar += 0.5 * mtrprod<D>(Mb, Qb) / var;
+    const double ilen = 1.0 / len;  // the step's only divisions: 1/ℓ and 1/var
+    gvar += 0.5 * mtrprod<D>(Mb, Qb) * (1.0 / var);
     // d/dℓ = -(λ/ℓ) d/dλ.  dQ/dλ_ij = ((i+j)/λ) Q_ij + var Δt q1 (T v)_i (T v)_j
     double dQ[D * D];
-    const double c = -lam / len;
+    const double c = -lam * ilen;
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll
-        for (int j = 0; j < D; ++j) dQ[i * D + j] = c * double(i + j) / lam * Qb[i * D + j];
+        for (int j = 0; j < D; ++j) dQ[i * D + j] = -double(i + j) * ilen * Qb[i * D + j];
     if (dt < 0.0) {  // anchor: dPinf/dℓ_ij = -(i+j)/ℓ Pinf_ij
         glen += 0.5 * mtrprod<D>(Mb, dQ);
         return;
@@ -242,7 +275,7 @@ SP_DEV void matern_grad(const double* lr, double dt, int o, const double* Phi, c
     }
     double FP[D * D], dph[D * D];
     mm<D>(FP, F, ph);
-    const double c1 = -1.0 / len, c2 = -dt / len;
+    const double c1 = -ilen, c2 = -dt * ilen;
 #pragma unroll
     for (int i = 0; i < D; ++i)
 #pragma unroll

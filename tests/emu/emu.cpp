@@ -72,9 +72,7 @@ void emu_eval(const HostModel& hm, const Plan& plan, std::vector<double>& params
         double acc[P_GRAD + kMaxTheta] = {};
         for (int c = 0; c < P_GRAD + nt; ++c)
             for (long long k = 0; k < g.K[0]; ++k) acc[c] += part[c * SK0 + s * g.K[0] + k];
-        double ld = acc[P_LOGDET] + top[s];
-        for (int l = 1; l < g.nlev; ++l)
-            for (long long k = 0; k < g.K[l]; ++k) ld += rec[l][Rec<B>::LOGDET * g.K[l] * g.S + s * g.K[l] + k];
+        const double ld = top[s];  // cumulative records: the whole log-determinant
         g_diag[0] = ld;
         g_diag[1] = acc[P_LDQ];
         g_diag[2] = acc[P_FITY];
@@ -122,12 +120,7 @@ void emu_btd(int64_t n, int b, const double* diag, const double* upper, const do
     emu_launch(nblocks(g.K[0], tpb), tpb, [&] {
         k_revL<B, UserSource<B>, UserSink<B>>(usrc, usink, g, 0, fac[0].data(), sol[1].data(), needC ? 1 : 0);
     });
-    if (logdet) {
-        double ld = top[0];
-        for (int l = 0; l < g.nlev; ++l)
-            for (long long kk = 0; kk < g.K[l]; ++kk) ld += rec[l][Rec<B>::LOGDET * g.K[l] + kk];
-        *logdet = ld;
-    }
+    if (logdet) *logdet = top[0];  // cumulative records
 }
 
 // ---------------------------------------------------------------- segment mode ----
@@ -206,10 +199,7 @@ struct SegState : SegStateBase {
             for (long long k = 0; k < g.K[0]; ++k) acc += part[c * g.K[0] + k];
             partials[c] = acc;
         }
-        double ld = partials[P_LOGDET] + top[0];
-        for (int l = 1; l < g.nlev; ++l)
-            for (long long k = 0; k < g.K[l]; ++k) ld += rec[l][Rec<B>::LOGDET * g.K[l] + k];
-        partials[P_LOGDET] = ld;
+        partials[P_LOGDET] = top[0];
     }
 };
 

@@ -35,17 +35,27 @@ def series(seed, n, lo=0.05, hi=0.15):
 
 
 def check(got, leaves, theta, t, y, sigma, tols, threads=16, keys=("loglik", "grad", "mean", "var"), factor=4.0):
-    o = O.evaluate(leaves, theta, t, y, sigma, grad="grad" in keys, mean="mean" in keys, var="var" in keys,
-                   threads=threads)
-    ld = None
+    """Pass when rel(gpu, fp64 oracle) < tol; otherwise the GPU must be within
+    factor x the fp64 floor of the long-double evaluation.  The floor is the larger
+    distance to long double of two valid fp64 evaluations of the reference formulas:
+    the oracle in forward time order and on the time-reversed series (a stationary GP
+    has the same likelihood, gradient and posterior under t -> -t; only the
+    elimination order, i.e. the rounding, differs)."""
+    want = dict(grad="grad" in keys, mean="mean" in keys, var="var" in keys)
+    o = O.evaluate(leaves, theta, t, y, sigma, threads=threads, **want)
+    ld = orev = None
     for k in keys:
         tol = tols[k]
         if rel(got[k], o[k]) < tol:
             continue
         if ld is None:
-            ld = O.evaluate(leaves, theta, t, y, sigma, grad="grad" in keys, mean="mean" in keys, var="var" in keys,
-                            precision=1, threads=threads)
-        floor = rel(o[k], ld[k])
+            ld = O.evaluate(leaves, theta, t, y, sigma, precision=1, threads=threads, **want)
+            orev = O.evaluate(leaves, theta, -np.asarray(t)[::-1].copy(), np.asarray(y)[::-1].copy(), sigma,
+                              threads=threads, **want)
+            for kk in ("mean", "var"):
+                if kk in keys:
+                    orev[kk] = np.asarray(orev[kk])[::-1]
+        floor = max(rel(o[k], ld[k]), rel(orev[k], ld[k]))
         assert rel(got[k], ld[k]) <= max(tol, factor * floor), (k, rel(got[k], o[k]), rel(got[k], ld[k]), floor)
 
 
