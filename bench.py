@@ -350,6 +350,18 @@ def run_ours(args, ws, rank, local):
     want = dict(grad=True, mean="mean" in wl.outputs, var="var" in wl.outputs)
     h_out = torch.empty(S * (nt + 1) + S + (S * n if want["mean"] else 0) + (S * n if want["var"] else 0),
                         dtype=torch.float64).pin_memory()
+    # the public API writes into caller-owned (here pinned) host arrays
+    ho = h_out.numpy()
+    k0 = 0
+    outs = {"loglik": ho[k0:k0 + S]}
+    k0 += S
+    outs["grad"] = ho[k0:k0 + S * (nt + 1)].reshape((S, nt + 1) if wl.batched else (nt + 1,))
+    k0 += S * (nt + 1)
+    if want["mean"]:
+        outs["mean"] = ho[k0:k0 + S * n].reshape((S, n) if wl.batched else (n,))
+        k0 += S * n
+    if want["var"]:
+        outs["var"] = ho[k0:k0 + S * n].reshape((S, n) if wl.batched else (n,))
 
     def e2e_step():
         if partitioned:  # device entry points with explicit pinned H2D / D2H (the ABI is device-side here)
@@ -367,9 +379,9 @@ def run_ours(args, ws, rank, local):
                 h_out[k0:k0 + n].copy_(d_v, non_blocking=True)
             return
         if wl.batched:
-            ctx.eval_batched(wl.leaves, wl.theta, h_t.numpy(), h_y.numpy(), wl.sigma, **want)
+            ctx.eval_batched(wl.leaves, wl.theta, h_t.numpy(), h_y.numpy(), wl.sigma, out=outs, **want)
         else:
-            ctx.eval(wl.leaves, wl.theta, h_t.numpy(), h_y.numpy(), wl.sigma, **want)
+            ctx.eval(wl.leaves, wl.theta, h_t.numpy(), h_y.numpy(), wl.sigma, out=outs, **want)
 
     for _ in range(2):
         e2e_step()

@@ -125,6 +125,9 @@ int spingp_ctx_set_chunk(spingp_ctx* ctx, int64_t m0);
  * stream) and report them: spingp_ctx_kernel_times synchronises, returns up to
  * `cap` (name, milliseconds) pairs in launch order and clears the record. */
 int spingp_ctx_set_profiling(spingp_ctx* ctx, int on);
+/* Diagnostics: a device buffer of >= 64 uint64 that the fused upper-level kernel fills
+ * with %globaltimer stamps at every phase boundary (NULL = off). */
+int spingp_ctx_set_phase_stamps(spingp_ctx* ctx, void* d_stamps);
 int spingp_ctx_kernel_times(spingp_ctx* ctx, const char** names, double* ms, int32_t cap,
                             int32_t* count);
 

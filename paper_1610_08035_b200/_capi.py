@@ -79,6 +79,7 @@ SIGNATURES = {
     "spingp_ctx_destroy": (ctypes.c_int, [_vp]),
     "spingp_ctx_set_stream": (ctypes.c_int, [_vp, _vp]),
     "spingp_ctx_use_own_stream": (ctypes.c_int, [_vp]),
+    "spingp_ctx_set_phase_stamps": (ctypes.c_int, [_vp, _vp]),
     "spingp_ctx_get_stream": (_vp, [_vp]),
     "spingp_ctx_status": (ctypes.c_int, [_vp, _i64p]),
     "spingp_ctx_launch_count": (_i64, [_vp]),
@@ -179,6 +180,16 @@ def state_space(leaves, theta):
     return dict(F=F, H=H, Pinf=P, dF=dF, dPinf=dP, f_constant=fc, b=b)
 
 
+def _out(out, key, shape):
+    """A caller-supplied output array (validated) or a fresh zeroed one."""
+    if out is None or out.get(key) is None:
+        return np.zeros(shape)
+    a = out[key]
+    if a.dtype != np.float64 or not a.flags.c_contiguous or a.shape != tuple(shape) or not a.flags.writeable:
+        raise ValueError(f"out[{key!r}] must be a writeable C-contiguous float64 array of shape {tuple(shape)}")
+    return a
+
+
 class Context:
     """spingp_ctx: one CUDA device + stream + workspace."""
 
@@ -219,6 +230,10 @@ class Context:
         else:
             _raise(lib().spingp_ctx_set_stream(self._h, ctypes.c_void_p(int(stream_ptr))))
 
+    def set_phase_stamps(self, d_ptr):
+        """Diagnostics: device buffer (>= 64 uint64) for per-phase timer stamps (0 = off)."""
+        _raise(lib().spingp_ctx_set_phase_stamps(self._h, ctypes.c_void_p(int(d_ptr)) if d_ptr else None))
+
     def set_chunk(self, m0):
         _raise(lib().spingp_ctx_set_chunk(self._h, int(m0)))
 
@@ -242,8 +257,10 @@ class Context:
         _raise(lib().spingp_ctx_status(self._h, ctypes.byref(fb)), fb)
 
     # ---- host-pointer entry points (synchronous) ----------------------------------
-    def eval(self, leaves, theta, t, y, sigma, grad=True, mean=False, var=False, include_noise=False):
-        """log_marginal_likelihood + mll_gradient + training-point posterior."""
+    def eval(self, leaves, theta, t, y, sigma, grad=True, mean=False, var=False, include_noise=False, out=None):
+        """log_marginal_likelihood + mll_gradient + training-point posterior.
+        out: optional dict of preallocated float64 C-contiguous arrays ('grad', 'mean', 'var'),
+        e.g. views of pinned host memory, written in place (no per-call allocation)."""
         lv = _leaves(leaves)
         th = _f64(theta); t = _f64(t); y = _f64(y)
         n = len(t)
@@ -252,16 +269,17 @@ class Context:
         flags = (WANT_GRAD if grad else 0) | (WANT_MEAN if mean else 0) | (WANT_VAR if var else 0) | \
             (INCLUDE_NOISE if include_noise else 0)
         ll = _dbl()
-        g = np.zeros(len(th) + 1) if grad else None
-        mu = np.zeros(n) if mean else None
-        v = np.zeros(n) if var else None
+        g = _out(out, "grad", (len(th) + 1,)) if grad else None
+        mu = _out(out, "mean", (n,)) if mean else None
+        v = _out(out, "var", (n,)) if var else None
         fb = _i64()
         st = lib().spingp_eval(self._h, lv.ctypes.data, len(leaves), _p(th), len(th), _p(t), _p(y), n, float(sigma), flags,
                                ctypes.byref(ll), _p(g), _p(mu), _p(v), ctypes.byref(fb))
         _raise(st, fb)
         return dict(loglik=ll.value, grad=g, mean=mu, var=v)
 
-    def eval_batched(self, leaves, theta, t, y, sigma, grad=True, mean=False, var=False, include_noise=False):
+    def eval_batched(self, leaves, theta, t, y, sigma, grad=True, mean=False, var=False, include_noise=False,
+                     out=None):
         lv = _leaves(leaves)
         t = _f64(t); y = _f64(y)
         S, n = t.shape
@@ -269,10 +287,10 @@ class Context:
         sg = _f64(np.broadcast_to(np.asarray(sigma, dtype=np.float64), (S,)))
         flags = (WANT_GRAD if grad else 0) | (WANT_MEAN if mean else 0) | (WANT_VAR if var else 0) | \
             (INCLUDE_NOISE if include_noise else 0)
-        ll = np.zeros(S)
-        g = np.zeros((S, th.shape[1] + 1)) if grad else None
-        mu = np.zeros((S, n)) if mean else None
-        v = np.zeros((S, n)) if var else None
+        ll = _out(out, "loglik", (S,))
+        g = _out(out, "grad", (S, th.shape[1] + 1)) if grad else None
+        mu = _out(out, "mean", (S, n)) if mean else None
+        v = _out(out, "var", (S, n)) if var else None
         fb = _i64()
         st = lib().spingp_eval_batched(self._h, lv.ctypes.data, len(leaves), _p(th), th.shape[1], S, n, _p(t), _p(y),
                                        _p(sg), flags, _p(ll), _p(g), _p(mu), _p(v), ctypes.byref(fb))

@@ -270,6 +270,15 @@ int spingp_ctx_status(spingp_ctx* ctx, int64_t* fail_block) {
 
 int64_t spingp_ctx_launch_count(spingp_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int spingp_ctx_set_phase_stamps(spingp_ctx* ctx, void* d_stamps) {
+    return guarded(nullptr, [&] {
+        checked(ctx);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        ctx->upper_stamps = static_cast<unsigned long long*>(d_stamps);
+        return static_cast<int>(SPINGP_OK);
+    });
+}
+
 int spingp_ctx_set_profiling(spingp_ctx* ctx, int on) {
     if (!ctx) return SPINGP_BAD_ARG;
     std::lock_guard<std::mutex> lk(ctx->mu);

@@ -107,6 +107,7 @@ struct spingp_ctx {
     // self-resetting per-series arrival counters of k_reduce (kept out of the arena so
     // their zero state survives between calls; grown on demand, zeroed when allocated)
     unsigned int* d_arrive = nullptr;
+    unsigned long long* upper_stamps = nullptr;  // diagnostics (spingp_ctx_upper_stamps)
     long long arrive_cap = 0;
     unsigned int* counters(long long S) {
         if (S > arrive_cap) {

@@ -36,6 +36,15 @@
 
 #include <cstdint>
 
+// Minimum resident CTAs (of 128 threads) per SM requested for the level-0 kernels:
+// caps their registers at 65536 / (128 * minB).  Tuned on B200 (profiles/).
+#ifndef SP_FWD0_MINB
+#define SP_FWD0_MINB 3
+#endif
+#ifndef SP_REV0_MINB
+#define SP_REV0_MINB 1
+#endif
+
 #include "devmat.cuh"
 #include "model_dev.cuh"
 #ifndef SPINGP_HOST_EMU
@@ -234,7 +243,7 @@ SP_UNROLL
 // ======================================================= level 0 (fused) ======
 
 template <class T>
-__global__ void __launch_bounds__(128, 3) k_fwd0(ModelDesc md, const double* __restrict__ params,
+__global__ void __launch_bounds__(128, SP_FWD0_MINB) k_fwd0(ModelDesc md, const double* __restrict__ params,
                                               const double* __restrict__ t,
                                               const double* __restrict__ y, Geom geo,
                                               double* __restrict__ fac, double* __restrict__ rec,
@@ -751,24 +760,37 @@ struct UpperArgs {
     double* toplogdet;
     unsigned long long* status;
     int needC, do_fwd, do_top, do_rev;
+    unsigned long long* stamps;  // diagnostics: %globaltimer after every phase (null = off)
 };
+SP_DEV void upper_stamp(const UpperArgs& a, int& k) {
+    if (a.stamps && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.stamps[k] = t;
+    }
+    ++k;
+}
 template <int B>
 __global__ void __launch_bounds__(128) k_upper(Geom geo, UpperArgs a) {
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
     const long long tid = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     const long long nth = static_cast<long long>(gridDim.x) * blockDim.x;
+    int ks = 0;
+    upper_stamp(a, ks);
     if (a.do_fwd) {
         for (int l = 1; l < geo.nlev; ++l) {
             const RecSource<B> src{a.rec[l - 1], geo.K[l - 1] * geo.S, geo.n[l]};
             const long long SK = geo.K[l] * geo.S;
             for (long long g = tid; g < SK; g += nth) fwdL_item<B, RecSource<B>>(src, geo, l, a.fac[l], a.rec[l], a.status, g);
             grid.sync();
+            upper_stamp(a, ks);
         }
     }
     if (a.do_top) {
         for (long long s = tid; s < geo.S; s += nth)
             top_item<B>(geo, a.rec[geo.nlev - 1], a.sol[geo.nlev], a.toplogdet, a.status, static_cast<int>(s));
         grid.sync();
+        upper_stamp(a, ks);
     }
     if (a.do_rev) {
         for (int l = geo.nlev - 1; l >= 1; --l) {
@@ -778,6 +800,7 @@ __global__ void __launch_bounds__(128) k_upper(Geom geo, UpperArgs a) {
             for (long long g = tid; g < SK; g += nth)
                 revL_item<B, RecSource<B>, SolSink<B>>(src, sink, geo, l, a.fac[l], a.sol[l + 1], a.needC, g);
             if (l > 1) grid.sync();
+            upper_stamp(a, ks);
         }
     }
 }
@@ -904,7 +927,7 @@ SP_UNROLL
 }
 
 template <class T>
-__global__ void __launch_bounds__(128) k_rev0(ModelDesc md, const double* __restrict__ params,
+__global__ void __launch_bounds__(128, SP_REV0_MINB) k_rev0(ModelDesc md, const double* __restrict__ params,
                                               const double* __restrict__ t,
                                               const double* __restrict__ y, Geom geo,
                                               const double* __restrict__ fac,

@@ -2,6 +2,7 @@
 // model description and per-series parameter records, plus the host-only C ABI
 // entry points (spingp_kernel_dims, spingp_state_space).  Uses the drop-in
 // C++ API of include/spingp/kernels.hpp for the reference's state_space_of.
+#include <cstdlib>
 #include "host_model.hpp"
 
 #include <algorithm>
@@ -316,7 +317,13 @@ Plan make_plan(int64_t n, int64_t S, int Bsz, int64_t m0_override) {
     Plan p;
     Geom& g = p.geo;
     g.S = static_cast<int>(S);
-    const int64_t target = Bsz <= 3 ? 37888 : 18944;
+    // level-0 chunk count: enough threads to fill every SM (tuned on B200);
+    // SPINGP_CHUNKS overrides it for tuning experiments
+    static const int64_t env_target = [] {
+        const char* e = std::getenv("SPINGP_CHUNKS");
+        return e ? std::atoll(e) : 0LL;
+    }();
+    const int64_t target = env_target > 0 ? env_target : (Bsz <= 3 ? 75776 : 18944);
     int64_t m0 = m0_override > 0 ? m0_override : std::max<int64_t>(8, (n * S + target - 1) / target);
     m0 = std::max<int64_t>(1, std::min<int64_t>(m0, n));
     int lev = 0;

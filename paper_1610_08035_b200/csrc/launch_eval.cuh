@@ -162,6 +162,7 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
         ua.do_fwd = a.mode == 0;
         ua.do_top = a.mode == 0;
         ua.do_rev = 1;
+        ua.stamps = ctx->upper_stamps;
         launch_upper<B>(ctx, g, ua);
     } else {
         if (a.mode != 3) {
