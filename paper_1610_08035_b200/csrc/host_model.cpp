@@ -323,7 +323,7 @@ Plan make_plan(int64_t n, int64_t S, int Bsz, int64_t m0_override) {
         const char* e = std::getenv("SPINGP_CHUNKS");
         return e ? std::atoll(e) : 0LL;
     }();
-    const int64_t target = env_target > 0 ? env_target : (Bsz <= 3 ? 75776 : 18944);
+    const int64_t target = env_target > 0 ? env_target : 75776;
     int64_t m0 = m0_override > 0 ? m0_override : std::max<int64_t>(8, (n * S + target - 1) / target);
     m0 = std::max<int64_t>(1, std::min<int64_t>(m0, n));
     int lev = 0;
