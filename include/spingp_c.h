@@ -121,6 +121,9 @@ int spingp_ctx_status(spingp_ctx* ctx, int64_t* fail_block);
 int64_t spingp_ctx_launch_count(spingp_ctx* ctx);
 /* Tuning/testing knob: force the level-0 chunk length (0 = automatic). */
 int spingp_ctx_set_chunk(spingp_ctx* ctx, int64_t m0);
+/* Testing knob: cap the records per shared-memory tree group of levels >= 1
+ * (0 = automatic, the largest that fits a CTA; >= 2 forces more tree levels). */
+int spingp_ctx_set_tree_group(spingp_ctx* ctx, int64_t g);
 /* Diagnostics: bracket every kernel launch with CUDA events (on the context's
  * stream) and report them: spingp_ctx_kernel_times synchronises, returns up to
  * `cap` (name, milliseconds) pairs in launch order and clears the record. */

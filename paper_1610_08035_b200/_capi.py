@@ -84,6 +84,7 @@ SIGNATURES = {
     "spingp_ctx_status": (ctypes.c_int, [_vp, _i64p]),
     "spingp_ctx_launch_count": (_i64, [_vp]),
     "spingp_ctx_set_chunk": (ctypes.c_int, [_vp, _i64]),
+    "spingp_ctx_set_tree_group": (ctypes.c_int, [_vp, _i64]),
     "spingp_ctx_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int]),
     "spingp_ctx_kernel_times": (ctypes.c_int, [_vp, _P(ctypes.c_char_p), _d, _i32, _i32p]),
     "spingp_eval": (ctypes.c_int, [_vp, _vp, _i32, _d, _i32, _d, _d, _i64, _dbl, _u32, _d, _d, _d, _d, _i64p]),
@@ -236,6 +237,9 @@ class Context:
 
     def set_chunk(self, m0):
         _raise(lib().spingp_ctx_set_chunk(self._h, int(m0)))
+
+    def set_tree_group(self, g):
+        _raise(lib().spingp_ctx_set_tree_group(self._h, int(g)))
 
     def set_profiling(self, on=True):
         _raise(lib().spingp_ctx_set_profiling(self._h, 1 if on else 0))

@@ -14,7 +14,7 @@ template <int B>
 void launch_btd(spingp_ctx* ctx, int64_t n, int b, const double* d_diag, const double* d_upper,
                 const double* d_rhs, int k, int col, double* d_x, double* d_cdiag, double* d_cupper,
                 double* d_logdet, bool needC) {
-    const Plan plan = make_plan(n, 1, B, ctx->m0_override);
+    const Plan plan = make_plan(n, 1, B, ctx->m0_override, 0);  // per-thread levels (materialised path)
     const Geom& g = plan.geo;
     size_t tot = 4096;
     for (int l = 0; l < g.nlev; ++l)

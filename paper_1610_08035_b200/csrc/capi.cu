@@ -153,7 +153,7 @@ static int seg_run(spingp_ctx* ctx, int mode, const spingp_leaf* leaves, int32_t
         if (rank + 1 < nranks && !(t_right < 0.0 || t_right >= 0.0)) throw std::invalid_argument("missing right halo time");
         std::lock_guard<std::mutex> lk(ctx->mu);
         const HostModel hm = build_model(leaves, n_leaves, n_theta);
-        Plan plan = make_plan(n_local, 1, plan_bsize(hm), ctx->m0_override);
+        Plan plan = make_plan(n_local, 1, plan_bsize(hm), ctx->m0_override, -1, ctx->g_override);
         plan.geo.segL = rank > 0 ? 1 : 0;
         plan.geo.segR = rank + 1 < nranks ? 1 : 0;
         std::vector<double> params(hm.rec_stride + 2, 0.0);
@@ -260,6 +260,12 @@ int spingp_ctx_set_chunk(spingp_ctx* ctx, int64_t m0) {
     return SPINGP_OK;
 }
 
+int spingp_ctx_set_tree_group(spingp_ctx* ctx, int64_t g) {
+    if (!ctx || g < 0 || g == 1) return SPINGP_BAD_ARG;
+    ctx->g_override = g;
+    return SPINGP_OK;
+}
+
 int spingp_ctx_status(spingp_ctx* ctx, int64_t* fail_block) {
     return guarded(fail_block, [&] {
         checked(ctx);
@@ -321,7 +327,7 @@ int spingp_eval_batched_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32
         if ((flags & SPINGP_WANT_VAR) && !d_var) throw std::invalid_argument("variance output is null");
         std::lock_guard<std::mutex> lk(ctx->mu);
         const HostModel hm = build_model(leaves, n_leaves, n_theta);
-        const Plan plan = make_plan(n, S, plan_bsize(hm), ctx->m0_override);
+        const Plan plan = make_plan(n, S, plan_bsize(hm), ctx->m0_override, -1, ctx->g_override);
         std::vector<double> params(static_cast<size_t>(S) * hm.rec_stride, 0.0);
         for (int64_t s = 0; s < S; ++s)
             fill_record(hm, theta + s * n_theta, sigma[s], params.data() + s * hm.rec_stride);

@@ -78,6 +78,7 @@ struct spingp_ctx {
     int stage_slot = 0, cur_slot = 0;
     int64_t launches = 0;
     int64_t m0_override = 0;  // testing knob: force the level-0 chunk length
+    int64_t g_override = 0;   // testing knob: force a smaller tree group (more tree levels)
     std::mutex mu;
     // optional per-launch CUDA-event timing (spingp_ctx_set_profiling)
     bool profiling = false;

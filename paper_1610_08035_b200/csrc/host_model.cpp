@@ -312,9 +312,21 @@ StaticModel static_model(const HostModel& hm) {
     return SM_NONE;
 }
 
-Plan make_plan(int64_t n, int64_t S, int Bsz, int64_t m0_override) {
+bool upper_tree() {
+    static const bool t = [] {
+        const char* e = std::getenv("SPINGP_UPPER");
+        return !(e && (std::strcmp(e, "coop") == 0 || std::strcmp(e, "levels") == 0));
+    }();
+    return t;
+}
+
+Plan make_plan(int64_t n, int64_t S, int Bsz, int64_t m0_override, int tree, int64_t g_override) {
     if (n < 1 || S < 1) throw std::invalid_argument("need at least one point and one series");
     Plan p;
+    // b >= 6: one thread per b x b merge is too long a chain for the tree's single-thread
+    // top rounds (measured on B200: cfg4 45.9 vs 33.9 ms, cfg5 811 vs 385 ms per 1M/200k
+    // points); those sizes keep the cooperative per-thread levels
+    p.tree = (tree < 0 ? upper_tree() : tree != 0) && Bsz <= 4;
     Geom& g = p.geo;
     g.S = static_cast<int>(S);
     // level-0 chunk count: enough threads to fill every SM (tuned on B200);
@@ -326,18 +338,20 @@ Plan make_plan(int64_t n, int64_t S, int Bsz, int64_t m0_override) {
     const int64_t target = env_target > 0 ? env_target : 75776;
     int64_t m0 = m0_override > 0 ? m0_override : std::max<int64_t>(8, (n * S + target - 1) / target);
     m0 = std::max<int64_t>(1, std::min<int64_t>(m0, n));
+    const int64_t G = g_override >= 2 ? std::min<int64_t>(g_override, tree_group_size(Bsz)) : tree_group_size(Bsz);
     int lev = 0;
     int64_t cur = n, m = m0;
     while (true) {
         if (lev >= kMaxLev) throw ApiError{SPINGP_UNSUPPORTED, -1, "too many reduction levels"};
-        if (lev > 0) m = cur <= 8 ? cur : 4;
+        if (lev > 0) m = p.tree ? std::min(cur, G) : (cur <= 8 ? cur : 4);
         if (m < 2 && cur > 1) m = 2;
         g.n[lev] = cur;
         g.m[lev] = static_cast<int>(m);
         g.K[lev] = (cur + m - 1) / m;
         cur = g.K[lev];
         ++lev;
-        if (cur == 1) break;
+        // the tree path always ends with a tree level (its top group holds the inverse)
+        if (cur == 1 && (!p.tree || lev > 1)) break;
     }
     g.nlev = lev;
     g.n[lev] = 1;

@@ -34,10 +34,19 @@ HostModel build_model(const spingp_leaf* leaves, int32_t n_leaves, int32_t n_the
 void fill_record(const HostModel& hm, const double* theta, double sigma, double* rec);
 
 // Level structure of the hierarchical reduction for S series of n points.
+// tree: levels >= 1 are shared-memory tree groups of tree_group_size(Bsz) records
+// (tree.cuh) and there is always at least one such level; otherwise the per-thread
+// 4-record chunks of k_fwdL / k_revL (the materialised btd_core path, and the
+// SPINGP_UPPER=coop|levels comparison knob).
 struct Plan {
     spingp_dev::Geom geo{};
+    bool tree = false;
 };
-Plan make_plan(int64_t n, int64_t S, int Bsz, int64_t m0_override = 0);
+// Upper-level scheme of the eval path: true = trees (default), false when
+// SPINGP_UPPER=coop|levels.
+bool upper_tree();
+// g_override (testing knob): a smaller tree group size than tree_group_size(Bsz).
+Plan make_plan(int64_t n, int64_t S, int Bsz, int64_t m0_override = 0, int tree = -1, int64_t g_override = 0);
 
 // Padded block size with a kernel instantiation (1, 2, 3, 4, 6, 8, 12, 16).
 int pad_b(int b);

@@ -2,6 +2,9 @@
 // level-0 fused forward -> upper-level forwards -> top inverse -> upper-level
 // reverses -> level-0 fused reverse (outputs, loglik terms, gradient) ->
 // deterministic two-stage reduction.  Included by the inst_*.cu files only.
+// Upper levels: shared-memory tree groups (tree.cuh; default), or the per-thread
+// 4-record chains as one cooperative kernel (SPINGP_UPPER=coop) or one kernel per
+// level (SPINGP_UPPER=levels).
 #pragma once
 
 #include <algorithm>
@@ -9,6 +12,7 @@
 #include <cstring>
 
 #include "ctx.hpp"
+#include "tree.cuh"
 
 namespace spingp_host {
 
@@ -33,7 +37,7 @@ EvalBufs carve_eval(spingp_ctx* ctx, const Plan& p, int nt, size_t params_count)
     size_t tot = arena_bytes(params_count) + 4096;
     for (int l = 0; l < g.nlev; ++l) {
         const size_t SK = static_cast<size_t>(g.K[l]) * g.S;
-        tot += arena_bytes(static_cast<size_t>(g.m[l]) * Fac<B>::N * SK) + arena_bytes(Rec<B>::N * SK);
+        tot += arena_bytes(static_cast<size_t>(g.m[l]) * (l ? Tree<B>::NF : Fac<B>::N) * SK) + arena_bytes(Rec<B>::N * SK);
     }
     for (int l = 1; l <= g.nlev; ++l) tot += arena_bytes(Sol<B>::N * static_cast<size_t>(g.n[l] + g.segL) * g.S);
     const size_t SK0 = static_cast<size_t>(g.K[0]) * g.S;
@@ -46,7 +50,7 @@ EvalBufs carve_eval(spingp_ctx* ctx, const Plan& p, int nt, size_t params_count)
     eb.params = ctx->ws.take<double>(params_count);
     for (int l = 0; l < g.nlev; ++l) {
         const size_t SK = static_cast<size_t>(g.K[l]) * g.S;
-        eb.fac[l] = ctx->ws.take<double>(static_cast<size_t>(g.m[l]) * Fac<B>::N * SK);
+        eb.fac[l] = ctx->ws.take<double>(static_cast<size_t>(g.m[l]) * (l ? Tree<B>::NF : Fac<B>::N) * SK);
         eb.rec[l] = ctx->ws.take<double>(Rec<B>::N * SK);
     }
     for (int l = 1; l <= g.nlev; ++l)
@@ -92,6 +96,58 @@ void launch_upper(spingp_ctx* ctx, const Geom& g, UpperArgs& ua) {
     ctx->launched("k_upper");
 }
 
+// Tree level l (>= 1): groups of m[l] records of level l-1.
+template <int B>
+TreeArgs tree_args(spingp_ctx* ctx, const Geom& g, const EvalBufs& eb, int l, bool needC) {
+    TreeArgs ta{};
+    ta.rec_in = eb.rec[l - 1];
+    ta.SKin = g.K[l - 1] * g.S;
+    ta.nin = g.n[l];
+    ta.rec_out = eb.rec[l];
+    ta.fac = eb.fac[l];
+    ta.solU = eb.sol[l + 1];
+    ta.sol = eb.sol[l];
+    ta.toplogdet = eb.toplogdet;
+    ta.status = ctx->d_status;
+    ta.G = g.m[l];
+    ta.nG = static_cast<int>(g.K[l]);
+    ta.S = g.S;
+    ta.segL = g.segL;
+    ta.needC = needC ? 1 : 0;
+    const long long gcap = std::min<long long>(g.m[l], g.n[l]);
+    ta.RS = static_cast<int>(tree_row(gcap));
+    ta.ES = static_cast<int>(tree_row(gcap + 1));
+    ta.span = 1;
+    for (int i = 1; i < l; ++i) ta.span *= g.m[i];
+    ta.K0 = g.K[0];
+    ta.n0 = g.n[0];
+    ta.m0 = g.m[0];
+    return ta;
+}
+
+enum TreeKind { TREE_FWD = 0, TREE_REV = 1, TREE_ONE = 2 };
+
+template <int B>
+void launch_tree(spingp_ctx* ctx, TreeKind kind, TreeArgs& ta) {
+    using TR = Tree<B>;
+    void (*kern)(TreeArgs) = kind == TREE_FWD ? k_tree_fwd<B> : kind == TREE_REV ? k_tree_rev<B> : k_tree_one<B>;
+    static bool attr[3] = {false, false, false};
+    if (!attr[kind]) {  // opt in to the full 227 KB of shared memory once per kernel
+        CUDA_OK(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(tree_smem_bytes(B, tree_group_size(B)))));
+        attr[kind] = true;
+    }
+    const size_t smem = 8 * (static_cast<size_t>(TR::NR) * ta.RS + (kind == TREE_FWD ? 0 : static_cast<size_t>(TR::NS) * ta.ES));
+    const int half = std::min(ta.G, static_cast<int>(ta.RS)) / 2 + 1;  // nodes of the first round
+    const int tpb = std::min(kTreeMaxThreads, std::max(32, (half + 31) / 32 * 32));
+    const long long groups = static_cast<long long>(ta.S) * ta.nG;
+    // diagnostics: stamps of CTA 0 at [0,16) k_tree_fwd, [16,48) k_tree_one, [48,64) k_tree_rev
+    ta.stamps = ctx->upper_stamps ? ctx->upper_stamps + (kind == TREE_FWD ? 0 : kind == TREE_ONE ? 16 : 48) : nullptr;
+    ctx->pre();
+    kern<<<static_cast<unsigned>(groups), tpb, smem, ctx->stream>>>(ta);
+    ctx->launched(kind == TREE_FWD ? "k_tree_fwd" : kind == TREE_REV ? "k_tree_rev" : "k_tree_one");
+}
+
 template <class T>
 void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     constexpr int B = T::B;
@@ -112,6 +168,8 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     const double* halo = (a.mode >= 2) ? eb.params + a.nparams - 2 : nullptr;
 
     const int tpb = 128;
+    const bool grad = a.flags & SPINGP_WANT_GRAD;
+    const bool needC = grad || (a.flags & SPINGP_WANT_VAR);
     if (a.mode == 1) {
         ctx->pre();
         k_assemble<T><<<blocks_for(g.n[0], tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g.n[0], a.d_diag,
@@ -120,15 +178,21 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
         return;
     }
     const long long SK0 = g.K[0] * g.S;
-    const bool grad = a.flags & SPINGP_WANT_GRAD;
-    const bool needC = grad || (a.flags & SPINGP_WANT_VAR);
+    const bool tree = a.plan->tree;
     const bool fused = upper_fused();
     if (a.mode != 3) {
         ctx->pre();
         k_fwd0<T><<<blocks_for(SK0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
                                                                  eb.rec[0], eb.part, ctx->d_status, halo);
         ctx->launched("k_fwd0");
-        if (!fused || a.mode == 2) {
+        if (tree) {
+            // mode 0: the last level (one group per series) is k_tree_one below
+            const int lastf = a.mode == 0 ? g.nlev - 2 : g.nlev - 1;
+            for (int l = 1; l <= lastf; ++l) {
+                TreeArgs ta = tree_args<B>(ctx, g, eb, l, needC);
+                launch_tree<B>(ctx, TREE_FWD, ta);
+            }
+        } else if (!fused || a.mode == 2) {
             for (int l = 1; l < g.nlev; ++l) {
                 RecSource<B> src{eb.rec[l - 1], g.K[l - 1] * g.S, g.n[l]};
                 ctx->pre();
@@ -149,7 +213,18 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
                                                  ctx->d_status, g.n[0] - 1, eb.segscratch);
         ctx->launched("k_seg_solve");
     }
-    if (fused && (a.mode == 0 || g.nlev > 1)) {
+    if (tree) {
+        int l = g.nlev - 1;
+        if (a.mode == 0) {
+            TreeArgs ta = tree_args<B>(ctx, g, eb, l, needC);
+            launch_tree<B>(ctx, TREE_ONE, ta);
+            --l;
+        }
+        for (; l >= 1; --l) {
+            TreeArgs ta = tree_args<B>(ctx, g, eb, l, needC);
+            launch_tree<B>(ctx, TREE_REV, ta);
+        }
+    } else if (fused && (a.mode == 0 || g.nlev > 1)) {
         UpperArgs ua{};
         for (int l = 0; l < g.nlev; ++l) {
             ua.rec[l] = eb.rec[l];

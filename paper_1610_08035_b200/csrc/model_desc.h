@@ -37,4 +37,19 @@ struct Geom {
     int segL, segR;
 };
 
+// Levels >= 1 as CTA-wide binary trees in shared memory (tree.cuh): a level-l group is
+// G(B) consecutive level-(l-1) records of one series.  G is the largest power of two
+// (<= 512, two records per thread of a 256-thread CTA) whose records plus separators fit
+// the 227 KB opt-in shared memory of a CTA (component-major rows of even length).
+constexpr long long kTreeSmemCap = 232448 - 2048;
+constexpr long long tree_row(long long n) { return (n + 1) & ~1LL; }
+constexpr long long tree_smem_bytes(int B, long long G) {
+    return 8 * ((3 * B * B + 2 * B + 1) * tree_row(G) + (B + 2 * B * B) * tree_row(G + 1));
+}
+constexpr int tree_group_size(int B) {
+    int G = 512;
+    while (G > 2 && tree_smem_bytes(B, G) > kTreeSmemCap) G >>= 1;
+    return G;
+}
+
 }  // namespace spingp_dev

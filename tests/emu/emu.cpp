@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../paper_1610_08035_b200/csrc/engine.cuh"
+#include "../../paper_1610_08035_b200/csrc/tree.cuh"
 #include "../../paper_1610_08035_b200/csrc/host_model.hpp"
 
 using namespace spingp_dev;
@@ -20,10 +21,93 @@ using namespace spingp_host;
 namespace {
 
 std::string g_err;
+int64_t g_tree_group = 0;  // emu_set_tree_group
 unsigned long long g_status;
 double g_diag[4];  // logdetP, logdetQ, fit_y, fit_e of the last series evaluated
 
 unsigned nblocks(long long n, int tpb) { return static_cast<unsigned>((n + tpb - 1) / tpb); }
+
+// ------------------------------------------------------------ tree levels (tree.cuh) --
+// The CTA of k_tree_fwd / k_tree_rev / k_tree_one emulated phase by phase: every
+// emulated thread runs a phase before any runs the next (the kernel's barriers).
+enum EmuTree { EMU_FWD = 0, EMU_REV = 1, EMU_ONE = 2 };
+
+template <int B>
+TreeArgs emu_tree_args(const Geom& g, int l, std::vector<std::vector<double>>& rec, std::vector<std::vector<double>>& fac,
+                       std::vector<std::vector<double>>& sol, std::vector<double>& top, bool needC) {
+    TreeArgs ta{};
+    ta.rec_in = rec[l - 1].data();
+    ta.SKin = g.K[l - 1] * g.S;
+    ta.nin = g.n[l];
+    ta.rec_out = rec[l].data();
+    ta.fac = fac[l].data();
+    ta.solU = sol[l + 1].data();
+    ta.sol = sol[l].data();
+    ta.toplogdet = top.data();
+    ta.status = &g_status;
+    ta.G = g.m[l];
+    ta.nG = static_cast<int>(g.K[l]);
+    ta.S = g.S;
+    ta.segL = g.segL;
+    ta.needC = needC ? 1 : 0;
+    const long long gcap = std::min<long long>(g.m[l], g.n[l]);
+    ta.RS = static_cast<int>(tree_row(gcap));
+    ta.ES = static_cast<int>(tree_row(gcap + 1));
+    ta.span = 1;
+    for (int i = 1; i < l; ++i) ta.span *= g.m[i];
+    ta.K0 = g.K[0];
+    ta.n0 = g.n[0];
+    ta.m0 = g.m[0];
+    return ta;
+}
+
+template <int B>
+void emu_tree(EmuTree kind, const TreeArgs& ta) {
+    using TR = Tree<B>;
+    std::vector<double> sm(static_cast<size_t>(TR::NR) * ta.RS + static_cast<size_t>(TR::NS) * ta.ES, std::nan(""));
+    double* R = sm.data();
+    double* E = R + static_cast<size_t>(TR::NR) * ta.RS;
+    const int nt = std::max(1, (std::min(ta.G, ta.RS) + 1) / 2);  // one node per thread per round
+    std::vector<TreeFwdScratch<B>> fs(nt);
+    std::vector<TreeRevScratch<B>> rs(nt);
+    const bool needC = ta.needC != 0;
+    for (long long gidx = 0; gidx < static_cast<long long>(ta.S) * ta.nG; ++gidx) {
+        const TreeGroup t = tree_group(ta, gidx);
+        auto all = [&](auto&& f) {
+            for (int tid = 0; tid < nt; ++tid) f(tid);
+        };
+        const int J = tree_levels(t.cnt);
+        if (kind != EMU_REV) {
+            all([&](int tid) { tree_load_recs<B>(ta, t, R, tid, nt); });
+            for (int j = 0; j < J; ++j) {
+                const int n = tree_width(t.cnt, j);
+                all([&](int tid) {
+                    tree_fwd_compute<B>(R, ta.RS, n, tid, fs[tid]);
+                    if (!fs[tid].ok) report(ta.status, tree_point(ta, t, t.k0 + std::min(t.cnt, (2 * tid + 1) << j) - 1), ST_NOT_PD);
+                });
+                all([&](int tid) { tree_fwd_store<B>(R, ta.RS, n, tid, fs[tid]); });
+            }
+        }
+        if (kind == EMU_FWD) {
+            all([&](int tid) { tree_store_fwd<B>(ta, t, R, tid, nt); });
+            continue;
+        }
+        if (kind == EMU_ONE) tree_top<B>(ta, t, R, E);
+        else all([&](int tid) { tree_load_rev<B>(ta, t, R, E, tid, nt); });
+        for (int j = J - 1; j >= 0; --j) {
+            const int n = tree_width(t.cnt, j);
+            all([&](int tid) { tree_rev_compute<B>(R, E, ta.RS, ta.ES, n, tid, needC, rs[tid]); });
+            all([&](int tid) { tree_rev_store<B>(E, ta.ES, n, tid, needC, rs[tid]); });
+        }
+        all([&](int tid) { tree_store_rev<B>(ta, t, E, tid, nt); });
+    }
+}
+
+// fac[l] sized for the tree factors at levels >= 1
+template <int B>
+size_t emu_fac_size(const Geom& g, int l) {
+    return static_cast<size_t>(g.m[l]) * (l ? Tree<B>::NF : Fac<B>::N) * g.K[l] * g.S;
+}
 
 template <class T>
 void emu_eval(const HostModel& hm, const Plan& plan, std::vector<double>& params, const double* t,
@@ -37,7 +121,7 @@ void emu_eval(const HostModel& hm, const Plan& plan, std::vector<double>& params
     std::vector<std::vector<double>> fac(g.nlev), rec(g.nlev), sol(g.nlev + 1);
     for (int l = 0; l < g.nlev; ++l) {
         const size_t SK = static_cast<size_t>(g.K[l]) * g.S;
-        fac[l].assign(static_cast<size_t>(g.m[l]) * Fac<B>::N * SK, 0.0);
+        fac[l].assign(emu_fac_size<B>(g, l), 0.0);
         rec[l].assign(Rec<B>::N * SK, 0.0);
     }
     for (int l = 1; l <= g.nlev; ++l) sol[l].assign(Sol<B>::N * static_cast<size_t>(g.n[l]) * g.S, 0.0);
@@ -49,19 +133,25 @@ void emu_eval(const HostModel& hm, const Plan& plan, std::vector<double>& params
     emu_launch(nblocks(SK0, tpb), tpb, [&] {
         k_fwd0<T>(md, params.data(), t, y, g, fac[0].data(), rec[0].data(), part.data(), st, nullptr);
     });
+    const bool gr = flags & 1u, needC = gr || (flags & 4u);
+    if (plan.tree) {
+        for (int l = 1; l + 1 < g.nlev; ++l) emu_tree<B>(EMU_FWD, emu_tree_args<B>(g, l, rec, fac, sol, top, needC));
+        emu_tree<B>(EMU_ONE, emu_tree_args<B>(g, g.nlev - 1, rec, fac, sol, top, needC));
+        for (int l = g.nlev - 2; l >= 1; --l) emu_tree<B>(EMU_REV, emu_tree_args<B>(g, l, rec, fac, sol, top, needC));
+    } else {
     for (int l = 1; l < g.nlev; ++l) {
         RecSource<B> src{rec[l - 1].data(), g.K[l - 1] * g.S, g.n[l]};
         emu_launch(nblocks(g.K[l] * g.S, tpb), tpb,
                    [&] { k_fwdL<B, RecSource<B>>(src, g, l, fac[l].data(), rec[l].data(), st); });
     }
     emu_launch(nblocks(g.S, tpb), tpb, [&] { k_top<B>(g, rec[g.nlev - 1].data(), sol[g.nlev].data(), top.data(), st); });
-    const bool gr = flags & 1u, needC = gr || (flags & 4u);
     for (int l = g.nlev - 1; l >= 1; --l) {
         RecSource<B> src{rec[l - 1].data(), g.K[l - 1] * g.S, g.n[l]};
         SolSink<B> sink{sol[l].data(), g.n[l] * g.S, g.n[l], 0};
         emu_launch(nblocks(g.K[l] * g.S, tpb), tpb, [&] {
             k_revL<B, RecSource<B>, SolSink<B>>(src, sink, g, l, fac[l].data(), sol[l + 1].data(), needC ? 1 : 0);
         });
+    }
     }
     Outs outs{(flags & 2u) ? mean : nullptr, (flags & 4u) ? var : nullptr, (flags & 8u) ? 1 : 0, gr ? 1 : 0,
               needC ? 1 : 0};
@@ -91,7 +181,7 @@ void emu_eval(const HostModel& hm, const Plan& plan, std::vector<double>& params
 template <int B>
 void emu_btd(int64_t n, int b, const double* diag, const double* upper, const double* rhs, int k, int col,
              double* x, double* cdiag, double* cupper, double* logdet, bool needC, int64_t m0) {
-    const Plan plan = make_plan(n, 1, B, m0);
+    const Plan plan = make_plan(n, 1, B, m0, 0);
     const Geom& g = plan.geo;
     std::vector<std::vector<double>> fac(g.nlev), rec(g.nlev), sol(g.nlev + 1);
     for (int l = 0; l < g.nlev; ++l) {
@@ -155,7 +245,7 @@ struct SegState : SegStateBase {
         rec.resize(g.nlev);
         sol.resize(g.nlev + 1);
         for (int l = 0; l < g.nlev; ++l) {
-            fac[l].assign(static_cast<size_t>(g.m[l]) * Fac<B>::N * g.K[l], 0.0);
+            fac[l].assign(emu_fac_size<B>(g, l), 0.0);
             rec[l].assign(Rec<B>::N * g.K[l], 0.0);
         }
         for (int l = 1; l <= g.nlev; ++l) sol[l].assign(Sol<B>::N * static_cast<size_t>(g.n[l] + g.segL), 0.0);
@@ -170,6 +260,10 @@ struct SegState : SegStateBase {
             k_fwd0<T>(md, params.data(), t, y, g, fac[0].data(), rec[0].data(), part.data(), st, halo());
         });
         for (int l = 1; l < g.nlev; ++l) {
+            if (plan.tree) {
+                emu_tree<B>(EMU_FWD, emu_tree_args<B>(g, l, rec, fac, sol, top, false));
+                continue;
+            }
             RecSource<B> src{rec[l - 1].data(), g.K[l - 1], g.n[l]};
             emu_launch(nblocks(g.K[l], 32), 32, [&] { k_fwdL<B, RecSource<B>>(src, g, l, fac[l].data(), rec[l].data(), st); });
         }
@@ -182,6 +276,10 @@ struct SegState : SegStateBase {
         emu_launch(1, 1, [&] { k_seg_solve<B>(nranks, rank, records, sol[g.nlev].data(), top.data(), st, 0, scratch.data()); });
         const bool gr = flags & 1u, needC = gr || (flags & 4u);
         for (int l = g.nlev - 1; l >= 1; --l) {
+            if (plan.tree) {
+                emu_tree<B>(EMU_REV, emu_tree_args<B>(g, l, rec, fac, sol, top, needC));
+                continue;
+            }
             RecSource<B> src{rec[l - 1].data(), g.K[l - 1], g.n[l]};
             SolSink<B> sink{sol[l].data(), g.n[l] + g.segL, g.n[l], g.segL};
             emu_launch(nblocks(g.K[l], 32), 32, [&] {
@@ -215,6 +313,7 @@ int finish() {
 extern "C" {
 
 const char* emu_last_error(void) { return g_err.c_str(); }
+void emu_set_tree_group(int64_t g) { g_tree_group = g; }
 void emu_last_diag(double* out) {
     for (int i = 0; i < 4; ++i) out[i] = g_diag[i];
 }
@@ -229,7 +328,7 @@ int emu_eval_batched(const spingp_leaf* leaves, int32_t n_leaves, const double* 
         const bool matern = hm.single_matern && !force_generic;
         const StaticModel sm = force_generic ? SM_NONE : static_model(hm);
         const int Bsz = (matern || sm != SM_NONE) ? hm.b : std::max(3, pad_b(hm.b));
-        const Plan plan = make_plan(n, S, Bsz, m0);
+        const Plan plan = make_plan(n, S, Bsz, m0, -1, g_tree_group);
         std::vector<double> params(static_cast<size_t>(S) * hm.rec_stride, 0.0);
         for (int64_t s = 0; s < S; ++s) fill_record(hm, theta + s * n_theta, sigma[s], params.data() + s * hm.rec_stride);
 #define E(...) emu_eval<__VA_ARGS__>(hm, plan, params, t, y, flags, loglik, grad, mean, var)
@@ -354,7 +453,7 @@ int emu_seg_forward(const spingp_leaf* leaves, int32_t n_leaves, const double* t
         const HostModel hm = build_model(leaves, n_leaves, n_theta);
         const StaticModel sm = static_model(hm);
         const int Bsz = (hm.single_matern || sm != SM_NONE) ? hm.b : std::max(3, pad_b(hm.b));
-        Plan plan = make_plan(n_local, 1, Bsz, m0);
+        Plan plan = make_plan(n_local, 1, Bsz, m0, -1, g_tree_group);
         plan.geo.segL = rank > 0;
         plan.geo.segR = rank + 1 < nranks;
         std::vector<double> params(hm.rec_stride + 2, 0.0);

@@ -30,10 +30,16 @@ def lib():
         L.emu_last_error.restype = ctypes.c_char_p
         L.emu_eval_batched.argtypes = [ctypes.c_void_p, ctypes.c_int32, _d, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
                                        _d, _d, _d, ctypes.c_uint32, _d, _d, _d, _d, _i64p, ctypes.c_int64, ctypes.c_int]
+        L.emu_set_tree_group.argtypes = [ctypes.c_int64]
         L.emu_btd.argtypes = [ctypes.c_int64, ctypes.c_int32, _d, _d, _d, ctypes.c_int32, _d, _d, _d, _d, _i64p,
                               ctypes.c_int64]
         _lib = L
     return _lib
+
+
+def set_tree_group(g):
+    """Cap the records per shared-memory tree group (0 = automatic): more tree levels."""
+    lib().emu_set_tree_group(int(g))
 
 
 class EmuError(RuntimeError):

@@ -150,3 +150,57 @@ def test_segment_partition_matches_oracle(leaves, theta, P, m0):
     assert rel(g, o["grad"]) < 1e-9
     assert rel(mean, o["mean"]) < 1e-9
     assert rel(var, o["var"]) < 1e-9
+
+
+@pytest.fixture
+def tree_group():
+    yield E.set_tree_group
+    E.set_tree_group(0)
+
+
+@pytest.mark.parametrize("leaves,theta", [KERNELS[1], KERNELS[2], KERNELS[4]])
+@pytest.mark.parametrize("G", [2, 3, 4, 7, 16])
+@pytest.mark.parametrize("n,m0", [(300, 2), (257, 3), (64, 1)])
+def test_multilevel_tree_groups_match_oracle(leaves, theta, G, n, m0, tree_group):
+    """Levels >= 1 as shared-memory tree groups (tree.cuh) with a forced small group size:
+    several k_tree_fwd / k_tree_rev levels below the k_tree_one top, ragged last groups,
+    non-power-of-two groups."""
+    tree_group(G)
+    t, y = series(n + G, n)
+    e = E.evaluate(leaves, theta, t, y, 0.3, m0=m0)
+    o = O.evaluate(leaves, theta, t, y, 0.3)
+    for k, tol in (("loglik", 1e-10), ("grad", 1e-9), ("mean", 1e-9), ("var", 1e-9)):
+        if rel(e[k], o[k]) >= tol:
+            ld = O.evaluate(leaves, theta, t, y, 0.3, precision=1)
+            assert rel(e[k], ld[k]) <= max(tol, 4 * rel(o[k], ld[k])), k
+
+
+@pytest.mark.parametrize("G", [2, 5])
+def test_multilevel_tree_groups_batched(G, tree_group):
+    tree_group(G)
+    rng = np.random.default_rng(11)
+    S, n = 5, 90
+    t = np.cumsum(rng.uniform(0.5, 1.5, (S, n)) * 0.01, axis=1)
+    y = rng.standard_normal((S, n))
+    theta = np.stack([np.exp(rng.uniform(np.log(0.5), np.log(2), S)), np.exp(rng.uniform(np.log(0.5), np.log(5), S))], 1)
+    e = E.evaluate([O.MATERN52], theta, t, y, np.full(S, 0.1), var=True, mean=True, m0=2)
+    for s in range(S):
+        o = O.evaluate([O.MATERN52], theta[s], t[s], y[s], 0.1)
+        for k, tol in (("loglik", 1e-10), ("grad", 1e-9), ("mean", 1e-9), ("var", 1e-9)):
+            if rel(e[k][s], o[k]) >= tol:  # arbitrate with the long-double evaluation
+                ld = O.evaluate([O.MATERN52], theta[s], t[s], y[s], 0.1, precision=1)
+                assert rel(e[k][s], ld[k]) <= max(tol, 4 * rel(o[k], ld[k])), k
+
+
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("G", [2, 3])
+def test_segment_partition_with_tree_levels(P, G, tree_group):
+    tree_group(G)
+    leaves, theta = KERNELS[2]
+    t, y = series(91 + P, 300)
+    ll, g, mean, var = _segment_run(leaves, theta, t, y, 0.3, P, 2)
+    o = O.evaluate(leaves, theta, t, y, 0.3)
+    assert rel(ll, o["loglik"]) < 1e-10
+    assert rel(g, o["grad"]) < 1e-9
+    assert rel(mean, o["mean"]) < 1e-9
+    assert rel(var, o["var"]) < 1e-9

@@ -265,3 +265,36 @@ def test_segment_protocol_on_gpu(ctx, leaves, theta, nranks):
     ll, g, mean, var = emulate_ranks(ctx, torch, torch.device("cuda", 0), leaves, theta, t, y, 0.3,
                                      P.WANT_GRAD | P.WANT_MEAN | P.WANT_VAR, nranks)
     check({"loglik": ll, "grad": g, "mean": mean, "var": var}, leaves, theta, t, y, 0.3, TOL, factor=50.0)
+
+
+@pytest.mark.parametrize("leaves,theta", [KERNELS[2], KERNELS[4], KERNELS[6]])
+@pytest.mark.parametrize("G", [2, 3, 16])
+def test_multilevel_tree_groups(ctx, leaves, theta, G):
+    """Levels >= 1 as shared-memory tree groups with a forced small group size: a chain of
+    k_tree_fwd / k_tree_rev levels below k_tree_one, ragged and non-power-of-two groups."""
+    t, y = series(500 + G, 5000)
+    ctx.set_tree_group(G)
+    ctx.set_chunk(2)
+    try:
+        g = ctx.eval(leaves, theta, t, y, 0.3, grad=True, mean=True, var=True)
+    finally:
+        ctx.set_tree_group(0)
+        ctx.set_chunk(0)
+    check(g, leaves, theta, t, y, 0.3, TOL, factor=50.0)
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_segment_protocol_with_tree_levels(ctx, nranks):
+    import torch
+    from paper_1610_08035_b200.partition import emulate_ranks
+    leaves, theta = [P.MATERN52], [2.0, 1.5]
+    t, y = series(190 + nranks, 4000)
+    ctx.set_tree_group(3)
+    ctx.set_chunk(2)
+    try:
+        ll, g, mean, var = emulate_ranks(ctx, torch, torch.device("cuda", 0), leaves, theta, t, y, 0.3,
+                                         P.WANT_GRAD | P.WANT_MEAN | P.WANT_VAR, nranks)
+    finally:
+        ctx.set_tree_group(0)
+        ctx.set_chunk(0)
+    check({"loglik": ll, "grad": g, "mean": mean, "var": var}, leaves, theta, t, y, 0.3, TOL, factor=50.0)

@@ -14,7 +14,11 @@ for rep in range(3):
     ctx.set_phase_stamps(st.data_ptr() if rep == 2 else 0)
     ctx.eval_device(w.leaves, w.theta, dt.data_ptr(), dy.data_ptr(), len(w.t), w.sigma, P.WANT_GRAD, ll.data_ptr(), g.data_ptr(), 0, 0)
     torch.cuda.synchronize()
-s = st.cpu().numpy()
-k = int(np.count_nonzero(s))
-d = np.diff(s[:k]) / 1e3
-print("phases", k - 1, "us:", np.round(d, 2), "total", round(float(d.sum()), 1))
+s = st.cpu().numpy().astype(np.int64)
+for name, lo, hi in (("k_tree_fwd", 0, 16), ("k_tree_one", 16, 48), ("k_tree_rev", 48, 64)):
+    v = s[lo:hi]
+    k = int(np.count_nonzero(v))
+    if k > 1:
+        d = np.diff(v[:k]) / 1e3
+        print(name, "phases", k - 1, "us:", np.round(d, 2), "total", round(float(d.sum()), 1))
+
