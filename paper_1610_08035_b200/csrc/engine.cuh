@@ -904,7 +904,15 @@ SP_UNROLL
 SP_UNROLL
             for (int j = 0; j < B; ++j)
                 E[i * B + j] = Ccc[i * B + j] - X[i * B + j] - X[j * B + i] + Z[i * B + j] + e[i] * e[j];
-        mmt<B>(Y, Cpp, Phi);
+        // C_pp Φ^T = (Φ C_pp)^T exactly (C_pp is symmetrised): transpose instead of a product
+SP_UNROLL
+        for (int i = 0; i < B; ++i)
+SP_UNROLL
+            for (int j = 0; j < i; ++j) {
+                const double t2 = Y[i * B + j];
+                Y[i * B + j] = Y[j * B + i];
+                Y[j * B + i] = t2;
+            }
 SP_UNROLL
         for (int i = 0; i < B; ++i)
 SP_UNROLL

@@ -190,9 +190,9 @@ HostModel build_model(const spingp_leaf* leaves, int32_t n_leaves, int32_t n_the
     for (int l = 0; l < n_leaves; ++l) {
         d.rec[l] = rec;
         switch (leaves[l].type) {
-            case SPINGP_MATERN12: case SPINGP_MATERN32: case SPINGP_MATERN52: rec += 3; break;
-            case SPINGP_EQ: rec += 2; break;
-            case SPINGP_QP: rec += 5 + 2 * (leaves[l].order + 1); break;
+            case SPINGP_MATERN12: case SPINGP_MATERN32: case SPINGP_MATERN52: rec += 5; break;  // var, len, lam, 1/len, 1/var
+            case SPINGP_EQ: rec += 4; break;  // var, len, 1/len, 1/var
+            case SPINGP_QP: rec += 7 + 2 * (leaves[l].order + 1); break;  // + 1/env, w0/period
         }
         d.eqc[l] = 0;
         if (leaves[l].type == SPINGP_EQ) {
@@ -238,6 +238,7 @@ void fill_record(const HostModel& hm, const double* theta, double sigma, double*
                                    : d.type[l] == MATERN32 ? std::sqrt(3.0) / len
                                                            : std::sqrt(5.0) / len;
                 lr[0] = var; lr[1] = len; lr[2] = lam;
+                lr[3] = 1.0 / len; lr[4] = 1.0 / var;  // the per-step gradient needs no division
                 // Pinf diagonal: var * (1, lam^2, lam^4 / ...) as in kernels.hpp:137-200
                 double pd[3] = {var, 0.0, 0.0};
                 if (d.type[l] == MATERN32) pd[1] = var * lam * lam;
@@ -254,6 +255,7 @@ void fill_record(const HostModel& hm, const double* theta, double sigma, double*
             }
             case EQ: {
                 lr[0] = var; lr[1] = len;
+                lr[2] = 1.0 / len; lr[3] = 1.0 / var;
                 const int J = d.dim[l];
                 const double* P1 = hm.eqconst.data() + d.eqc[l] + J;
                 for (int i = 0; i < J; ++i) {
@@ -267,6 +269,8 @@ void fill_record(const HostModel& hm, const double* theta, double sigma, double*
                 const int J = d.order[l];
                 lr[0] = var; lr[1] = len; lr[2] = period; lr[3] = env;
                 lr[4] = 2.0 * std::numbers::pi / period;
+                lr[5 + 2 * (J + 1)] = 1.0 / env;        // per-step code multiplies, never divides
+                lr[5 + 2 * (J + 1) + 1] = lr[4] / period;
                 const double x = 1.0 / (len * len), ex = std::exp(-x);
                 for (int j = 0; j <= J; ++j) {
                     const double cj = j == 0 ? 1.0 : 2.0;

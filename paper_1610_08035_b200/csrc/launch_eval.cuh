@@ -148,6 +148,48 @@ void launch_tree(spingp_ctx* ctx, TreeKind kind, TreeArgs& ta) {
     ctx->launched(kind == TREE_FWD ? "k_tree_fwd" : kind == TREE_REV ? "k_tree_rev" : "k_tree_one");
 }
 
+// Levels L-1 and L (= nlev-1, one group per series) as one cooperative launch when
+// every level-(L-1) group gets a co-resident CTA and the top group fits the
+// separator area (SPINGP_TREE_COOP=0 disables).
+template <int B>
+bool launch_tree_coop(spingp_ctx* ctx, TreeArgs& a1, TreeArgs& a2) {
+    using TR = Tree<B>;
+    static const bool enabled = [] {
+        const char* e = std::getenv("SPINGP_TREE_COOP");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    if (!enabled) return false;
+    const size_t smem = 8 * (static_cast<size_t>(TR::NR) * a1.RS + static_cast<size_t>(TR::NS) * a1.ES);
+    if (static_cast<size_t>(TR::NR) * a2.RS + static_cast<size_t>(TR::NS) * a2.ES >
+        static_cast<size_t>(TR::NS) * a1.ES)
+        return false;
+    const int half = std::min(a1.G, static_cast<int>(a1.RS)) / 2 + 1;
+    const int half2 = static_cast<int>(a2.RS) / 2 + 1;
+    const int tpb = std::min(kTreeMaxThreads, std::max(32, (std::max(half, half2) + 31) / 32 * 32));
+    if ((a2.RS + 1) / 2 > tpb) return false;
+    static int set = 0;
+    if (!set) {
+        CUDA_OK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_tree_coop<B>),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(tree_smem_bytes(B, tree_group_size(B)))));
+        set = 1;
+    }
+    int per = 0, dev = 0, sms = 0;
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tree_coop<B>, tpb, smem));
+    CUDA_OK(cudaGetDevice(&dev));
+    CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const long long groups = static_cast<long long>(a1.S) * a1.nG;
+    if (groups > static_cast<long long>(per) * sms) return false;
+    a1.stamps = ctx->upper_stamps;
+    a2.stamps = nullptr;
+    void* args[] = {&a1, &a2};
+    ctx->pre();
+    CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_tree_coop<B>), dim3(static_cast<unsigned>(groups)),
+                                        dim3(tpb), args, smem, ctx->stream));
+    ctx->launched("k_tree_coop");
+    return true;
+}
+
 template <class T>
 void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     constexpr int B = T::B;
@@ -179,6 +221,7 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     }
     const long long SK0 = g.K[0] * g.S;
     const bool tree = a.plan->tree;
+    bool coop = false;  // top two tree levels in one cooperative launch
     const bool fused = upper_fused();
     if (a.mode != 3) {
         ctx->pre();
@@ -186,9 +229,24 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
                                                                  eb.rec[0], eb.part, ctx->d_status, halo);
         ctx->launched("k_fwd0");
         if (tree) {
-            // mode 0: the last level (one group per series) is k_tree_one below
+            // mode 0: the last level (one group per series) is k_tree_one, or the two
+            // top levels k_tree_coop, below
+            coop = a.mode == 0 && g.nlev >= 3;
+            if (coop) {
+                TreeArgs t1 = tree_args<B>(ctx, g, eb, g.nlev - 2, needC);
+                TreeArgs t2 = tree_args<B>(ctx, g, eb, g.nlev - 1, needC);
+                const int lowf = g.nlev - 3;
+                for (int l = 1; l <= lowf; ++l) {
+                    TreeArgs ta = tree_args<B>(ctx, g, eb, l, needC);
+                    launch_tree<B>(ctx, TREE_FWD, ta);
+                }
+                coop = launch_tree_coop<B>(ctx, t1, t2);
+                if (!coop) {
+                    launch_tree<B>(ctx, TREE_FWD, t1);
+                }
+            }
             const int lastf = a.mode == 0 ? g.nlev - 2 : g.nlev - 1;
-            for (int l = 1; l <= lastf; ++l) {
+            for (int l = (a.mode == 0 && g.nlev >= 3) ? lastf + 1 : 1; l <= lastf; ++l) {
                 TreeArgs ta = tree_args<B>(ctx, g, eb, l, needC);
                 launch_tree<B>(ctx, TREE_FWD, ta);
             }
@@ -215,7 +273,9 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     }
     if (tree) {
         int l = g.nlev - 1;
-        if (a.mode == 0) {
+        if (coop) {
+            l = g.nlev - 3;
+        } else if (a.mode == 0) {
             TreeArgs ta = tree_args<B>(ctx, g, eb, l, needC);
             launch_tree<B>(ctx, TREE_ONE, ta);
             --l;

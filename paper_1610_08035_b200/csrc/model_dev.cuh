@@ -225,8 +225,9 @@ SP_DEV void matern_grad(const double* lr, double dt, int o, const double* Phi, c
             Qb[i * D + j] = Q[(o + i) * LD + o + j];
         }
     // d/dvar: dΦ = 0, dQ = Q / var (also at the anchor, where Q = Pinf)
-    const double ilen = 1.0 / len;  // the step's only divisions: 1/ℓ and 1/var
-    gvar += 0.5 * mtrprod<D>(Mb, Qb) * (1.0 / var);
+    (void)len;
+    const double ilen = lr[3];  // 1/ℓ and 1/var come with the record (no per-step division)
+    gvar += 0.5 * mtrprod<D>(Mb, Qb) * lr[4];
     // d/dℓ = -(λ/ℓ) d/dλ.  dQ/dλ_ij = ((i+j)/λ) Q_ij + var Δt q1 (T v)_i (T v)_j
     double dQ[D * D];
     const double c = -lam * ilen;
@@ -321,7 +322,7 @@ SP_DEV void eq_block(int o, int J, const double* ac, const double* lr, double dt
     }
     for (int i = 0; i < J; ++i)
         for (int j = 0; j < J; ++j) Phi[(o + i) * LD + o + j] = 0.0;
-    const double tau = dt / len;
+    const double tau = dt * lr[2];  // dt / len
     for (int p = 0; p < J / 2; ++p) {
         const double a = ac[2 * p], c = ac[2 * p + 1];
         const double rho = exp(a * tau);
@@ -363,39 +364,41 @@ SP_DEV void eq_grad(int o, int J, const double* ac, const double* lr, double dt,
     double s = 0.0;
     for (int i = 0; i < J; ++i)
         for (int k = 0; k < J; ++k) s += M[(o + i) * LD + o + k] * Q[(o + k) * LD + o + i];
-    gvar += 0.5 * s / var;
+    const double ilen = lr[2], ivar = lr[3];
+    gvar += 0.5 * s * ivar;
     if (dt < 0.0) return;  // dPinf/dℓ = 0 and dΦ = 0 at the anchor
-    const double tau = dt / len;
+    const double tau = dt * ilen;
     // dQ/dℓ = -var s0 (Δt/ℓ²) z z^T with z = e^{Aτ} g: pair p -> e^{a τ} [cos(cτ), -sin(cτ)]
+    double z0[kMaxB / 2], z1[kMaxB / 2];
+    for (int p = 0; p < J / 2; ++p) {
+        const double rho = exp(ac[2 * p] * tau);
+        double sn, cs;
+        sincos(ac[2 * p + 1] * tau, &sn, &cs);
+        z0[p] = rho * cs;
+        z1[p] = -rho * sn;
+    }
     double tq = 0.0, tb = 0.0;
+    const double cdt = -dt * ilen;
     for (int p = 0; p < J / 2; ++p) {
         const double a = ac[2 * p], c = ac[2 * p + 1];
         const int k = o + 2 * p;
-        const double rho = exp(a * tau);
-        double sn, cs;
-        sincos(c * tau, &sn, &cs);
-        const double zp0 = rho * cs, zp1 = -rho * sn;
+        const double zp0 = z0[p], zp1 = z1[p];
         for (int q = 0; q < J / 2; ++q) {
-            const double aq = ac[2 * q], cq = ac[2 * q + 1];
             const int kq = o + 2 * q;
-            const double rq = exp(aq * tau);
-            double snq, csq;
-            sincos(cq * tau, &snq, &csq);
-            const double zq0 = rq * csq, zq1 = -rq * snq;
+            const double zq0 = z0[q], zq1 = z1[q];
             tq += M[kq * LD + k] * zp0 * zq0 + M[(kq + 1) * LD + k] * zp0 * zq1 +
                   M[kq * LD + k + 1] * zp1 * zq0 + M[(kq + 1) * LD + k + 1] * zp1 * zq1;
         }
         // dΦ = -(Δt/ℓ) F Φ on the 2x2 block
-        const double f00 = a / len, f01 = c / len, f10 = -c / len, f11 = a / len;
+        const double f00 = a * ilen, f01 = c * ilen, f10 = -c * ilen, f11 = a * ilen;
         const double p00 = Phi[k * LD + k], p01 = Phi[k * LD + k + 1];
         const double p10 = Phi[(k + 1) * LD + k], p11 = Phi[(k + 1) * LD + k + 1];
-        const double cdt = -dt / len;
         const double d00 = cdt * (f00 * p00 + f01 * p10), d01 = cdt * (f00 * p01 + f01 * p11);
         const double d10 = cdt * (f10 * p00 + f11 * p10), d11 = cdt * (f10 * p01 + f11 * p11);
         tb += d00 * Bm[k * LD + k] + d01 * Bm[(k + 1) * LD + k] + d10 * Bm[k * LD + k + 1] +
               d11 * Bm[(k + 1) * LD + k + 1];
     }
-    glen += 0.5 * (-var * s0 * dt / (len * len)) * tq + tb;
+    glen += 0.5 * (-var * s0 * dt * ilen * ilen) * tq + tb;
 }
 
 // ---------------------------------------------------------------------- QP --
@@ -409,13 +412,21 @@ SP_DEV void qp_block(int o, int J, const double* lr, double dt, double* Phi, dou
             Phi[(o + i) * LD + o + j] = 0.0;
             Q[(o + i) * LD + o + j] = 0.0;
         }
-    const double rho = dt < 0.0 ? 0.0 : exp(-dt / env);
-    const double one_m = dt < 0.0 ? 1.0 : -expm1(-2.0 * dt / env);
+    (void)env;
+    const double ienv = lr[5 + 2 * (J + 1)];
+    const double rho = dt < 0.0 ? 0.0 : exp(-dt * ienv);
+    const double one_m = dt < 0.0 ? 1.0 : -expm1(-2.0 * dt * ienv);
+    // harmonics by the angle-addition recurrence from one sincos (error ~ j ulp, j <= 15)
+    double s1 = 0.0, c1 = 1.0, sn = 0.0, cs = 1.0;
+    if (dt >= 0.0) sincos(w0 * dt, &s1, &c1);
     for (int j = 0; j <= J; ++j) {
         const int k = o + 2 * j;
+        if (j > 0) {
+            const double cn = cs * c1 - sn * s1;
+            sn = sn * c1 + cs * s1;
+            cs = cn;
+        }
         if (dt >= 0.0) {
-            double sn, cs;
-            sincos(double(j) * w0 * dt, &sn, &cs);
             Phi[k * LD + k] = rho * cs;
             Phi[k * LD + k + 1] = -rho * sn;
             Phi[(k + 1) * LD + k] = rho * sn;
@@ -431,11 +442,12 @@ SP_DEV void qp_block(int o, int J, const double* lr, double dt, double* Phi, dou
 template <int LD>
 SP_DEV void qp_grad(int o, int J, const double* lr, double dt, const double* Phi, const double* M,
                     const double* Bm, double* g4) {
-    const double var = lr[0], period = lr[2], env = lr[3], w0 = lr[4];
+    const double var = lr[0];
     const double* q2 = lr + 5;
     const double* dq2 = lr + 5 + (J + 1);
-    const double rho2 = dt < 0.0 ? 0.0 : exp(-2.0 * dt / env);
-    const double one_m = dt < 0.0 ? 1.0 : -expm1(-2.0 * dt / env);
+    const double ienv = lr[5 + 2 * (J + 1)], dwp = lr[5 + 2 * (J + 1) + 1];  // 1/env, w0/period
+    const double rho2 = dt < 0.0 ? 0.0 : exp(-2.0 * dt * ienv);
+    const double one_m = dt < 0.0 ? 1.0 : -expm1(-2.0 * dt * ienv);
     for (int j = 0; j <= J; ++j) {
         const int k = o + 2 * j;
         const double trM = M[k * LD + k] + M[(k + 1) * LD + k + 1];
@@ -443,13 +455,13 @@ SP_DEV void qp_grad(int o, int J, const double* lr, double dt, const double* Phi
         g4[1] += 0.5 * trM * var * dq2[j] * one_m;  // dQ/dlen = var dq2 (1 - ρ²) I
         if (dt < 0.0) continue;
         // env: dΦ = (Δt/env²) Φ ; dQ = -2 var q2 (Δt/env²) ρ² I
-        const double ce = dt / (env * env);
+        const double ce = dt * ienv * ienv;
         const double trPB = Phi[k * LD + k] * Bm[k * LD + k] + Phi[k * LD + k + 1] * Bm[(k + 1) * LD + k] +
                             Phi[(k + 1) * LD + k] * Bm[k * LD + k + 1] +
                             Phi[(k + 1) * LD + k + 1] * Bm[(k + 1) * LD + k + 1];
         g4[3] += 0.5 * trM * (-2.0 * var * q2[j] * ce * rho2) + ce * trPB;
         // period: dF = j dω [[0,-1],[1,0]], dω = -ω0/period; dΦ = Δt dF Φ; dQ = 0
-        const double s = double(j) * (-w0 / period) * dt;
+        const double s = double(j) * (-dwp) * dt;
         // dΦ = s * [[-Φ10, -Φ11], [Φ00, Φ01]]
         const double d00 = -s * Phi[(k + 1) * LD + k], d01 = -s * Phi[(k + 1) * LD + k + 1];
         const double d10 = s * Phi[k * LD + k], d11 = s * Phi[k * LD + k + 1];

@@ -464,6 +464,83 @@ __global__ void __launch_bounds__(kTreeMaxThreads) k_tree_one(TreeArgs a) {
     tree_store_rev<B>(a, t, E, threadIdx.x, blockDim.x);
     tree_stamp(a, ks);
 }
+
+// The two top levels in one cooperative launch (one CTA per level-(L-1) group, all
+// co-resident):  A) every CTA reduces its group, keeping the merge factors in shared
+// memory, and publishes its group record;  grid barrier;  B) the first CTA of each
+// series reduces the series' group records (the top group, staged in its separator
+// area, which is still free), inverts the top block and runs the top reverse tree,
+// publishing the group boundaries' separators;  grid barrier;  C) every CTA loads its
+// two boundary separators and runs its reverse tree from the factors it kept.
+// Saves the factor store/reload of k_tree_fwd/k_tree_rev, the reload of k_tree_one
+// and two launch boundaries.  a1 = level L-1 (many groups), a2 = level L (one group
+// per series); the top group's capacity must fit a1's separator area.
+template <int B>
+SP_DEV void tree_load_recs_cg(const TreeArgs& a, const TreeGroup& t, double* R, int tid, int nt) {
+    using TR = Tree<B>;  // records written by other CTAs before a grid barrier: L2 loads
+    const double* src = a.rec_in + static_cast<long long>(t.s) * a.nin + t.k0;
+    constexpr int CB = 8;
+    for (int i = tid; i < t.cnt; i += nt)
+        for (int c0 = 0; c0 < TR::NR; c0 += CB) {
+            double v[CB];
+TR_UNROLL
+            for (int c = 0; c < CB; ++c)
+                if (c0 + c < TR::NR) v[c] = __ldcg(src + (c0 + c) * a.SKin + i);
+TR_UNROLL
+            for (int c = 0; c < CB; ++c)
+                if (c0 + c < TR::NR) R[(c0 + c) * a.RS + i] = v[c];
+        }
+}
+template <int B>
+__global__ void __launch_bounds__(kTreeMaxThreads) k_tree_coop(TreeArgs a1, TreeArgs a2) {
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    using TR = Tree<B>;
+    extern __shared__ double2 tsm2[];
+    double* R = reinterpret_cast<double*>(tsm2);
+    double* E = R + static_cast<long long>(TR::NR) * a1.RS;
+    const TreeGroup t = tree_group(a1, blockIdx.x);
+    const int tid = threadIdx.x, nt = blockDim.x;
+    int ks = 0;
+    tree_stamp(a1, ks);
+    tree_load_recs<B>(a1, t, R, tid, nt);
+    __syncthreads();
+    tree_stamp(a1, ks);
+    tree_forward_rounds<B>(R, a1.RS, a1, t, ks);
+    {
+        const long long SKo = static_cast<long long>(a1.S) * a1.nG;
+        for (int c = tid; c < TR::NR; c += nt) a1.rec_out[c * SKo + t.gidx] = R[c * a1.RS];
+    }
+    grid.sync();
+    tree_stamp(a1, ks);
+    if (t.j == 0) {  // the series' top group, staged in this CTA's separator area
+        const TreeGroup t2 = tree_group(a2, t.s);
+        double* R2 = E;
+        double* E2 = R2 + static_cast<long long>(TR::NR) * a2.RS;
+        int ks2 = 0;
+        tree_load_recs_cg<B>(a2, t2, R2, tid, nt);
+        __syncthreads();
+        tree_forward_rounds<B>(R2, a2.RS, a2, t2, ks2);
+        if (tid == 0) tree_top<B>(a2, t2, R2, E2);
+        __syncthreads();
+        tree_reverse_rounds<B>(R2, E2, a2, t2, ks2);
+        tree_store_rev<B>(a2, t2, E2, tid, nt);
+    }
+    grid.sync();
+    tree_stamp(a1, ks);
+    {  // boundary separators of this group (written by the top CTA)
+        const long long SnU = static_cast<long long>(a1.S) * (a1.nG + a1.segL);
+        const long long u = static_cast<long long>(t.s) * (a1.nG + a1.segL) + a1.segL + t.j;
+        for (int q = tid; q < TR::NS; q += nt) {
+            const bool want = q < B || a1.needC;
+            E[q * a1.ES + 1] = (want && q < TR::SCU) ? __ldcg(a1.solU + q * SnU + u) : 0.0;
+            E[q * a1.ES] = (want && t.hasL) ? __ldcg(a1.solU + q * SnU + u - 1) : 0.0;
+        }
+    }
+    __syncthreads();
+    tree_reverse_rounds<B>(R, E, a1, t, ks);
+    tree_store_rev<B>(a1, t, E, tid, nt);
+    tree_stamp(a1, ks);
+}
 #endif
 
 }  // namespace spingp_dev
