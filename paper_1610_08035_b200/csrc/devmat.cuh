@@ -13,7 +13,13 @@
 
 namespace spingp_dev {
 
+// SP_DEV_NOINLINE (experiment for the b >= 6 builds): every block
+// routine becomes a real call with its own frame instead of being inlined.
+#ifdef SP_DEV_NOINLINE
+#define SP_DEV __device__ __noinline__ inline
+#else
 #define SP_DEV __device__ __forceinline__
+#endif
 // Loop-unrolling hint for the b x b loops.  Deliberately empty: nvcc fully
 // unrolls the constant-trip loops of the register-resident sizes (b <= 4) on
 // its own, and an explicit `#pragma unroll (B <= 4 ? 64 : 1)` was measured to

@@ -1031,7 +1031,7 @@ SP_UNROLL
 //            sums seg[s][0..nseg) the same way and writes loglik / gradient (or, in
 //            segment mode, the raw partial sums).
 // The log-determinant of the whole precision is toplogdet[s] (cumulative records).
-constexpr int kSeg = 1024;
+constexpr int kSeg = 256;  // chunks per stage-1 block (cfg2: 280 blocks)
 constexpr int kRedThreads = 256;
 constexpr int kMaxNC = P_GRAD + kMaxTheta;
 
