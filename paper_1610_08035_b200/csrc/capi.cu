@@ -7,6 +7,8 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "ctx.hpp"
@@ -23,10 +25,13 @@ std::string& last_error() {
 
 
 int take_status(spingp_ctx* ctx, int64_t* fail_block) {
-    unsigned long long h = 0;
+    // status word -> pinned host slot and reset, both stream-ordered; one synchronisation
+    if (!ctx->h_status) CUDA_OK(cudaMallocHost(&ctx->h_status, sizeof(unsigned long long)));
+    CUDA_OK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    CUDA_OK(cudaMemsetAsync(ctx->d_status, 0xFF, sizeof(unsigned long long), ctx->stream));
     CUDA_OK(cudaStreamSynchronize(ctx->stream));
-    CUDA_OK(cudaMemcpy(&h, ctx->d_status, sizeof h, cudaMemcpyDeviceToHost));
-    CUDA_OK(cudaMemset(ctx->d_status, 0xFF, sizeof(unsigned long long)));
+    const unsigned long long h = *ctx->h_status;
     if (h == ~0ULL) return SPINGP_OK;
     if (fail_block) *fail_block = static_cast<int64_t>((h >> 4) & ((1ULL << 56) - 1));
     const int code = static_cast<int>(h & 15ULL);
@@ -141,6 +146,30 @@ int spingp_seg_sizes(const spingp_leaf* leaves, int32_t n_leaves, int32_t* n_rec
     });
 }
 
+// build_model for a ctx, reusing the last result while the structure repeats (call with
+// ctx->mu held)
+static const HostModel& ctx_model(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves, int32_t n_theta) {
+    std::vector<int32_t> key{n_leaves, n_theta};
+    for (int32_t l = 0; l < n_leaves && leaves; ++l) {
+        key.push_back(static_cast<int32_t>(leaves[l].type));
+        key.push_back(leaves[l].order);
+    }
+    if (key != ctx->model_key || ctx->model_key.empty()) {
+        ctx->model = build_model(leaves, n_leaves, n_theta);
+        ctx->model_key = std::move(key);
+    }
+    return ctx->model;
+}
+
+// SPINGP_PIPELINE=0 disables host-input pipelining (A/B knob)
+static bool pipeline_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SPINGP_PIPELINE");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    return on;
+}
+
 static int seg_run(spingp_ctx* ctx, int mode, const spingp_leaf* leaves, int32_t n_leaves, const double* theta,
                    int32_t n_theta, const double* d_t, const double* d_y, int64_t n_local, double t_left,
                    double t_right, int32_t rank, int32_t nranks, double sigma, uint32_t flags,
@@ -152,7 +181,7 @@ static int seg_run(spingp_ctx* ctx, int mode, const spingp_leaf* leaves, int32_t
         if (rank > 0 && !(t_left < 0.0 || t_left >= 0.0)) throw std::invalid_argument("missing left halo time");
         if (rank + 1 < nranks && !(t_right < 0.0 || t_right >= 0.0)) throw std::invalid_argument("missing right halo time");
         std::lock_guard<std::mutex> lk(ctx->mu);
-        const HostModel hm = build_model(leaves, n_leaves, n_theta);
+        const HostModel& hm = ctx_model(ctx, leaves, n_leaves, n_theta);
         Plan plan = make_plan(n_local, 1, plan_bsize(hm), ctx->m0_override, -1, ctx->g_override);
         plan.geo.segL = rank > 0 ? 1 : 0;
         plan.geo.segR = rank + 1 < nranks ? 1 : 0;
@@ -223,6 +252,12 @@ int spingp_ctx_destroy(spingp_ctx* ctx) {
         if (ctx->stage_ev[k]) cudaEventDestroy(ctx->stage_ev[k]);
     }
     for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->h_status) cudaFreeHost(ctx->h_status);
+    if (ctx->copy_stream) {
+        cudaStreamSynchronize(ctx->copy_stream);
+        for (cudaEvent_t e : ctx->pipe_ev) cudaEventDestroy(e);
+        cudaStreamDestroy(ctx->copy_stream);
+    }
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return SPINGP_OK;
@@ -326,7 +361,7 @@ int spingp_eval_batched_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32
         if ((flags & SPINGP_WANT_MEAN) && !d_mean) throw std::invalid_argument("mean output is null");
         if ((flags & SPINGP_WANT_VAR) && !d_var) throw std::invalid_argument("variance output is null");
         std::lock_guard<std::mutex> lk(ctx->mu);
-        const HostModel hm = build_model(leaves, n_leaves, n_theta);
+        const HostModel& hm = ctx_model(ctx, leaves, n_leaves, n_theta);
         const Plan plan = make_plan(n, S, plan_bsize(hm), ctx->m0_override, -1, ctx->g_override);
         std::vector<double> params(static_cast<size_t>(S) * hm.rec_stride, 0.0);
         for (int64_t s = 0; s < S; ++s)
@@ -346,6 +381,91 @@ int spingp_eval_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_lea
                                       flags, d_loglik, d_grad, d_mean, d_var);
 }
 
+// Host-input pipelining for one long series (S = 1, n >= kPipeMin): the H2D of t, y runs
+// on a copy stream in kPipeIn pieces of level-0 chunks and k_fwd0 starts on each piece as
+// soon as it has landed; k_rev0 runs in kPipeOut pieces and each piece's mean/var is copied
+// back while the next piece computes.  Results are identical to the unpipelined call (the
+// kernels and their per-chunk arithmetic do not change; only launch boundaries do).
+constexpr int64_t kPipeMin = 1 << 18;
+constexpr int kPipeIn = 4, kPipeOut = 2;
+
+static int eval_host_pipelined(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves, const double* theta,
+                               int32_t n_theta, int64_t n, const double* t, const double* y, double sigma,
+                               uint32_t flags, double* out_loglik, double* out_grad, double* out_mean,
+                               double* out_var, int64_t* fail_block) {
+    static thread_local DeviceVec dbuf;
+    const size_t nt1 = static_cast<size_t>(n_theta) + 1;
+    const size_t ng = (flags & SPINGP_WANT_GRAD) ? nt1 : 0;
+    const size_t nm = (flags & SPINGP_WANT_MEAN) ? n : 0;
+    const size_t nv = (flags & SPINGP_WANT_VAR) ? n : 0;
+    double* base = dbuf.get(2 * static_cast<size_t>(n) + 1 + ng + nm + nv);
+    double* d_t = base;
+    double* d_y = d_t + n;
+    double* d_ll = d_y + n;
+    double* d_g = d_ll + 1;
+    double* d_m = d_g + ng;
+    double* d_v = d_m + nm;
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        const HostModel& hm = ctx_model(ctx, leaves, n_leaves, n_theta);
+        const Plan plan = make_plan(n, 1, plan_bsize(hm), ctx->m0_override, -1, ctx->g_override);
+        std::vector<double> params(hm.rec_stride, 0.0);
+        fill_record(hm, theta, sigma, params.data());
+        const long long K0 = plan.geo.K[0], m0 = plan.geo.m[0];
+        long long ic[kPipeIn + 1], oc[kPipeOut + 1];
+        for (int p = 0; p <= kPipeIn; ++p) ic[p] = K0 * p / kPipeIn;
+        for (int q = 0; q <= kPipeOut; ++q) oc[q] = K0 * q / kPipeOut;
+        if (!ctx->copy_stream) {
+            CUDA_OK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+            for (auto& e : ctx->pipe_ev) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        cudaEvent_t* in_ev = ctx->pipe_ev;
+        cudaEvent_t* out_ev = ctx->pipe_ev + kPipeIn;
+        cudaEvent_t ev_start = ctx->pipe_ev[kPipeIn + kPipeOut], ev_done = ctx->pipe_ev[kPipeIn + kPipeOut + 1];
+        cudaStream_t cs = ctx->copy_stream;
+        CUDA_OK(cudaEventRecord(ev_start, ctx->stream));  // earlier work on d_t, d_y is done first
+        CUDA_OK(cudaStreamWaitEvent(cs, ev_start, 0));
+        for (int p = 0; p < kPipeIn; ++p) {
+            // piece p: the points of its chunks plus the next time (the last separator's step)
+            const long long lo = ic[p] * m0, hi = std::min<long long>(n, ic[p + 1] * m0 + 1);
+            if (hi > lo) {
+                CUDA_OK(cudaMemcpyAsync(d_t + lo, t + lo, (hi - lo) * sizeof(double), cudaMemcpyHostToDevice, cs));
+                CUDA_OK(cudaMemcpyAsync(d_y + lo, y + lo, (hi - lo) * sizeof(double), cudaMemcpyHostToDevice, cs));
+            }
+            CUDA_OK(cudaEventRecord(in_ev[p], cs));
+        }
+        EvalArgs a{&hm, &plan, params.data(), params.size(), d_t, d_y, flags, d_ll, d_g, d_m, d_v,
+                   0, nullptr, nullptr, nullptr};
+        a.in_pieces = kPipeIn;
+        a.in_chunk = ic;
+        a.in_ready = in_ev;
+        if (nm || nv) {
+            a.out_pieces = kPipeOut;
+            a.out_chunk = oc;
+            a.out_ready = out_ev;
+        }
+        dispatch_eval(ctx, a);
+        if (nm || nv) {
+            for (int q = 0; q < kPipeOut; ++q) {
+                const long long lo = oc[q] * m0, hi = std::min<long long>(n, oc[q + 1] * m0);
+                CUDA_OK(cudaStreamWaitEvent(cs, out_ev[q], 0));
+                if (hi <= lo) continue;
+                if (nm)
+                    CUDA_OK(cudaMemcpyAsync(out_mean + lo, d_m + lo, (hi - lo) * sizeof(double),
+                                            cudaMemcpyDeviceToHost, cs));
+                if (nv)
+                    CUDA_OK(cudaMemcpyAsync(out_var + lo, d_v + lo, (hi - lo) * sizeof(double),
+                                            cudaMemcpyDeviceToHost, cs));
+            }
+        }
+        CUDA_OK(cudaEventRecord(ev_done, cs));
+        CUDA_OK(cudaMemcpyAsync(out_loglik, d_ll, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        if (ng) CUDA_OK(cudaMemcpyAsync(out_grad, d_g, ng * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_OK(cudaStreamWaitEvent(ctx->stream, ev_done, 0));
+        return take_status(ctx, fail_block);
+    }
+}
+
 int spingp_eval_batched(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
                         const double* theta, int32_t n_theta, int64_t S, int64_t n, const double* t,
                         const double* y, const double* sigma, uint32_t flags, double* out_loglik,
@@ -356,6 +476,10 @@ int spingp_eval_batched(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_le
         if ((flags & SPINGP_WANT_GRAD) && !out_grad) throw std::invalid_argument("gradient output is null");
         if ((flags & SPINGP_WANT_MEAN) && !out_mean) throw std::invalid_argument("mean output is null");
         if ((flags & SPINGP_WANT_VAR) && !out_var) throw std::invalid_argument("variance output is null");
+        if (!sigma) throw std::invalid_argument("null argument");
+        if (S == 1 && n >= kPipeMin && pipeline_enabled())
+            return eval_host_pipelined(ctx, leaves, n_leaves, theta, n_theta, n, t, y, sigma[0], flags, out_loglik,
+                                       out_grad, out_mean, out_var, fail_block);
         static thread_local DeviceVec dbuf;
         const size_t N = static_cast<size_t>(S) * n;
         const size_t nt1 = static_cast<size_t>(n_theta) + 1;
@@ -402,7 +526,7 @@ int spingp_assemble(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves
         checked(ctx);
         if (!t || !y || !diag || n < 1) throw std::invalid_argument("bad argument");
         std::lock_guard<std::mutex> lk(ctx->mu);
-        const HostModel hm = build_model(leaves, n_leaves, n_theta);
+        const HostModel& hm = ctx_model(ctx, leaves, n_leaves, n_theta);
         const int b = hm.b;
         static thread_local DeviceVec dbuf;
         const size_t nd = static_cast<size_t>(n) * b * b, nu = static_cast<size_t>(n > 1 ? n - 1 : 0) * b * b;

@@ -72,6 +72,7 @@ struct spingp_ctx {
     bool own_stream = false;
     spingp_host::Arena ws;
     unsigned long long* d_status = nullptr;
+    unsigned long long* h_status = nullptr;  // pinned landing slot of the status word
     double* h_stage[2] = {nullptr, nullptr};
     size_t h_stage_cap[2] = {0, 0};
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
@@ -79,6 +80,13 @@ struct spingp_ctx {
     int64_t launches = 0;
     int64_t m0_override = 0;  // testing knob: force the level-0 chunk length
     int64_t g_override = 0;   // testing knob: force a smaller tree group (more tree levels)
+    // last model built (build_model is per-structure host work: EQ roots in long double,
+    // the reference state_space_of); reused while the leaves and theta count repeat
+    std::vector<int32_t> model_key;
+    spingp_host::HostModel model;
+    // host-input pipelining: copy stream + events (created on first use)
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t pipe_ev[16] = {};
     std::mutex mu;
     // optional per-launch CUDA-event timing (spingp_ctx_set_profiling)
     bool profiling = false;
@@ -196,6 +204,16 @@ struct EvalArgs {
     int rank = 0, nranks = 1;
     const double* d_seg_in = nullptr;
     double* d_seg_out = nullptr;
+    // host-input pipelining (spingp_eval_batched, S = 1): k_fwd0 runs in pieces of level-0
+    // chunks [in_chunk[p], in_chunk[p+1]), each after in_ready[p] (its inputs' H2D);
+    // k_rev0 runs in pieces [out_chunk[q], out_chunk[q+1]) and records out_ready[q]
+    // after each (its points' mean/var may then be copied back)
+    int in_pieces = 0;
+    const long long* in_chunk = nullptr;
+    const cudaEvent_t* in_ready = nullptr;
+    int out_pieces = 0;
+    const long long* out_chunk = nullptr;
+    const cudaEvent_t* out_ready = nullptr;
 };
 // one translation unit per instantiation (inst_*.cu, btd_b*.cu) so they build in parallel
 void eval_matern_1(spingp_ctx* ctx, const EvalArgs& a);

@@ -249,11 +249,12 @@ __global__ void __launch_bounds__(128, SP_FWD0_MINB) k_fwd0(ModelDesc md, const 
                                               double* __restrict__ fac, double* __restrict__ rec,
                                               double* __restrict__ part,
                                               unsigned long long* status,
-                                              const double* __restrict__ halo) {
+                                              const double* __restrict__ halo, long long g0, long long g1) {
+    // chunks [g0, g1) of the S * K level-0 chunks (host-input pipelining launches pieces)
     constexpr int B = T::B;
     const long long K = geo.K[0], SK = K * geo.S;
-    const long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (g >= SK) return;
+    const long long g = g0 + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (g >= g1) return;
     const int s = static_cast<int>(g / K);
     const long long c = g - s * K;
     const long long n = geo.n[0];
@@ -942,11 +943,12 @@ __global__ void __launch_bounds__(128, SP_REV0_MINB) k_rev0(ModelDesc md, const 
                                               const double* __restrict__ solU,
                                               double* __restrict__ part, Outs outs,
                                               unsigned long long* status,
-                                              const double* __restrict__ halo) {
+                                              const double* __restrict__ halo, long long g0, long long g1) {
+    // chunks [g0, g1) of the S * K level-0 chunks (host-input pipelining launches pieces)
     constexpr int B = T::B;
     const long long K = geo.K[0], SK = K * geo.S;
-    const long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (g >= SK) return;
+    const long long g = g0 + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (g >= g1) return;
     const int s = static_cast<int>(g / K);
     const long long c = g - s * K;
     const long long n = geo.n[0];

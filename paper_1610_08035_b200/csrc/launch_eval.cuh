@@ -174,10 +174,18 @@ bool launch_tree_coop(spingp_ctx* ctx, TreeArgs& a1, TreeArgs& a2) {
                                      static_cast<int>(tree_smem_bytes(B, tree_group_size(B)))));
         set = 1;
     }
-    int per = 0, dev = 0, sms = 0;
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tree_coop<B>, tpb, smem));
-    CUDA_OK(cudaGetDevice(&dev));
-    CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    static int sms = 0, occ_tpb = -1, per = 0;  // device SMs, occupancy of the last shape
+    static size_t occ_smem = 0;
+    if (!sms) {
+        int dev = 0;
+        CUDA_OK(cudaGetDevice(&dev));
+        CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    if (occ_tpb != tpb || occ_smem != smem) {
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tree_coop<B>, tpb, smem));
+        occ_tpb = tpb;
+        occ_smem = smem;
+    }
     const long long groups = static_cast<long long>(a1.S) * a1.nG;
     if (groups > static_cast<long long>(per) * sms) return false;
     a1.stamps = ctx->upper_stamps;
@@ -224,10 +232,17 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     bool coop = false;  // top two tree levels in one cooperative launch
     const bool fused = upper_fused();
     if (a.mode != 3) {
-        ctx->pre();
-        k_fwd0<T><<<blocks_for(SK0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
-                                                                 eb.rec[0], eb.part, ctx->d_status, halo);
-        ctx->launched("k_fwd0");
+        const int np = a.in_pieces > 0 ? a.in_pieces : 1;
+        for (int p = 0; p < np; ++p) {
+            const long long c0 = a.in_pieces > 0 ? a.in_chunk[p] : 0, c1 = a.in_pieces > 0 ? a.in_chunk[p + 1] : SK0;
+            if (a.in_pieces > 0) CUDA_OK(cudaStreamWaitEvent(ctx->stream, a.in_ready[p], 0));
+            if (c1 <= c0) continue;
+            ctx->pre();
+            k_fwd0<T><<<blocks_for(c1 - c0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
+                                                                         eb.rec[0], eb.part, ctx->d_status, halo,
+                                                                         c0, c1);
+            ctx->launched("k_fwd0");
+        }
         if (tree) {
             // mode 0: the last level (one group per series) is k_tree_one, or the two
             // top levels k_tree_coop, below
@@ -317,10 +332,18 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     }
     Outs outs{(a.flags & SPINGP_WANT_MEAN) ? a.d_mean : nullptr, (a.flags & SPINGP_WANT_VAR) ? a.d_var : nullptr,
               (a.flags & SPINGP_INCLUDE_NOISE) ? 1 : 0, grad ? 1 : 0, needC ? 1 : 0};
-    ctx->pre();
-    k_rev0<T><<<blocks_for(SK0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
-                                                             eb.sol[1], eb.part, outs, ctx->d_status, halo);
-    ctx->launched("k_rev0");
+    const int nq = a.out_pieces > 0 ? a.out_pieces : 1;
+    for (int q = 0; q < nq; ++q) {
+        const long long c0 = a.out_pieces > 0 ? a.out_chunk[q] : 0, c1 = a.out_pieces > 0 ? a.out_chunk[q + 1] : SK0;
+        if (c1 > c0) {
+            ctx->pre();
+            k_rev0<T><<<blocks_for(c1 - c0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
+                                                                         eb.sol[1], eb.part, outs, ctx->d_status,
+                                                                         halo, c0, c1);
+            ctx->launched("k_rev0");
+        }
+        if (a.out_pieces > 0) CUDA_OK(cudaEventRecord(a.out_ready[q], ctx->stream));
+    }
     FinalArgs fa{};
     fa.part = eb.part;
     fa.K = g.K[0];

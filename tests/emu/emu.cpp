@@ -131,7 +131,7 @@ void emu_eval(const HostModel& hm, const Plan& plan, std::vector<double>& params
     const int tpb = 32;
     unsigned long long* st = &g_status;
     emu_launch(nblocks(SK0, tpb), tpb, [&] {
-        k_fwd0<T>(md, params.data(), t, y, g, fac[0].data(), rec[0].data(), part.data(), st, nullptr);
+        k_fwd0<T>(md, params.data(), t, y, g, fac[0].data(), rec[0].data(), part.data(), st, nullptr, 0, SK0);
     });
     const bool gr = flags & 1u, needC = gr || (flags & 4u);
     if (plan.tree) {
@@ -156,7 +156,7 @@ void emu_eval(const HostModel& hm, const Plan& plan, std::vector<double>& params
     Outs outs{(flags & 2u) ? mean : nullptr, (flags & 4u) ? var : nullptr, (flags & 8u) ? 1 : 0, gr ? 1 : 0,
               needC ? 1 : 0};
     emu_launch(nblocks(SK0, tpb), tpb, [&] {
-        k_rev0<T>(md, params.data(), t, y, g, fac[0].data(), sol[1].data(), part.data(), outs, st, nullptr);
+        k_rev0<T>(md, params.data(), t, y, g, fac[0].data(), sol[1].data(), part.data(), outs, st, nullptr, 0, SK0);
     });
     for (int s = 0; s < g.S; ++s) {
         double acc[P_GRAD + kMaxTheta] = {};
@@ -257,7 +257,7 @@ struct SegState : SegStateBase {
         const Geom& g = plan.geo;
         unsigned long long* st = &g_status;
         emu_launch(nblocks(g.K[0], 32), 32, [&] {
-            k_fwd0<T>(md, params.data(), t, y, g, fac[0].data(), rec[0].data(), part.data(), st, halo());
+            k_fwd0<T>(md, params.data(), t, y, g, fac[0].data(), rec[0].data(), part.data(), st, halo(), 0, g.K[0]);
         });
         for (int l = 1; l < g.nlev; ++l) {
             if (plan.tree) {
@@ -289,7 +289,7 @@ struct SegState : SegStateBase {
         Outs outs{(flags & 2u) ? mean : nullptr, (flags & 4u) ? var : nullptr, (flags & 8u) ? 1 : 0, gr ? 1 : 0,
                   needC ? 1 : 0};
         emu_launch(nblocks(g.K[0], 32), 32, [&] {
-            k_rev0<T>(md, params.data(), t, y, g, fac[0].data(), sol[1].data(), part.data(), outs, st, halo());
+            k_rev0<T>(md, params.data(), t, y, g, fac[0].data(), sol[1].data(), part.data(), outs, st, halo(), 0, g.K[0]);
         });
         const int NC = P_GRAD + hm.nt;
         for (int c = 0; c < NC; ++c) {

@@ -298,3 +298,34 @@ def test_segment_protocol_with_tree_levels(ctx, nranks):
         ctx.set_tree_group(0)
         ctx.set_chunk(0)
     check({"loglik": ll, "grad": g, "mean": mean, "var": var}, leaves, theta, t, y, 0.3, TOL, factor=50.0)
+
+
+@pytest.mark.parametrize("n", [1 << 18, 300_001])
+@pytest.mark.parametrize("want", [dict(grad=True, mean=True, var=True), dict(grad=True), dict(mean=True)])
+def test_pipelined_host_eval_equals_device_eval(ctx, n, want):
+    """The host-pointer call overlaps its H2D with k_fwd0 pieces and its mean/var D2H with
+    k_rev0 pieces (n >= 2^18, one series).  Only launch boundaries move, so the results
+    must equal the device-pointer call bit for bit."""
+    import torch
+    t, y = series(31, n)
+    dev = torch.device("cuda", 0)
+    dt_, dy_ = torch.from_numpy(t).to(dev), torch.from_numpy(y).to(dev)
+    ll = torch.zeros(1, dtype=torch.float64, device=dev)
+    gg = torch.zeros(3, dtype=torch.float64, device=dev)
+    mm = torch.zeros(n, dtype=torch.float64, device=dev)
+    vv = torch.zeros(n, dtype=torch.float64, device=dev)
+    flags = (P.WANT_GRAD if want.get("grad") else 0) | (P.WANT_MEAN if want.get("mean") else 0) | \
+            (P.WANT_VAR if want.get("var") else 0)
+    ctx.eval_device([P.MATERN52], [2.0, 1.5], dt_.data_ptr(), dy_.data_ptr(), n, 0.2, flags, ll.data_ptr(),
+                    gg.data_ptr() if want.get("grad") else 0, mm.data_ptr() if want.get("mean") else 0,
+                    vv.data_ptr() if want.get("var") else 0)
+    ctx.status()
+    torch.cuda.synchronize()
+    h = ctx.eval([P.MATERN52], [2.0, 1.5], t, y, 0.2, **want)
+    assert ll.item() == h["loglik"]
+    if want.get("grad"):
+        assert np.array_equal(gg.cpu().numpy(), h["grad"])
+    if want.get("mean"):
+        assert np.array_equal(mm.cpu().numpy(), h["mean"])
+    if want.get("var"):
+        assert np.array_equal(vv.cpu().numpy(), h["var"])
