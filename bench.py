@@ -454,6 +454,15 @@ def run_ours(args, ws, rank, local):
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
+    if ws == 1:
+        # SURVEY.md §8(d) figure 1: the materialised-SymBTD solve operator at cfg2's size
+        # (1 rhs, device-resident, compulsory bytes 8 (2 b^2 + 2 b) per block row)
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            import bench_solve
+            line["solve_operator"] = bench_solve.measure(n=1_000_000, b=3, steps=10, device=local)
+        except Exception as e:  # report, never break the metric line
+            line["solve_operator"] = {"error": str(e)[:200]}
     if ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl)
     print(json.dumps(line), flush=True)

@@ -166,6 +166,18 @@ int spingp_eval_batched_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32
                                uint32_t flags, double* d_loglik, double* d_grad, double* d_mean,
                                double* d_var);
 
+/* predict at arbitrary test times: posterior
+ * mean H mu and latent variance H C H^T (+ sigma^2 with SPINGP_INCLUDE_NOISE) at test_t[m]
+ * (any order, outputs in input order), plus the training-data loglik and, with
+ * SPINGP_WANT_GRAD, its gradient.  The test points join the n training points in one
+ * sorted grid without an observation term (Sigma'^{-1} = 0 there); a test
+ * time at or before the previous grid time is nudged by 1e-9 x (time span).
+ * Host pointers; fail_block indexes the merged grid. */
+int spingp_predict(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves, const double* theta,
+                   int32_t n_theta, const double* t, const double* y, int64_t n, const double* test_t,
+                   int64_t m, double sigma, uint32_t flags, double* out_loglik, double* out_grad,
+                   double* out_mean, double* out_var, int64_t* fail_block);
+
 /* assemble_prior_precision + add_observation_term with the jitter
  * of SPEC.md:328 and Q_0 := Pinf: diag[n*b*b], upper[(n-1)*b*b], rhs[n*b]
  * (rhs_i = H^T y_i / sigma^2). */

@@ -88,6 +88,8 @@ SIGNATURES = {
     "spingp_ctx_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int]),
     "spingp_ctx_kernel_times": (ctypes.c_int, [_vp, _P(ctypes.c_char_p), _d, _i32, _i32p]),
     "spingp_eval": (ctypes.c_int, [_vp, _vp, _i32, _d, _i32, _d, _d, _i64, _dbl, _u32, _d, _d, _d, _d, _i64p]),
+    "spingp_predict": (ctypes.c_int, [_vp, _vp, _i32, _d, _i32, _d, _d, _i64, _d, _i64, _dbl, _u32, _d, _d, _d, _d,
+                                      _i64p]),
     "spingp_eval_device": (ctypes.c_int, [_vp, _vp, _i32, _d, _i32, _vp, _vp, _i64, _dbl, _u32, _vp, _vp, _vp, _vp]),
     "spingp_eval_batched": (ctypes.c_int, [_vp, _vp, _i32, _d, _i32, _i64, _i64, _d, _d, _d, _u32, _d, _d, _d, _d,
                                            _i64p]),
@@ -279,6 +281,25 @@ class Context:
         fb = _i64()
         st = lib().spingp_eval(self._h, lv.ctypes.data, len(leaves), _p(th), len(th), _p(t), _p(y), n, float(sigma), flags,
                                ctypes.byref(ll), _p(g), _p(mu), _p(v), ctypes.byref(fb))
+        _raise(st, fb)
+        return dict(loglik=ll.value, grad=g, mean=mu, var=v)
+
+    def predict(self, leaves, theta, t, y, test_t, sigma, grad=True, include_noise=False):
+        """predict at arbitrary test times: posterior mean / variance at
+        test_t (input order) with the training loglik (+ gradient)."""
+        lv = _leaves(leaves)
+        th = _f64(theta); t = _f64(t); y = _f64(y); ts = _f64(test_t)
+        if len(y) != len(t):
+            raise ValueError("t and y lengths differ")
+        m = len(ts)
+        ll = _dbl()
+        g = np.empty(len(th) + 1) if grad else None
+        mu = np.empty(m)
+        v = np.empty(m)
+        fb = _i64()
+        flags = (WANT_GRAD if grad else 0) | (INCLUDE_NOISE if include_noise else 0)
+        st = lib().spingp_predict(self._h, lv.ctypes.data, len(leaves), _p(th), len(th), _p(t), _p(y), len(t), _p(ts),
+                                  m, float(sigma), flags, ctypes.byref(ll), _p(g), _p(mu), _p(v), ctypes.byref(fb))
         _raise(st, fb)
         return dict(loglik=ll.value, grad=g, mean=mu, var=v)
 

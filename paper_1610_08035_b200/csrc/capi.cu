@@ -510,6 +510,56 @@ int spingp_eval_batched(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_le
     });
 }
 
+int spingp_predict(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves, const double* theta,
+                   int32_t n_theta, const double* t, const double* y, int64_t n, const double* test_t, int64_t m,
+                   double sigma, uint32_t flags, double* out_loglik, double* out_grad, double* out_mean,
+                   double* out_var, int64_t* fail_block) {
+    return guarded(fail_block, [&] {
+        checked(ctx);
+        if (!out_loglik || (m > 0 && (!out_mean || !out_var))) throw std::invalid_argument("null argument");
+        if ((flags & SPINGP_WANT_GRAD) && !out_grad) throw std::invalid_argument("gradient output is null");
+        const PredictGrid pg = predict_grid(t, y, n, test_t, m);
+        const int64_t L = n + m;
+        static thread_local DeviceVec dbuf;
+        const size_t nt1 = static_cast<size_t>(n_theta) + 1;
+        // t, y, mean, var (L each), loglik, grad, then the mask bytes
+        double* base = dbuf.get(4 * static_cast<size_t>(L) + 1 + nt1 + (static_cast<size_t>(L) + 7) / 8);
+        double* d_t = base;
+        double* d_y = d_t + L;
+        double* d_m = d_y + L;
+        double* d_v = d_m + L;
+        double* d_ll = d_v + L;
+        double* d_g = d_ll + 1;
+        unsigned char* d_obs = reinterpret_cast<unsigned char*>(d_g + nt1);
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        const HostModel& hm = ctx_model(ctx, leaves, n_leaves, n_theta);
+        const Plan plan = make_plan(L, 1, plan_bsize(hm), ctx->m0_override, -1, ctx->g_override);
+        std::vector<double> params(hm.rec_stride, 0.0);
+        fill_record(hm, theta, sigma, params.data());
+        CUDA_OK(cudaMemcpyAsync(d_t, pg.t.data(), L * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_OK(cudaMemcpyAsync(d_y, pg.y.data(), L * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_OK(cudaMemcpyAsync(d_obs, pg.obs.data(), L, cudaMemcpyHostToDevice, ctx->stream));
+        const uint32_t f = (flags & (SPINGP_WANT_GRAD | SPINGP_INCLUDE_NOISE)) | SPINGP_WANT_MEAN | SPINGP_WANT_VAR;
+        EvalArgs a{&hm, &plan, params.data(), params.size(), d_t, d_y, f, d_ll, d_g, d_m, d_v, 0, nullptr, nullptr,
+                   nullptr};
+        a.d_obs = d_obs;
+        a.n_obs = n;
+        dispatch_eval(ctx, a);
+        std::vector<double> mean(static_cast<size_t>(L)), var(static_cast<size_t>(L));
+        CUDA_OK(cudaMemcpyAsync(mean.data(), d_m, L * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_OK(cudaMemcpyAsync(var.data(), d_v, L * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_OK(cudaMemcpyAsync(out_loglik, d_ll, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        if (flags & SPINGP_WANT_GRAD)
+            CUDA_OK(cudaMemcpyAsync(out_grad, d_g, nt1 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        const int st = take_status(ctx, fail_block);
+        for (int64_t k = 0; k < m; ++k) {
+            out_mean[k] = mean[static_cast<size_t>(pg.test_pos[static_cast<size_t>(k)])];
+            out_var[k] = var[static_cast<size_t>(pg.test_pos[static_cast<size_t>(k)])];
+        }
+        return st;
+    });
+}
+
 int spingp_eval(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves, const double* theta,
                 int32_t n_theta, const double* t, const double* y, int64_t n, double sigma,
                 uint32_t flags, double* out_loglik, double* out_grad, double* out_mean,

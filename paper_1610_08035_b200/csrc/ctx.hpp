@@ -208,6 +208,10 @@ struct EvalArgs {
     // chunks [in_chunk[p], in_chunk[p+1]), each after in_ready[p] (its inputs' H2D);
     // k_rev0 runs in pieces [out_chunk[q], out_chunk[q+1]) and records out_ready[q]
     // after each (its points' mean/var may then be copied back)
+    // observation mask (predict at test times): d_obs[S*n] 1 = observed (null = all);
+    // n_obs = observed points per series (the loglik's N; < 0 = n)
+    const unsigned char* d_obs = nullptr;
+    long long n_obs = -1;
     int in_pieces = 0;
     const long long* in_chunk = nullptr;
     const cudaEvent_t* in_ready = nullptr;

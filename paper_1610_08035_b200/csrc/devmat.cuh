@@ -20,6 +20,13 @@ namespace spingp_dev {
 #else
 #define SP_DEV __device__ __forceinline__
 #endif
+// The fixed-size primitives of this file: always inlined, unless SP_DEVM_NOINLINE (the
+// whole-call-tree variant of the b >= 6 build).
+#if defined(SP_DEV_NOINLINE) && defined(SP_DEVM_NOINLINE)
+#define SP_DEVM __device__ __noinline__ inline
+#else
+#define SP_DEVM __device__ __forceinline__
+#endif
 // Loop-unrolling hint for the b x b loops.  Deliberately empty: nvcc fully
 // unrolls the constant-trip loops of the register-resident sizes (b <= 4) on
 // its own, and an explicit `#pragma unroll (B <= 4 ? 64 : 1)` was measured to
@@ -36,24 +43,24 @@ namespace spingp_dev {
 #endif
 
 template <int B>
-SP_DEV void mzero(double* a) {
+SP_DEVM void mzero(double* a) {
 SP_UNROLL
     for (int i = 0; i < B * B; ++i) a[i] = 0.0;
 }
 template <int B>
-SP_DEV void mcopy(double* d, const double* s) {
+SP_DEVM void mcopy(double* d, const double* s) {
 SP_UNROLL
     for (int i = 0; i < B * B; ++i) d[i] = s[i];
 }
 template <int B>
-SP_DEV void vzero(double* a) {
+SP_DEVM void vzero(double* a) {
 SP_UNROLL
     for (int i = 0; i < B; ++i) a[i] = 0.0;
 }
 
 // C = A * B
 template <int B>
-SP_DEV void mm(double* C, const double* A, const double* Bm) {
+SP_DEVM void mm(double* C, const double* A, const double* Bm) {
 SP_UNROLL
     for (int i = 0; i < B; ++i)
 SP_UNROLL
@@ -66,7 +73,7 @@ SP_UNROLL
 }
 // C = A^T * B
 template <int B>
-SP_DEV void mtm(double* C, const double* A, const double* Bm) {
+SP_DEVM void mtm(double* C, const double* A, const double* Bm) {
 SP_UNROLL
     for (int i = 0; i < B; ++i)
 SP_UNROLL
@@ -79,7 +86,7 @@ SP_UNROLL
 }
 // C = A * B^T
 template <int B>
-SP_DEV void mmt(double* C, const double* A, const double* Bm) {
+SP_DEVM void mmt(double* C, const double* A, const double* Bm) {
 SP_UNROLL
     for (int i = 0; i < B; ++i)
 SP_UNROLL
@@ -92,7 +99,7 @@ SP_UNROLL
 }
 // C = A^T * B, known to be symmetric: compute the lower triangle and mirror.
 template <int B>
-SP_DEV void mtm_sym(double* C, const double* A, const double* Bm) {
+SP_DEVM void mtm_sym(double* C, const double* A, const double* Bm) {
 SP_UNROLL
     for (int i = 0; i < B; ++i)
 SP_UNROLL
@@ -106,7 +113,7 @@ SP_UNROLL
 }
 // y = A x
 template <int B>
-SP_DEV void mv(double* y, const double* A, const double* x) {
+SP_DEVM void mv(double* y, const double* A, const double* x) {
 SP_UNROLL
     for (int i = 0; i < B; ++i) {
         double s = 0.0;
@@ -117,7 +124,7 @@ SP_UNROLL
 }
 // y = A^T x
 template <int B>
-SP_DEV void mtv(double* y, const double* A, const double* x) {
+SP_DEVM void mtv(double* y, const double* A, const double* x) {
 SP_UNROLL
     for (int i = 0; i < B; ++i) {
         double s = 0.0;
@@ -127,7 +134,7 @@ SP_UNROLL
     }
 }
 template <int B>
-SP_DEV void msym(double* a) {
+SP_DEVM void msym(double* a) {
 SP_UNROLL
     for (int i = 0; i < B; ++i)
 SP_UNROLL
@@ -138,7 +145,7 @@ SP_UNROLL
         }
 }
 template <int B>
-SP_DEV double mtrace(const double* a) {
+SP_DEVM double mtrace(const double* a) {
     double s = 0.0;
 SP_UNROLL
     for (int i = 0; i < B; ++i) s += a[i * B + i];
@@ -146,7 +153,7 @@ SP_UNROLL
 }
 // Tr(A B)
 template <int B>
-SP_DEV double mtrprod(const double* A, const double* Bm) {
+SP_DEVM double mtrprod(const double* A, const double* Bm) {
     double s = 0.0;
 SP_UNROLL
     for (int i = 0; i < B; ++i)
@@ -160,7 +167,7 @@ SP_UNROLL
 // pivot and no divisions).  Returns false on a non-positive / non-finite pivot.
 // logdet = log det A = -2 log prod_j (1/l_jj), taken in groups of 4 pivots.
 template <int B>
-SP_DEV bool chol_nolog(double* L, const double* A) {
+SP_DEVM bool chol_nolog(double* L, const double* A) {
     bool ok = true;
 SP_UNROLL
     for (int j = 0; j < B; ++j) {
@@ -183,7 +190,7 @@ SP_UNROLL
     return ok;
 }
 template <int B>
-SP_DEV double chol_logdet(const double* L) {
+SP_DEVM double chol_logdet(const double* L) {
     double ld = 0.0;
 SP_UNROLL
     for (int j0 = 0; j0 < B; j0 += 4) {
@@ -195,7 +202,7 @@ SP_UNROLL
     return -2.0 * ld;
 }
 template <int B>
-SP_DEV bool chol(double* L, const double* A, double& logdet) {
+SP_DEVM bool chol(double* L, const double* A, double& logdet) {
     const bool ok = chol_nolog<B>(L, A);
     logdet = ok ? chol_logdet<B>(L) : 0.0;
     return ok;
@@ -208,11 +215,11 @@ SP_DEV bool chol(double* L, const double* A, double& logdet) {
 struct LogDetAcc {
     double m;
     int e;
-    SP_DEV void init() {
+    SP_DEVM void init() {
         m = 1.0;
         e = 0;
     }
-    SP_DEV void mul(double p) {  // p > 0 finite
+    SP_DEVM void mul(double p) {  // p > 0 finite
         double x = m * p;
 #ifdef SPINGP_HOST_EMU
         int ex;
@@ -226,10 +233,10 @@ struct LogDetAcc {
         m = x;
     }
     // log det of the factored matrices = -2 log prod(1/l_jj)
-    SP_DEV double logdet() const { return -2.0 * (log(m) + static_cast<double>(e) * 0.69314718055994530942); }
+    SP_DEVM double logdet() const { return -2.0 * (log(m) + static_cast<double>(e) * 0.69314718055994530942); }
 };
 template <int B>
-SP_DEV void chol_accum(const double* L, LogDetAcc& acc) {
+SP_DEVM void chol_accum(const double* L, LogDetAcc& acc) {
 SP_UNROLL
     for (int j0 = 0; j0 < B; j0 += 4) {
         double p = 1.0;
@@ -239,7 +246,7 @@ SP_UNROLL
     }
 }
 template <int B>
-SP_DEV bool chol(double* L, const double* A, LogDetAcc& acc) {
+SP_DEVM bool chol(double* L, const double* A, LogDetAcc& acc) {
     const bool ok = chol_nolog<B>(L, A);
     if (ok) chol_accum<B>(L, acc);
     return ok;
@@ -247,7 +254,7 @@ SP_DEV bool chol(double* L, const double* A, LogDetAcc& acc) {
 
 // Ainv = (L L^T)^{-1} = L^{-T} L^{-1}, symmetric.
 template <int B>
-SP_DEV void chol_inverse(double* Ainv, const double* L) {
+SP_DEVM void chol_inverse(double* Ainv, const double* L) {
     double Li[B * B];  // L^{-1}, lower
 SP_UNROLL
     for (int j = 0; j < B; ++j) {
@@ -277,7 +284,7 @@ SP_UNROLL
 // ---- triangular-factor forms (the numerically preferred route) -------------
 // Li = L^{-1} for lower-triangular L (Li lower, zero upper).
 template <int B>
-SP_DEV void tri_inverse(double* Li, const double* L) {
+SP_DEVM void tri_inverse(double* Li, const double* L) {
 SP_UNROLL
     for (int j = 0; j < B; ++j) {
         const double dj = L[j * B + j];  // inverted pivot
@@ -298,7 +305,7 @@ SP_UNROLL
 }
 // C = Li A   (Li lower triangular)
 template <int B>
-SP_DEV void lmul(double* C, const double* Li, const double* A) {
+SP_DEVM void lmul(double* C, const double* Li, const double* A) {
 SP_UNROLL
     for (int i = 0; i < B; ++i)
 SP_UNROLL
@@ -311,7 +318,7 @@ SP_UNROLL
 }
 // C = Li^T A   (Li lower triangular)
 template <int B>
-SP_DEV void ltmul(double* C, const double* Li, const double* A) {
+SP_DEVM void ltmul(double* C, const double* Li, const double* A) {
 SP_UNROLL
     for (int i = 0; i < B; ++i)
 SP_UNROLL
@@ -324,7 +331,7 @@ SP_UNROLL
 }
 // y = Li x ; y = Li^T x
 template <int B>
-SP_DEV void lmv(double* y, const double* Li, const double* x) {
+SP_DEVM void lmv(double* y, const double* Li, const double* x) {
 SP_UNROLL
     for (int i = 0; i < B; ++i) {
         double s = 0.0;
@@ -334,7 +341,7 @@ SP_UNROLL
     }
 }
 template <int B>
-SP_DEV void ltmv(double* y, const double* Li, const double* x) {
+SP_DEVM void ltmv(double* y, const double* Li, const double* x) {
 SP_UNROLL
     for (int i = 0; i < B; ++i) {
         double s = 0.0;
@@ -345,7 +352,7 @@ SP_UNROLL
 }
 // C = Li^T X Li for symmetric X (result symmetric)
 template <int B>
-SP_DEV void sandwich(double* C, const double* Li, const double* X) {
+SP_DEVM void sandwich(double* C, const double* Li, const double* X) {
     double T[B * B];
     // T = X Li
 SP_UNROLL
@@ -370,7 +377,7 @@ SP_UNROLL
 }
 // C = Li^T Li = (L L^T)^{-1}
 template <int B>
-SP_DEV void ltl(double* C, const double* Li) {
+SP_DEVM void ltl(double* C, const double* Li) {
 SP_UNROLL
     for (int i = 0; i < B; ++i)
 SP_UNROLL
@@ -386,7 +393,7 @@ SP_UNROLL
 // Triangular solves with the inverted-pivot Cholesky factor L (lower):
 // forward L X = A, backward L^T X = A.
 template <int B>
-SP_DEV void lsolve(double* X, const double* L, const double* A, int ncol = B) {
+SP_DEVM void lsolve(double* X, const double* L, const double* A, int ncol = B) {
 SP_UNROLL
     for (int c = 0; c < B; ++c) {
         if (c >= ncol) break;
@@ -400,7 +407,7 @@ SP_UNROLL
     }
 }
 template <int B>
-SP_DEV void lsolve_v(double* x, const double* L, const double* a) {
+SP_DEVM void lsolve_v(double* x, const double* L, const double* a) {
 SP_UNROLL
     for (int i = 0; i < B; ++i) {
         double s = a[i];
@@ -410,7 +417,7 @@ SP_UNROLL
     }
 }
 template <int B>
-SP_DEV void ltsolve(double* X, const double* L, const double* A) {
+SP_DEVM void ltsolve(double* X, const double* L, const double* A) {
 SP_UNROLL
     for (int c = 0; c < B; ++c)
 SP_UNROLL
@@ -422,7 +429,7 @@ SP_UNROLL
         }
 }
 template <int B>
-SP_DEV void ltsolve_v(double* x, const double* L, const double* a) {
+SP_DEVM void ltsolve_v(double* x, const double* L, const double* a) {
 SP_UNROLL
     for (int i = B - 1; i >= 0; --i) {
         double s = a[i];

@@ -249,7 +249,8 @@ __global__ void __launch_bounds__(128, SP_FWD0_MINB) k_fwd0(ModelDesc md, const 
                                               double* __restrict__ fac, double* __restrict__ rec,
                                               double* __restrict__ part,
                                               unsigned long long* status,
-                                              const double* __restrict__ halo, long long g0, long long g1) {
+                                              const double* __restrict__ halo, long long g0, long long g1,
+                                              const unsigned char* __restrict__ obs) {
     // chunks [g0, g1) of the S * K level-0 chunks (host-input pipelining launches pieces)
     constexpr int B = T::B;
     const long long K = geo.K[0], SK = K * geo.S;
@@ -313,9 +314,12 @@ SP_UNROLL
         }
         double D[B * B], U[B * B], r[B];
         step_assembly<B>(Phn, Mqn, D, U);
+        // observation mask (predict at test times): a test point
+        // has no observation term (Σ'^{-1} = 0 there)
+        const double wo = (!obs || obs[gbase + j]) ? 1.0 : 0.0;
 SP_UNROLL
-        for (int i = 0; i < B * B; ++i) D[i] += Qinv[i] + HH[i];
-        const double yj = ys[j];
+        for (int i = 0; i < B * B; ++i) D[i] += Qinv[i] + wo * HH[i];
+        const double yj = wo != 0.0 ? ys[j] : 0.0;
         if (!isfinite(yj)) {
             report(status, gbase + j, ST_BAD_ARG);
             return;
@@ -331,8 +335,9 @@ SP_UNROLL
     }
     // separator R = en - 1
     double D[B * B], Rr[B];
+    const double woR = (!obs || obs[gbase + en - 1]) ? 1.0 : 0.0;
 SP_UNROLL
-    for (int i = 0; i < B * B; ++i) D[i] = Qinv[i] + HH[i];
+    for (int i = 0; i < B * B; ++i) D[i] = Qinv[i] + woR * HH[i];
     if (en < n || geo.segR) {
         const double dte = (en < n ? ts[en] : halo[2 * s + 1]) - ts[en - 1];
         if (!(dte > 0.0) || !isfinite(dte)) {
@@ -349,7 +354,7 @@ SP_UNROLL
 SP_UNROLL
         for (int i = 0; i < B * B; ++i) D[i] += PQP[i];
     }
-    const double yR = ys[en - 1];
+    const double yR = woR != 0.0 ? ys[en - 1] : 0.0;
     if (!isfinite(yR)) {
         report(status, gbase + en - 1, ST_BAD_ARG);
         return;
@@ -820,13 +825,13 @@ struct Outs {
 template <class T>
 SP_DEV void point_out(const ModelDesc& md, const Outs& o, long long gi, double yv, double is2,
                       double sig, const double* x, const double* C, double& fy, double& noise,
-                      unsigned long long* status) {
+                      unsigned long long* status, bool ob = true) {
     constexpr int B = T::B;
     double mu = 0.0;
 SP_UNROLL
     for (int k = 0; k < B; ++k) mu += T::H(md, k) * x[k];
     const double r = yv - mu;
-    fy += r * r * is2;
+    if (ob) fy += r * r * is2;
     if (o.mean) o.mean[gi] = mu;
     if (o.need_c) {
         double v = 0.0;
@@ -834,7 +839,7 @@ SP_UNROLL
         for (int a = 0; a < B; ++a)
 SP_UNROLL
             for (int b2 = 0; b2 < B; ++b2) v += T::H(md, a) * C[a * B + b2] * T::H(md, b2);
-        noise += r * r + v;
+        if (ob) noise += r * r + v;
         if (o.var) {
             if (v < -1e-10) report(status, gi, ST_NEG_VAR);
             if (v < 0.0) v = 0.0;  // clamp [-1e-10, 0) -> 0
@@ -943,7 +948,8 @@ __global__ void __launch_bounds__(128, SP_REV0_MINB) k_rev0(ModelDesc md, const 
                                               const double* __restrict__ solU,
                                               double* __restrict__ part, Outs outs,
                                               unsigned long long* status,
-                                              const double* __restrict__ halo, long long g0, long long g1) {
+                                              const double* __restrict__ halo, long long g0, long long g1,
+                                              const unsigned char* __restrict__ obs) {
     // chunks [g0, g1) of the S * K level-0 chunks (host-input pipelining launches pieces)
     constexpr int B = T::B;
     const long long K = geo.K[0], SK = K * geo.S;
@@ -992,7 +998,8 @@ SP_UNROLL
         lsolve<B>(X, Li, U);
         double xj[B], CjL[B * B], Cjn[B * B], Cjj[B * B];
         back_step<B>(Li, Y, z, X, hasL, needC, sd, xn, Cnn, CnL, xj, CjL, Cjn, Cjj);
-        point_out<T>(md, outs, gbase + nb, ys[nb], is2, sig, xn, Cnn, fy, noise, status);
+        const bool obn = !obs || obs[gbase + nb];
+        point_out<T>(md, outs, gbase + nb, obn ? ys[nb] : 0.0, is2, sig, xn, Cnn, fy, noise, status, obn);
         step_terms<T>(md, rp, dt, Phn, Qn, Mqn, xn, Cnn, xj, Cjj, Cjn, false, grad, fe, gr);
 SP_UNROLL
         for (int q = 0; q < B; ++q) xn[q] = xj[q];
@@ -1002,7 +1009,8 @@ SP_UNROLL
         }
     }
     // block st: previous block is the left separator (or the anchor at st = 0)
-    point_out<T>(md, outs, gbase + st, ys[st], is2, sig, xn, Cnn, fy, noise, status);
+    const bool obs0 = !obs || obs[gbase + st];
+    point_out<T>(md, outs, gbase + st, obs0 ? ys[st] : 0.0, is2, sig, xn, Cnn, fy, noise, status, obs0);
     {
         const bool anchor = st == 0 && !geo.segL;
         const double dt = anchor ? -1.0 : ts[st] - (st > 0 ? ts[st - 1] : halo[2 * s]);

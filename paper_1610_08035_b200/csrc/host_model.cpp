@@ -316,6 +316,50 @@ StaticModel static_model(const HostModel& hm) {
     return SM_NONE;
 }
 
+PredictGrid predict_grid(const double* t, const double* y, int64_t n, const double* test_t, int64_t m) {
+    if (n < 1 || m < 0 || !t || !y || (m > 0 && !test_t)) throw std::invalid_argument("bad predict arguments");
+    for (int64_t k = 0; k < m; ++k)
+        if (!std::isfinite(test_t[k])) throw std::invalid_argument("test times must be finite");
+    std::vector<int64_t> ord(static_cast<size_t>(m));
+    for (int64_t k = 0; k < m; ++k) ord[static_cast<size_t>(k)] = k;
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return test_t[a] < test_t[b]; });
+    double lo = t[0], hi = t[n - 1];
+    if (m) {
+        lo = std::min(lo, test_t[ord.front()]);
+        hi = std::max(hi, test_t[ord.back()]);
+    }
+    const double eps = 1e-9 * (hi > lo ? hi - lo : 1.0);
+    PredictGrid g;
+    const size_t L = static_cast<size_t>(n + m);
+    g.t.reserve(L);
+    g.y.reserve(L);
+    g.obs.reserve(L);
+    g.test_pos.assign(static_cast<size_t>(m), -1);
+    int64_t i = 0, k = 0;
+    while (i < n || k < m) {
+        // training point first on ties: the test point is then nudged past it
+        const bool take_train = k >= m || (i < n && t[i] <= test_t[ord[static_cast<size_t>(k)]]);
+        if (take_train) {
+            if (!g.t.empty() && !(t[i] > g.t.back()))
+                throw std::invalid_argument("a test time nudged by 1e-9 x span reaches the next training time");
+            g.t.push_back(t[i]);
+            g.y.push_back(y[i]);
+            g.obs.push_back(1);
+            ++i;
+        } else {
+            const int64_t kk = ord[static_cast<size_t>(k)];
+            double tt = test_t[kk];
+            if (!g.t.empty() && !(tt > g.t.back())) tt = g.t.back() + eps;
+            g.test_pos[static_cast<size_t>(kk)] = static_cast<int64_t>(g.t.size());
+            g.t.push_back(tt);
+            g.y.push_back(0.0);
+            g.obs.push_back(0);
+            ++k;
+        }
+    }
+    return g;
+}
+
 bool upper_tree() {
     static const bool t = [] {
         const char* e = std::getenv("SPINGP_UPPER");

@@ -48,6 +48,18 @@ bool upper_tree();
 // g_override (testing knob): a smaller tree group size than tree_group_size(Bsz).
 Plan make_plan(int64_t n, int64_t S, int Bsz, int64_t m0_override = 0, int tree = -1, int64_t g_override = 0);
 
+// predict at test times: the merged grid of n training points (strictly
+// increasing t) and m test times (any order).  Test points carry no observation term
+// (obs = 0, y = 0).  A test time at or before the previous grid time is nudged to that
+// time + eps_t, eps_t = 1e-9 * (time span); a nudge that would reach the
+// next grid time throws std::invalid_argument.
+struct PredictGrid {
+    std::vector<double> t, y;
+    std::vector<unsigned char> obs;
+    std::vector<int64_t> test_pos;  // merged index of test point k (input order)
+};
+PredictGrid predict_grid(const double* t, const double* y, int64_t n, const double* test_t, int64_t m);
+
 // Padded block size with a kernel instantiation (1, 2, 3, 4, 6, 8, 12, 16).
 int pad_b(int b);
 

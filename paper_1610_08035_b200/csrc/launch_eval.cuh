@@ -240,7 +240,7 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
             ctx->pre();
             k_fwd0<T><<<blocks_for(c1 - c0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
                                                                          eb.rec[0], eb.part, ctx->d_status, halo,
-                                                                         c0, c1);
+                                                                         c0, c1, a.d_obs);
             ctx->launched("k_fwd0");
         }
         if (tree) {
@@ -339,7 +339,7 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
             ctx->pre();
             k_rev0<T><<<blocks_for(c1 - c0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
                                                                          eb.sol[1], eb.part, outs, ctx->d_status,
-                                                                         halo, c0, c1);
+                                                                         halo, c0, c1, a.d_obs);
             ctx->launched("k_rev0");
         }
         if (a.out_pieces > 0) CUDA_OK(cudaEventRecord(a.out_ready[q], ctx->stream));
@@ -354,7 +354,7 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     fa.params = eb.params;
     fa.rec_stride = hm.rec_stride;
     fa.nt = nt;
-    fa.n = g.n[0];
+    fa.n = a.n_obs >= 0 ? a.n_obs : g.n[0];
     fa.loglik = a.d_loglik;
     fa.grad = grad ? a.d_grad : nullptr;
     fa.partials = a.mode == 3 ? a.d_seg_out : nullptr;

@@ -22,6 +22,7 @@ namespace {
 
 std::string g_err;
 int64_t g_tree_group = 0;  // emu_set_tree_group
+const unsigned char* g_obs = nullptr;  // emu_set_obs: observation mask of the next eval (S = 1)
 unsigned long long g_status;
 double g_diag[4];  // logdetP, logdetQ, fit_y, fit_e of the last series evaluated
 
@@ -131,7 +132,7 @@ void emu_eval(const HostModel& hm, const Plan& plan, std::vector<double>& params
     const int tpb = 32;
     unsigned long long* st = &g_status;
     emu_launch(nblocks(SK0, tpb), tpb, [&] {
-        k_fwd0<T>(md, params.data(), t, y, g, fac[0].data(), rec[0].data(), part.data(), st, nullptr, 0, SK0);
+        k_fwd0<T>(md, params.data(), t, y, g, fac[0].data(), rec[0].data(), part.data(), st, nullptr, 0, SK0, g_obs);
     });
     const bool gr = flags & 1u, needC = gr || (flags & 4u);
     if (plan.tree) {
@@ -156,7 +157,7 @@ void emu_eval(const HostModel& hm, const Plan& plan, std::vector<double>& params
     Outs outs{(flags & 2u) ? mean : nullptr, (flags & 4u) ? var : nullptr, (flags & 8u) ? 1 : 0, gr ? 1 : 0,
               needC ? 1 : 0};
     emu_launch(nblocks(SK0, tpb), tpb, [&] {
-        k_rev0<T>(md, params.data(), t, y, g, fac[0].data(), sol[1].data(), part.data(), outs, st, nullptr, 0, SK0);
+        k_rev0<T>(md, params.data(), t, y, g, fac[0].data(), sol[1].data(), part.data(), outs, st, nullptr, 0, SK0, g_obs);
     });
     for (int s = 0; s < g.S; ++s) {
         double acc[P_GRAD + kMaxTheta] = {};
@@ -168,7 +169,12 @@ void emu_eval(const HostModel& hm, const Plan& plan, std::vector<double>& params
         g_diag[2] = acc[P_FITY];
         g_diag[3] = acc[P_FITE];
         const double* rp = params.data() + static_cast<size_t>(s) * hm.rec_stride;
-        const double sig = rp[0], s2 = sig * sig, nn = static_cast<double>(g.n[0]);
+        long long nobs = g.n[0];
+        if (g_obs) {
+            nobs = 0;
+            for (long long i = 0; i < g.n[0]; ++i) nobs += g_obs[s * g.n[0] + i] ? 1 : 0;
+        }
+        const double sig = rp[0], s2 = sig * sig, nn = static_cast<double>(nobs);
         loglik[s] = -0.5 * (acc[P_FITY] + acc[P_FITE]) - 0.5 * (ld + acc[P_LDQ] + nn * std::log(s2)) -
                     0.5 * nn * 1.8378770664093454835606594728112;
         if (gr) {
@@ -257,7 +263,7 @@ struct SegState : SegStateBase {
         const Geom& g = plan.geo;
         unsigned long long* st = &g_status;
         emu_launch(nblocks(g.K[0], 32), 32, [&] {
-            k_fwd0<T>(md, params.data(), t, y, g, fac[0].data(), rec[0].data(), part.data(), st, halo(), 0, g.K[0]);
+            k_fwd0<T>(md, params.data(), t, y, g, fac[0].data(), rec[0].data(), part.data(), st, halo(), 0, g.K[0], nullptr);
         });
         for (int l = 1; l < g.nlev; ++l) {
             if (plan.tree) {
@@ -289,7 +295,7 @@ struct SegState : SegStateBase {
         Outs outs{(flags & 2u) ? mean : nullptr, (flags & 4u) ? var : nullptr, (flags & 8u) ? 1 : 0, gr ? 1 : 0,
                   needC ? 1 : 0};
         emu_launch(nblocks(g.K[0], 32), 32, [&] {
-            k_rev0<T>(md, params.data(), t, y, g, fac[0].data(), sol[1].data(), part.data(), outs, st, halo(), 0, g.K[0]);
+            k_rev0<T>(md, params.data(), t, y, g, fac[0].data(), sol[1].data(), part.data(), outs, st, halo(), 0, g.K[0], nullptr);
         });
         const int NC = P_GRAD + hm.nt;
         for (int c = 0; c < NC; ++c) {
@@ -314,6 +320,7 @@ extern "C" {
 
 const char* emu_last_error(void) { return g_err.c_str(); }
 void emu_set_tree_group(int64_t g) { g_tree_group = g; }
+void emu_set_obs(const unsigned char* obs) { g_obs = obs; }
 void emu_last_diag(double* out) {
     for (int i = 0; i < 4; ++i) out[i] = g_diag[i];
 }
@@ -360,6 +367,31 @@ int emu_eval_batched(const spingp_leaf* leaves, int32_t n_leaves, const double* 
     }
     if (fail_block) *fail_block = g_status == ~0ULL ? -1 : static_cast<int64_t>((g_status >> 4) & ((1ULL << 56) - 1));
     return finish();
+}
+
+// spingp_predict (capi.cu) on the host emulation: same grid merge, masked evaluation
+int emu_predict(const spingp_leaf* leaves, int32_t n_leaves, const double* theta, int32_t n_theta, int64_t n,
+                const double* t, const double* y, const double* test_t, int64_t m, double sigma, uint32_t flags,
+                double* loglik, double* grad, double* mean, double* var, int64_t* fail_block, int64_t m0) {
+    PredictGrid pg;
+    try {
+        pg = predict_grid(t, y, n, test_t, m);
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return SPINGP_BAD_ARG;
+    }
+    const int64_t L = n + m;
+    std::vector<double> mu(static_cast<size_t>(L)), v(static_cast<size_t>(L));
+    g_obs = pg.obs.data();
+    const uint32_t f = (flags & 9u) | 2u | 4u;
+    const int st = emu_eval_batched(leaves, n_leaves, theta, n_theta, 1, L, pg.t.data(), pg.y.data(), &sigma, f, loglik,
+                                    grad, mu.data(), v.data(), fail_block, m0, 0);
+    g_obs = nullptr;
+    for (int64_t k = 0; k < m; ++k) {
+        mean[k] = mu[static_cast<size_t>(pg.test_pos[static_cast<size_t>(k)])];
+        var[k] = v[static_cast<size_t>(pg.test_pos[static_cast<size_t>(k)])];
+    }
+    return st;
 }
 
 int emu_btd(int64_t n, int32_t b, const double* diag, const double* upper, const double* rhs, int32_t k,

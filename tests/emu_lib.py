@@ -31,6 +31,9 @@ def lib():
         L.emu_eval_batched.argtypes = [ctypes.c_void_p, ctypes.c_int32, _d, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
                                        _d, _d, _d, ctypes.c_uint32, _d, _d, _d, _d, _i64p, ctypes.c_int64, ctypes.c_int]
         L.emu_set_tree_group.argtypes = [ctypes.c_int64]
+        L.emu_predict.argtypes = [ctypes.c_void_p, ctypes.c_int32, _d, ctypes.c_int32, ctypes.c_int64, _d, _d, _d,
+                                  ctypes.c_int64, ctypes.c_double, ctypes.c_uint32, _d, _d, _d, _d, _i64p,
+                                  ctypes.c_int64]
         L.emu_btd.argtypes = [ctypes.c_int64, ctypes.c_int32, _d, _d, _d, ctypes.c_int32, _d, _d, _d, _d, _i64p,
                               ctypes.c_int64]
         _lib = L
@@ -78,6 +81,24 @@ def evaluate(leaves, theta, t, y, sigma, grad=True, mean=True, var=True, include
     if S == 1:
         return dict(loglik=ll[0], grad=g[0] if grad else None, mean=mu[0] if mean else None, var=v[0] if var else None)
     return dict(loglik=ll, grad=g if grad else None, mean=mu if mean else None, var=v if var else None)
+
+
+def predict(leaves, theta, t, y, test_t, sigma, grad=True, include_noise=False, m0=0):
+    """spingp_predict on the host emulation (merged grid, test points unobserved)."""
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    ts = np.ascontiguousarray(test_t, dtype=np.float64)
+    th = np.ascontiguousarray(theta, dtype=np.float64)
+    m = len(ts)
+    ll = np.zeros(1); g = np.zeros(len(th) + 1); mu = np.zeros(max(m, 1)); v = np.zeros(max(m, 1))
+    fb = ctypes.c_int64()
+    lv = _leaves(leaves)
+    flags = (1 if grad else 0) | (8 if include_noise else 0)
+    st = lib().emu_predict(lv.ctypes.data, len(leaves), _p(th), len(th), len(t), _p(t), _p(y), _p(ts), m,
+                           float(sigma), flags, _p(ll), _p(g), _p(mu), _p(v), ctypes.byref(fb), int(m0))
+    if st:
+        raise EmuError(st, fb.value, lib().emu_last_error().decode())
+    return dict(loglik=ll[0], grad=g if grad else None, mean=mu[:m], var=v[:m])
 
 
 def btd(diag, upper, rhs=None, selinv=False, m0=0):

@@ -13,11 +13,10 @@ import torch  # noqa: E402
 import paper_1610_08035_b200 as P  # noqa: E402
 
 
-def main():
-    n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
-    b = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-    steps = int(sys.argv[3]) if len(sys.argv) > 3 else 20
-    dev = torch.device("cuda", 0)
+def measure(n=1_000_000, b=3, steps=20, device=0, check=True):
+    """Median ms of one cr_solve (1 rhs) on a device-resident random SPD SymBTD, with the
+    HBM roofline figures of SURVEY.md §8(d); L2 flushed before each timed call."""
+    dev = torch.device("cuda", device)
     g = torch.Generator(device=dev).manual_seed(7)
     A = torch.randn(n, b, b, device=dev, dtype=torch.float64, generator=g)
     diag = (A @ A.transpose(1, 2) + 4 * b * torch.eye(b, device=dev, dtype=torch.float64)).contiguous()
@@ -26,7 +25,7 @@ def main():
     x = torch.empty_like(rhs)
     ld = torch.empty(1, device=dev, dtype=torch.float64)
     flush = torch.empty(64 * 1024 * 1024, device=dev, dtype=torch.float32)
-    ctx = P.Context(0)
+    ctx = P.Context(device)
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
     L = P.lib()
@@ -51,13 +50,13 @@ def main():
         e1.synchronize()
         ms.append(e0.elapsed_time(e1))
     t = float(np.median(ms))
-    # residual check: || M x - rhs || / || rhs || (matvec on the host, float64)
-    d, u, r, xx = (v.cpu().numpy() for v in (diag, upper, rhs, x))
-    xb = xx.reshape(n, b)
-    y = np.einsum("nij,nj->ni", d, xb)
-    y[:-1] += np.einsum("nij,nj->ni", u, xb[1:])
-    y[1:] += np.einsum("nji,nj->ni", u, xb[:-1])
-    res = float(np.linalg.norm(y.ravel() - r) / np.linalg.norm(r))
+    res = None
+    if check:  # residual || M x - rhs || / || rhs || (block matvec on the device, fp64)
+        xb = x.view(n, b)
+        yv = torch.einsum("nij,nj->ni", diag, xb)
+        yv[:-1] += torch.einsum("nij,nj->ni", upper, xb[1:])
+        yv[1:] += torch.einsum("nji,nj->ni", upper, xb[:-1])
+        res = float(torch.linalg.norm(yv.reshape(-1) - rhs) / torch.linalg.norm(rhs))
     bytes_ = 8 * (2 * b * b + 2 * b) * n
     peak = 6538.9
     try:
@@ -66,9 +65,18 @@ def main():
     except OSError:
         pass
     gbs = bytes_ / (t * 1e-3) / 1e9
-    print(json.dumps({"op": "btd_cr_solve_device", "n": n, "b": b, "k": 1, "ms": t, "blocks_per_s": n / (t * 1e-3),
-                      "compulsory_bytes": bytes_, "achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak,
-                      "residual": res, "launches": ctx.launch_count()}))
+    out = {"op": "spingp_btd_cr_solve_device", "n": n, "b": b, "k": 1, "ms": t, "blocks_per_s": n / (t * 1e-3),
+           "compulsory_bytes": bytes_, "achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak,
+           "residual": res, "data": "random SPD blocks (seeded), L2 flushed before each call"}
+    ctx.close()
+    return out
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
+    b = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+    steps = int(sys.argv[3]) if len(sys.argv) > 3 else 20
+    print(json.dumps(measure(n, b, steps)))
 
 
 if __name__ == "__main__":
