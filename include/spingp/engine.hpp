@@ -9,8 +9,8 @@
 //   log_marginal_likelihood
 //   mll_gradient                               SPEC.md:289-297 (raw θ, then ∂/∂σ_n, σ_n = std-dev)
 //   predict (at the training times)            SPEC.md:298-306 (clamp :329)
-// Out of scope this round: predict at new test times and optimize_hyperparameters
-// (SURVEY.md §8(f)).
+//   predict (at arbitrary test times)          SPEC.md:298-306, nudge :327 (spingp_predict)
+// Out of scope this round: optimize_hyperparameters.
 
 #include <cmath>
 #include <limits>
@@ -143,6 +143,29 @@ inline PosteriorSummary predict(const Dataset& data, const KernelSpec& spec, con
                               (include_noise ? SPINGP_INCLUDE_NOISE : 0u),
                           dev);
     return PosteriorSummary{data.times, std::move(o.mean), std::move(o.var), o.loglik, std::move(o.grad)};
+}
+
+// Posterior at arbitrary test times: the test points join the training
+// grid without an observation term; test times colliding with earlier grid times are
+// nudged by 1e-9 x span.  PosteriorSummary.times are the test times in the
+// caller's order; mll / mll_grad are the training data's.
+inline PosteriorSummary predict(const Dataset& data, const KernelSpec& spec, const HyperparameterSet& theta,
+                                const NoiseModel& noise, const std::vector<double>& test_times, bool include_noise,
+                                Device& dev = default_device()) {
+    detail::check_data(data, noise);
+    const auto lv = detail::leaves_of(spec);
+    const size_t m = test_times.size();
+    PosteriorSummary out{test_times, std::vector<double>(m), std::vector<double>(m), 0.0,
+                         std::vector<double>(theta.size() + 1)};
+    int64_t fb = -1;
+    const int st_ = spingp_predict(dev.get(), lv.data(), static_cast<int32_t>(lv.size()), theta.data(),
+                                   static_cast<int32_t>(theta.size()), data.times.data(), data.values.data(),
+                                   static_cast<int64_t>(data.times.size()), test_times.data(),
+                                   static_cast<int64_t>(m), std::sqrt(noise.sigma_n2),
+                                   SPINGP_WANT_GRAD | (include_noise ? SPINGP_INCLUDE_NOISE : 0u), &out.mll,
+                                   out.mll_grad.data(), out.mean.data(), out.variance.data(), &fb);
+    Device::check(st_, fb);
+    return out;
 }
 
 }  // namespace spingp

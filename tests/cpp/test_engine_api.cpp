@@ -93,4 +93,23 @@ TEST(Engine, PredictVariancesNonNegativeAndNoiseFlag) {
     }
 }
 
+// SPEC.md:302 example: test time = train time, sigma_n -> 1e-8: the predictive mean
+// approaches y there (1e-4) and the latent variance ~0; far test points revert to the prior.
+TEST(Engine, PredictAtTestTimesInterpolatesAndReverts) {
+    Dataset d;
+    for (int i = 0; i < 50; ++i) {
+        d.times.push_back(0.2 * i);
+        d.values.push_back(std::sin(0.2 * i));
+    }
+    const std::vector<double> tt = {d.times[10], 1000.0, d.times[33]};
+    auto p = predict(d, KernelSpec::matern32(1.0, 2.0), {1.0, 2.0}, NoiseModel{1e-16}, tt, false);
+    EXPECT_NEAR(p.mean[0], d.values[10], 1e-4);
+    EXPECT_NEAR(p.mean[2], d.values[33], 1e-4);
+    EXPECT_NEAR(p.variance[0], 0.0, 1e-4);
+    EXPECT_NEAR(p.mean[1], 0.0, 1e-6);
+    EXPECT_NEAR(p.variance[1], 1.0, 1e-6);  // k(0) = var
+    EXPECT_EQ(p.times.size(), tt.size());
+    EXPECT_EQ(p.mll_grad.size(), 3u);
+}
+
 int main() { return minitest::run_all(); }
