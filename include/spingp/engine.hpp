@@ -10,7 +10,7 @@
 //   mll_gradient                               SPEC.md:289-297 (raw θ, then ∂/∂σ_n, σ_n = std-dev)
 //   predict (at the training times)            SPEC.md:298-306 (clamp :329)
 //   predict (at arbitrary test times)          SPEC.md:298-306, nudge :327 (spingp_predict)
-// Out of scope this round: optimize_hyperparameters.
+//   optimize_hyperparameters                   SPEC.md:307-315 (spingp/optimize.hpp)
 
 #include <cmath>
 #include <limits>

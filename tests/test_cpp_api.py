@@ -33,3 +33,12 @@ def test_spec_engine_api_on_gpu():
     exe = build("test_engine_api", True)
     r = subprocess.run([exe], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_optimize_hyperparameters_api_on_gpu():
+    """SPEC.md:307-315 examples through include/spingp/optimize.hpp (L-BFGS over the GPU
+    loglik + gradient)."""
+    exe = build("test_optimize_api", True)
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
