@@ -42,6 +42,15 @@ namespace spingp_dev {
 #define SP_MEMFENCE() asm volatile("" ::: "memory")
 #endif
 
+// L1 prefetch hint for a global address (no register, no wait; no-op on the host).
+SP_DEVM void prefetch_l1(const void* p) {
+#ifndef SPINGP_HOST_EMU
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+#else
+    (void)p;
+#endif
+}
+
 template <int B>
 SP_DEVM void mzero(double* a) {
 SP_UNROLL

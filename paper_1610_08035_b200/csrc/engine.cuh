@@ -301,6 +301,10 @@ SP_UNROLL
         for (int j = 0; j < B; ++j) HH[i * B + j] = T::H(md, i) * T::H(md, j) * is2;
 
     for (long long j = st; j < en - 1; ++j) {
+        if (m >= 32 && j + 2 < en) {  // long chunks: next step's inputs, while this one computes
+            prefetch_l1(ts + j + 2);
+            prefetch_l1(ys + j + 1);
+        }
         const double dtn = ts[j + 1] - ts[j];
         if (!(dtn > 0.0) || !isfinite(dtn)) {
             report(status, gbase + j + 1, dtn == 0.0 ? ST_DUPLICATE : ST_BAD_ARG);
@@ -988,6 +992,12 @@ SP_UNROLL
 
     for (long long j = en - 2; j >= st; --j) {
         const long long nb = j + 1;
+        if (m >= 32 && j - 1 >= st) {  // long chunks: the next (lower) step's time and value
+            // (prefetching its 18-component factor as well measured slower at b = 3:
+            // the 255-register kernel starts to spill)
+            prefetch_l1(ts + j - 1);
+            prefetch_l1(ys + j - 1);
+        }
         const double dt = ts[nb] - ts[j];
         double Phn[B * B], Qn[B * B], Mqn[B * B];
         T::step(md, rp, dt, Phn, Qn);
