@@ -251,7 +251,7 @@ SP_DEV void tree_load_rev(const TreeArgs& a, const TreeGroup& t, double* R, doub
 
 // the single record left of a series (no left separator): invert it -> E_J
 template <int B>
-SP_DEV void tree_top(const TreeArgs& a, const TreeGroup& t, const double* R, double* E) {
+SP_DEV void tree_top(const TreeArgs& a, const TreeGroup& t, const double* R, double* E, bool write_ld = true) {
     using TR = Tree<B>;
     using RC = Rec<B>;
     double D[B * B], r[B], Lc[B * B], C[B * B], x[B], z[B], ld;
@@ -260,7 +260,7 @@ TR_UNROLL
 TR_UNROLL
     for (int q = 0; q < B; ++q) r[q] = R[(RC::RRHS + q) * a.RS];
     msym<B>(D);
-    if (!chol<B>(Lc, D, ld)) report(a.status, tree_point(a, t, t.k0 + t.cnt - 1), ST_NOT_PD);
+    if (!chol<B>(Lc, D, ld) && a.status) report(a.status, tree_point(a, t, t.k0 + t.cnt - 1), ST_NOT_PD);
     chol_inv_solve<B>(C, Lc);
     lsolve_v<B>(z, Lc, r);
     ltsolve_v<B>(x, Lc, z);
@@ -271,7 +271,7 @@ TR_UNROLL
     for (int q = 0; q < B * B; ++q) E[(TR::SCD + q) * a.ES + 1] = C[q];
 TR_UNROLL
     for (int q = 0; q < B * B; ++q) E[(TR::SCU + q) * a.ES + 1] = 0.0;
-    a.toplogdet[t.s] = ld + R[RC::LOGDET * a.RS];
+    if (write_ld) a.toplogdet[t.s] = ld + R[RC::LOGDET * a.RS];
 }
 
 template <int B>
@@ -392,7 +392,8 @@ SP_DEV void tree_forward_rounds(double* R, int RS, const TreeArgs& a, const Tree
         const int n = tree_width(t.cnt, j);
         TreeFwdScratch<B> sc;
         tree_fwd_compute<B>(R, RS, n, threadIdx.x, sc);
-        if (!sc.ok) report(a.status, tree_point(a, t, t.k0 + min(t.cnt, (2 * threadIdx.x + 1) << j) - 1), ST_NOT_PD);
+        if (!sc.ok && a.status)
+            report(a.status, tree_point(a, t, t.k0 + min(t.cnt, (2 * threadIdx.x + 1) << j) - 1), ST_NOT_PD);
         __syncthreads();
         tree_fwd_store<B>(R, RS, n, threadIdx.x, sc);
         __syncthreads();
@@ -512,30 +513,41 @@ __global__ void __launch_bounds__(kTreeMaxThreads) k_tree_coop(TreeArgs a1, Tree
     }
     grid.sync();
     tree_stamp(a1, ks);
-    if (t.j == 0) {  // the series' top group, staged in this CTA's separator area
+    {  // every CTA reduces its series' top group redundantly (in its still-free separator
+       // area): its own boundary separators then come out of shared memory, with no second
+       // grid barrier and no global round trip
         const TreeGroup t2 = tree_group(a2, t.s);
         double* R2 = E;
         double* E2 = R2 + static_cast<long long>(TR::NR) * a2.RS;
         int ks2 = 0;
+        TreeArgs a2q = a2;
+        if (t.j != 0) a2q.status = nullptr;  // report failures once per series
         tree_load_recs_cg<B>(a2, t2, R2, tid, nt);
         __syncthreads();
-        tree_forward_rounds<B>(R2, a2.RS, a2, t2, ks2);
-        if (tid == 0) tree_top<B>(a2, t2, R2, E2);
+        tree_forward_rounds<B>(R2, a2.RS, a2q, t2, ks2);
+        if (tid == 0) tree_top<B>(a2q, t2, R2, E2, t.j == 0);
         __syncthreads();
-        tree_reverse_rounds<B>(R2, E2, a2, t2, ks2);
-        tree_store_rev<B>(a2, t2, E2, tid, nt);
-    }
-    grid.sync();
-    tree_stamp(a1, ks);
-    {  // boundary separators of this group (written by the top CTA)
-        const long long SnU = static_cast<long long>(a1.S) * (a1.nG + a1.segL);
-        const long long u = static_cast<long long>(t.s) * (a1.nG + a1.segL) + a1.segL + t.j;
-        for (int q = tid; q < TR::NS; q += nt) {
+        tree_reverse_rounds<B>(R2, E2, a2q, t2, ks2);
+        // boundaries j (L: x, C_LL, C_{L,R}) and j + 1 (R: x, C_RR) of this group
+        constexpr int NPT = (TR::NS + 31) / 32;  // components per thread (>= 32 threads)
+        double vL[NPT], vR[NPT];
+        for (int r = 0; r < NPT; ++r) {
+            vL[r] = vR[r] = 0.0;
+            const int q = tid + r * nt;
+            if (q >= TR::NS) continue;
             const bool want = q < B || a1.needC;
-            E[q * a1.ES + 1] = (want && q < TR::SCU) ? __ldcg(a1.solU + q * SnU + u) : 0.0;
-            E[q * a1.ES] = (want && t.hasL) ? __ldcg(a1.solU + q * SnU + u - 1) : 0.0;
+            vL[r] = (want && t.hasL) ? E2[q * a2.ES + t.j] : 0.0;
+            vR[r] = (want && q < TR::SCU) ? E2[q * a2.ES + t.j + 1] : 0.0;
+        }
+        __syncthreads();
+        for (int r = 0; r < NPT; ++r) {
+            const int q = tid + r * nt;
+            if (q >= TR::NS) break;
+            E[q * a1.ES] = vL[r];
+            E[q * a1.ES + 1] = vR[r];
         }
     }
+    tree_stamp(a1, ks);
     __syncthreads();
     tree_reverse_rounds<B>(R, E, a1, t, ks);
     tree_store_rev<B>(a1, t, E, tid, nt);
