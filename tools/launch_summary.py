@@ -5,7 +5,7 @@ import sys
 from collections import defaultdict
 
 
-def main(path, skip_prefixes=("void at::", "at::", "void cutlass")):
+def main(path, keep_prefix="spingp_dev::"):
     rows = []
     with open(path) as f:
         lines = [ln for ln in f if ln.startswith('"')]
@@ -19,7 +19,7 @@ def main(path, skip_prefixes=("void at::", "at::", "void cutlass")):
         rows.append((name, v))
     agg = defaultdict(list)
     for n, v in rows:
-        if n.startswith(skip_prefixes):
+        if not n.startswith(keep_prefix):  # torch fill/flush, cuBLAS residual checks
             continue
         agg[n].append(v)
     total = sum(sum(v) for v in agg.values())
@@ -27,7 +27,7 @@ def main(path, skip_prefixes=("void at::", "at::", "void cutlass")):
     for n, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
         print(f"| `{n}` | {len(v)} | {sum(v):.1f} | {sum(v) / len(v):.2f} | {100 * sum(v) / total:.1f}% |")
     print(f"\nlibrary kernels: {sum(len(v) for v in agg.values())} launches, {total:.1f} us total "
-          f"(torch fill/flush kernels excluded)")
+          f"(library kernels only; torch/cuBLAS kernels of the harness excluded)")
 
 
 if __name__ == "__main__":
