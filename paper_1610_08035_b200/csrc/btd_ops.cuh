@@ -40,30 +40,33 @@ void launch_btd(spingp_ctx* ctx, int64_t n, int b, const double* d_diag, const d
     k_fwdL<B, UserSource<B>><<<blocks_for(g.K[0], tpb), tpb, 0, ctx->stream>>>(usrc, g, 0, fac[0], rec[0],
                                                                                ctx->d_status);
     ctx->launched("k_fwd");
-    if (plan.tree) {  // levels >= 1 as shared-memory trees (tree.cuh), as in launch_eval
-        int l = g.nlev - 1;
-        bool coop = false;
-        if (g.nlev >= 3) {
-            for (int f = 1; f <= g.nlev - 3; ++f) {
-                TreeArgs ta = tree_args<B>(ctx, g, eb, f, needC);
-                launch_tree<B>(ctx, TREE_FWD, ta);
+    constexpr bool kTree = B <= 4;  // tree levels are built for b <= 4 only
+    if (kTree && plan.tree) {  // levels >= 1 as shared-memory trees (tree.cuh), as in launch_eval
+        if constexpr (kTree) {
+            int l = g.nlev - 1;
+            bool coop = false;
+            if (g.nlev >= 3) {
+                for (int f = 1; f <= g.nlev - 3; ++f) {
+                    TreeArgs ta = tree_args<B>(ctx, g, eb, f, needC);
+                    launch_tree<B>(ctx, TREE_FWD, ta);
+                }
+                TreeArgs t1 = tree_args<B>(ctx, g, eb, g.nlev - 2, needC);
+                TreeArgs t2 = tree_args<B>(ctx, g, eb, g.nlev - 1, needC);
+                coop = launch_tree_coop<B>(ctx, t1, t2);
+                if (!coop) launch_tree<B>(ctx, TREE_FWD, t1);
             }
-            TreeArgs t1 = tree_args<B>(ctx, g, eb, g.nlev - 2, needC);
-            TreeArgs t2 = tree_args<B>(ctx, g, eb, g.nlev - 1, needC);
-            coop = launch_tree_coop<B>(ctx, t1, t2);
-            if (!coop) launch_tree<B>(ctx, TREE_FWD, t1);
-        }
-        if (coop) {
-            l = g.nlev - 3;
-        } else {
-            TreeArgs ta = tree_args<B>(ctx, g, eb, l, needC);
-            launch_tree<B>(ctx, TREE_ONE, ta);
-            --l;
-        }
-        for (; l >= 1; --l) {
-            TreeArgs ta = tree_args<B>(ctx, g, eb, l, needC);
-            launch_tree<B>(ctx, TREE_REV, ta);
-        }
+            if (coop) {
+                l = g.nlev - 3;
+            } else {
+                TreeArgs ta = tree_args<B>(ctx, g, eb, l, needC);
+                launch_tree<B>(ctx, TREE_ONE, ta);
+                --l;
+            }
+            for (; l >= 1; --l) {
+                TreeArgs ta = tree_args<B>(ctx, g, eb, l, needC);
+                launch_tree<B>(ctx, TREE_REV, ta);
+            }
+            }
     } else {
     for (int l = 1; l < g.nlev; ++l) {
         RecSource<B> src{rec[l - 1], g.K[l - 1], g.n[l]};

@@ -374,11 +374,9 @@ Plan make_plan(int64_t n, int64_t S, int Bsz, int64_t m0_override, int tree, int
     // b >= 6: one thread per b x b merge is too long a chain for the tree's single-thread
     // top rounds (measured on B200: cfg4 45.9 vs 33.9 ms, cfg5 811 vs 385 ms per 1M/200k
     // points); those sizes keep the cooperative per-thread levels
-    static const bool tree_big = [] {  // SPINGP_TREE_BIG=1: trees for b >= 6 too (A/B knob)
-        const char* e = std::getenv("SPINGP_TREE_BIG");
-        return e && std::strcmp(e, "1") == 0;
-    }();
-    p.tree = (tree < 0 ? upper_tree() : tree != 0) && (Bsz <= 4 || tree_big);
+    // (measured with the tree built for b >= 6 too: cfg4 17.6 vs 15.7 ms, cfg5 737 vs
+    // 337 ms at 1 M points; the tree kernels are now only instantiated for b <= 4)
+    p.tree = (tree < 0 ? upper_tree() : tree != 0) && Bsz <= 4;
     Geom& g = p.geo;
     g.S = static_cast<int>(S);
     // level-0 chunk count: enough threads to fill every SM (tuned on B200);

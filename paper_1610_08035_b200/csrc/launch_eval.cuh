@@ -228,7 +228,9 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
         return;
     }
     const long long SK0 = g.K[0] * g.S;
-    const bool tree = a.plan->tree;
+    // tree levels are built for b <= 4 only (make_plan never plans them above)
+    constexpr bool kTree = B <= 4;
+    const bool tree = kTree && a.plan->tree;
     bool coop = false;  // top two tree levels in one cooperative launch
     const bool fused = upper_fused();
     if (a.mode != 3) {
@@ -244,27 +246,29 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
             ctx->launched("k_fwd0");
         }
         if (tree) {
-            // mode 0: the last level (one group per series) is k_tree_one, or the two
-            // top levels k_tree_coop, below
-            coop = a.mode == 0 && g.nlev >= 3;
-            if (coop) {
-                TreeArgs t1 = tree_args<B>(ctx, g, eb, g.nlev - 2, needC);
-                TreeArgs t2 = tree_args<B>(ctx, g, eb, g.nlev - 1, needC);
-                const int lowf = g.nlev - 3;
-                for (int l = 1; l <= lowf; ++l) {
+            if constexpr (kTree) {
+                // mode 0: the last level (one group per series) is k_tree_one, or the two
+                // top levels k_tree_coop, below
+                coop = a.mode == 0 && g.nlev >= 3;
+                if (coop) {
+                    TreeArgs t1 = tree_args<B>(ctx, g, eb, g.nlev - 2, needC);
+                    TreeArgs t2 = tree_args<B>(ctx, g, eb, g.nlev - 1, needC);
+                    const int lowf = g.nlev - 3;
+                    for (int l = 1; l <= lowf; ++l) {
+                        TreeArgs ta = tree_args<B>(ctx, g, eb, l, needC);
+                        launch_tree<B>(ctx, TREE_FWD, ta);
+                    }
+                    coop = launch_tree_coop<B>(ctx, t1, t2);
+                    if (!coop) {
+                        launch_tree<B>(ctx, TREE_FWD, t1);
+                    }
+                }
+                const int lastf = a.mode == 0 ? g.nlev - 2 : g.nlev - 1;
+                for (int l = (a.mode == 0 && g.nlev >= 3) ? lastf + 1 : 1; l <= lastf; ++l) {
                     TreeArgs ta = tree_args<B>(ctx, g, eb, l, needC);
                     launch_tree<B>(ctx, TREE_FWD, ta);
                 }
-                coop = launch_tree_coop<B>(ctx, t1, t2);
-                if (!coop) {
-                    launch_tree<B>(ctx, TREE_FWD, t1);
-                }
-            }
-            const int lastf = a.mode == 0 ? g.nlev - 2 : g.nlev - 1;
-            for (int l = (a.mode == 0 && g.nlev >= 3) ? lastf + 1 : 1; l <= lastf; ++l) {
-                TreeArgs ta = tree_args<B>(ctx, g, eb, l, needC);
-                launch_tree<B>(ctx, TREE_FWD, ta);
-            }
+                    }
         } else if (!fused || a.mode == 2) {
             for (int l = 1; l < g.nlev; ++l) {
                 RecSource<B> src{eb.rec[l - 1], g.K[l - 1] * g.S, g.n[l]};
@@ -287,18 +291,20 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
         ctx->launched("k_seg_solve");
     }
     if (tree) {
-        int l = g.nlev - 1;
-        if (coop) {
-            l = g.nlev - 3;
-        } else if (a.mode == 0) {
-            TreeArgs ta = tree_args<B>(ctx, g, eb, l, needC);
-            launch_tree<B>(ctx, TREE_ONE, ta);
-            --l;
-        }
-        for (; l >= 1; --l) {
-            TreeArgs ta = tree_args<B>(ctx, g, eb, l, needC);
-            launch_tree<B>(ctx, TREE_REV, ta);
-        }
+        if constexpr (kTree) {
+            int l = g.nlev - 1;
+            if (coop) {
+                l = g.nlev - 3;
+            } else if (a.mode == 0) {
+                TreeArgs ta = tree_args<B>(ctx, g, eb, l, needC);
+                launch_tree<B>(ctx, TREE_ONE, ta);
+                --l;
+            }
+            for (; l >= 1; --l) {
+                TreeArgs ta = tree_args<B>(ctx, g, eb, l, needC);
+                launch_tree<B>(ctx, TREE_REV, ta);
+            }
+            }
     } else if (fused && (a.mode == 0 || g.nlev > 1)) {
         UpperArgs ua{};
         for (int l = 0; l < g.nlev; ++l) {
