@@ -321,6 +321,27 @@ extern "C" {
 const char* emu_last_error(void) { return g_err.c_str(); }
 void emu_set_tree_group(int64_t g) { g_tree_group = g; }
 void emu_set_obs(const unsigned char* obs) { g_obs = obs; }
+
+// The level structure make_plan gives (host logic shared with the library): nlev, tree
+// flag, then per level n, m, K.
+int emu_plan(int64_t n, int64_t S, int32_t Bsz, int64_t m0, int64_t* out, int32_t cap) {
+    try {
+        const Plan p = make_plan(n, S, Bsz, m0);
+        const Geom& g = p.geo;
+        if (cap < 2 + 3 * g.nlev) return SPINGP_BAD_ARG;
+        out[0] = g.nlev;
+        out[1] = p.tree ? 1 : 0;
+        for (int l = 0; l < g.nlev; ++l) {
+            out[2 + 3 * l] = g.n[l];
+            out[3 + 3 * l] = g.m[l];
+            out[4 + 3 * l] = g.K[l];
+        }
+        return SPINGP_OK;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SPINGP_BAD_ARG;
+    }
+}
 void emu_last_diag(double* out) {
     for (int i = 0; i < 4; ++i) out[i] = g_diag[i];
 }

@@ -31,6 +31,7 @@ def lib():
         L.emu_eval_batched.argtypes = [ctypes.c_void_p, ctypes.c_int32, _d, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
                                        _d, _d, _d, ctypes.c_uint32, _d, _d, _d, _d, _i64p, ctypes.c_int64, ctypes.c_int]
         L.emu_set_tree_group.argtypes = [ctypes.c_int64]
+        L.emu_plan.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, _i64p, ctypes.c_int32]
         L.emu_predict.argtypes = [ctypes.c_void_p, ctypes.c_int32, _d, ctypes.c_int32, ctypes.c_int64, _d, _d, _d,
                                   ctypes.c_int64, ctypes.c_double, ctypes.c_uint32, _d, _d, _d, _d, _i64p,
                                   ctypes.c_int64]
@@ -38,6 +39,16 @@ def lib():
                               ctypes.c_int64]
         _lib = L
     return _lib
+
+
+def plan(n, S, Bsz, m0=0):
+    """make_plan's level structure: dict(nlev, tree, levels=[(n, m, K), ...])."""
+    out = np.zeros(2 + 3 * 24, dtype=np.int64)
+    st = lib().emu_plan(int(n), int(S), int(Bsz), int(m0), out.ctypes.data_as(_i64p), len(out))
+    if st:
+        raise EmuError(st, -1, lib().emu_last_error().decode())
+    L = int(out[0])
+    return dict(nlev=L, tree=bool(out[1]), levels=[tuple(int(v) for v in out[2 + 3 * l:5 + 3 * l]) for l in range(L)])
 
 
 def set_tree_group(g):

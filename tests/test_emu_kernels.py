@@ -204,3 +204,18 @@ def test_segment_partition_with_tree_levels(P, G, tree_group):
     assert rel(g, o["grad"]) < 1e-9
     assert rel(mean, o["mean"]) < 1e-9
     assert rel(var, o["var"]) < 1e-9
+
+
+def test_plan_level_structure():
+    """make_plan (host_model.cpp): the level-0 chunk count targets 75,776 chunks; tree
+    levels of G(b) = 512 records at b = 3 end in one group per series; b >= 6 keeps the
+    per-thread 4-record levels."""
+    p = E.plan(1_000_000, 1, 3)  # cfg2
+    assert p["tree"] and p["levels"][0] == (1_000_000, 14, 71429)
+    assert p["levels"][1] == (71429, 512, 140) and p["levels"][2] == (140, 140, 1) and p["nlev"] == 3
+    q = E.plan(2048, 4096, 3)  # cfg3: chunks lengthened so k_rev0's last wave is full
+    assert q["levels"][0] == (2048, 114, 18) and 18 * 4096 <= 2 * 296 * 128
+    r = E.plan(16_000_000, 1, 6)  # cfg4: b = 6, per-thread levels
+    assert not r["tree"] and all(m == 4 for _, m, _ in r["levels"][1:-1])
+    one = E.plan(1, 1, 3)  # a single point still gets a tree level (its top inverse)
+    assert one["nlev"] == 2 and one["levels"][1] == (1, 1, 1)
