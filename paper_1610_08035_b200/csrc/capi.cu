@@ -53,27 +53,6 @@ void upload(spingp_ctx* ctx, double* dst, const double* src, size_t count) {
 
 namespace {
 
-// device scratch for the host-pointer entry points
-struct DeviceVec {
-    double* p = nullptr;
-    size_t n = 0;
-    double* get(size_t count) {
-        if (count > n) {
-            if (p) cudaFree(p);
-            p = nullptr;
-            n = 0;
-            CUDA_OK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double)));
-            n = count;
-        }
-        return p;
-    }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        n = 0;
-    }
-};
-
 void dispatch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     const HostModel& hm = *a.hm;
     if (hm.single_matern) {
@@ -235,6 +214,7 @@ int spingp_ctx_create(int32_t device, spingp_ctx** out) {
         CUDA_OK(cudaMemset(c->d_status, 0xFF, sizeof(unsigned long long)));
         CUDA_OK(cudaEventCreateWithFlags(&c->stage_ev[0], cudaEventDisableTiming));
         CUDA_OK(cudaEventCreateWithFlags(&c->stage_ev[1], cudaEventDisableTiming));
+        set_plan_wave(rev0_wave_threads_m3());
         *out = c;
         return SPINGP_OK;
     });
@@ -245,6 +225,7 @@ int spingp_ctx_destroy(spingp_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->ws.base) cudaFree(ctx->ws.base);
+    ctx->host_io.release();
     if (ctx->d_status) cudaFree(ctx->d_status);
     if (ctx->d_arrive) cudaFree(ctx->d_arrive);
     for (int k = 0; k < 2; ++k) {
@@ -349,6 +330,26 @@ int spingp_ctx_kernel_times(spingp_ctx* ctx, const char** names, double* ms, int
     });
 }
 
+static void eval_batched_locked(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves, const double* theta,
+                                int32_t n_theta, int64_t S, int64_t n, const double* d_t, const double* d_y,
+                                const double* sigma, uint32_t flags, double* d_loglik, double* d_grad,
+                                double* d_mean, double* d_var) {
+    // caller holds ctx->mu
+    if (!theta || !sigma || !d_t || !d_y || !d_loglik) throw std::invalid_argument("null argument");
+    if (S < 1 || n < 1) throw std::invalid_argument("need at least one point and one series");
+    if ((flags & SPINGP_WANT_GRAD) && !d_grad) throw std::invalid_argument("gradient output is null");
+    if ((flags & SPINGP_WANT_MEAN) && !d_mean) throw std::invalid_argument("mean output is null");
+    if ((flags & SPINGP_WANT_VAR) && !d_var) throw std::invalid_argument("variance output is null");
+    const HostModel& hm = ctx_model(ctx, leaves, n_leaves, n_theta);
+    const Plan plan = make_plan(n, S, plan_bsize(hm), ctx->m0_override, -1, ctx->g_override);
+    std::vector<double> params(static_cast<size_t>(S) * hm.rec_stride, 0.0);
+    for (int64_t s = 0; s < S; ++s)
+        fill_record(hm, theta + s * n_theta, sigma[s], params.data() + s * hm.rec_stride);
+    EvalArgs a{&hm, &plan, params.data(), params.size(), d_t, d_y, flags, d_loglik, d_grad, d_mean, d_var,
+               0, nullptr, nullptr, nullptr};
+    dispatch_eval(ctx, a);
+}
+
 int spingp_eval_batched_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
                                const double* theta, int32_t n_theta, int64_t S, int64_t n,
                                const double* d_t, const double* d_y, const double* sigma,
@@ -356,19 +357,9 @@ int spingp_eval_batched_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32
                                double* d_var) {
     return guarded(nullptr, [&] {
         checked(ctx);
-        if (!theta || !sigma || !d_t || !d_y || !d_loglik) throw std::invalid_argument("null argument");
-        if ((flags & SPINGP_WANT_GRAD) && !d_grad) throw std::invalid_argument("gradient output is null");
-        if ((flags & SPINGP_WANT_MEAN) && !d_mean) throw std::invalid_argument("mean output is null");
-        if ((flags & SPINGP_WANT_VAR) && !d_var) throw std::invalid_argument("variance output is null");
         std::lock_guard<std::mutex> lk(ctx->mu);
-        const HostModel& hm = ctx_model(ctx, leaves, n_leaves, n_theta);
-        const Plan plan = make_plan(n, S, plan_bsize(hm), ctx->m0_override, -1, ctx->g_override);
-        std::vector<double> params(static_cast<size_t>(S) * hm.rec_stride, 0.0);
-        for (int64_t s = 0; s < S; ++s)
-            fill_record(hm, theta + s * n_theta, sigma[s], params.data() + s * hm.rec_stride);
-        EvalArgs a{&hm, &plan, params.data(), params.size(), d_t, d_y, flags, d_loglik, d_grad, d_mean, d_var,
-                   0, nullptr, nullptr, nullptr};
-        dispatch_eval(ctx, a);
+        eval_batched_locked(ctx, leaves, n_leaves, theta, n_theta, S, n, d_t, d_y, sigma, flags, d_loglik, d_grad,
+                            d_mean, d_var);
         return SPINGP_OK;
     });
 }
@@ -393,12 +384,12 @@ static int eval_host_pipelined(spingp_ctx* ctx, const spingp_leaf* leaves, int32
                                int32_t n_theta, int64_t n, const double* t, const double* y, double sigma,
                                uint32_t flags, double* out_loglik, double* out_grad, double* out_mean,
                                double* out_var, int64_t* fail_block) {
-    static thread_local DeviceVec dbuf;
+    // caller holds ctx->mu
     const size_t nt1 = static_cast<size_t>(n_theta) + 1;
     const size_t ng = (flags & SPINGP_WANT_GRAD) ? nt1 : 0;
     const size_t nm = (flags & SPINGP_WANT_MEAN) ? n : 0;
     const size_t nv = (flags & SPINGP_WANT_VAR) ? n : 0;
-    double* base = dbuf.get(2 * static_cast<size_t>(n) + 1 + ng + nm + nv);
+    double* base = ctx->host_io.get(2 * static_cast<size_t>(n) + 1 + ng + nm + nv);
     double* d_t = base;
     double* d_y = d_t + n;
     double* d_ll = d_y + n;
@@ -406,7 +397,6 @@ static int eval_host_pipelined(spingp_ctx* ctx, const spingp_leaf* leaves, int32
     double* d_m = d_g + ng;
     double* d_v = d_m + nm;
     {
-        std::lock_guard<std::mutex> lk(ctx->mu);
         const HostModel& hm = ctx_model(ctx, leaves, n_leaves, n_theta);
         const Plan plan = make_plan(n, 1, plan_bsize(hm), ctx->m0_override, -1, ctx->g_override);
         std::vector<double> params(hm.rec_stride, 0.0);
@@ -472,36 +462,31 @@ int spingp_eval_batched(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_le
                         double* out_grad, double* out_mean, double* out_var, int64_t* fail_block) {
     return guarded(fail_block, [&] {
         checked(ctx);
-        if (!t || !y || !out_loglik || S < 1 || n < 1) throw std::invalid_argument("bad argument");
+        if (!theta || !sigma || !t || !y || !out_loglik || S < 1 || n < 1) throw std::invalid_argument("bad argument");
         if ((flags & SPINGP_WANT_GRAD) && !out_grad) throw std::invalid_argument("gradient output is null");
         if ((flags & SPINGP_WANT_MEAN) && !out_mean) throw std::invalid_argument("mean output is null");
         if ((flags & SPINGP_WANT_VAR) && !out_var) throw std::invalid_argument("variance output is null");
-        if (!sigma) throw std::invalid_argument("null argument");
+        // one lock from upload to status: the scratch buffers and the status word are the ctx's
+        std::lock_guard<std::mutex> lk(ctx->mu);
         if (S == 1 && n >= kPipeMin && pipeline_enabled())
             return eval_host_pipelined(ctx, leaves, n_leaves, theta, n_theta, n, t, y, sigma[0], flags, out_loglik,
                                        out_grad, out_mean, out_var, fail_block);
-        static thread_local DeviceVec dbuf;
         const size_t N = static_cast<size_t>(S) * n;
         const size_t nt1 = static_cast<size_t>(n_theta) + 1;
         const size_t ng = (flags & SPINGP_WANT_GRAD) ? S * nt1 : 0;
         const size_t nm = (flags & SPINGP_WANT_MEAN) ? N : 0;
         const size_t nv = (flags & SPINGP_WANT_VAR) ? N : 0;
-        double* base = dbuf.get(2 * N + S + ng + nm + nv);
+        double* base = ctx->host_io.get(2 * N + S + ng + nm + nv);
         double* d_t = base;
         double* d_y = d_t + N;
         double* d_ll = d_y + N;
         double* d_g = d_ll + S;
         double* d_m = d_g + ng;
         double* d_v = d_m + nm;
-        {
-            std::lock_guard<std::mutex> lk(ctx->mu);
-            CUDA_OK(cudaMemcpyAsync(d_t, t, N * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-            CUDA_OK(cudaMemcpyAsync(d_y, y, N * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        }
-        const int st = spingp_eval_batched_device(ctx, leaves, n_leaves, theta, n_theta, S, n, d_t, d_y, sigma,
-                                                  flags, d_ll, d_g, d_m, d_v);
-        if (st != SPINGP_OK) return st;
-        std::lock_guard<std::mutex> lk(ctx->mu);
+        CUDA_OK(cudaMemcpyAsync(d_t, t, N * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_OK(cudaMemcpyAsync(d_y, y, N * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        eval_batched_locked(ctx, leaves, n_leaves, theta, n_theta, S, n, d_t, d_y, sigma, flags, d_ll,
+                            ng ? d_g : nullptr, nm ? d_m : nullptr, nv ? d_v : nullptr);
         CUDA_OK(cudaMemcpyAsync(out_loglik, d_ll, S * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         if (ng) CUDA_OK(cudaMemcpyAsync(out_grad, d_g, ng * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         if (nm) CUDA_OK(cudaMemcpyAsync(out_mean, d_m, nm * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -520,10 +505,10 @@ int spingp_predict(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
         if ((flags & SPINGP_WANT_GRAD) && !out_grad) throw std::invalid_argument("gradient output is null");
         const PredictGrid pg = predict_grid(t, y, n, test_t, m);
         const int64_t L = n + m;
-        static thread_local DeviceVec dbuf;
+        std::lock_guard<std::mutex> lk(ctx->mu);
         const size_t nt1 = static_cast<size_t>(n_theta) + 1;
         // t, y, mean, var (L each), loglik, grad, then the mask bytes
-        double* base = dbuf.get(4 * static_cast<size_t>(L) + 1 + nt1 + (static_cast<size_t>(L) + 7) / 8);
+        double* base = ctx->host_io.get(4 * static_cast<size_t>(L) + 1 + nt1 + (static_cast<size_t>(L) + 7) / 8);
         double* d_t = base;
         double* d_y = d_t + L;
         double* d_m = d_y + L;
@@ -531,7 +516,6 @@ int spingp_predict(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves,
         double* d_ll = d_v + L;
         double* d_g = d_ll + 1;
         unsigned char* d_obs = reinterpret_cast<unsigned char*>(d_g + nt1);
-        std::lock_guard<std::mutex> lk(ctx->mu);
         const HostModel& hm = ctx_model(ctx, leaves, n_leaves, n_theta);
         const Plan plan = make_plan(L, 1, plan_bsize(hm), ctx->m0_override, -1, ctx->g_override);
         std::vector<double> params(hm.rec_stride, 0.0);
@@ -578,9 +562,8 @@ int spingp_assemble(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves
         std::lock_guard<std::mutex> lk(ctx->mu);
         const HostModel& hm = ctx_model(ctx, leaves, n_leaves, n_theta);
         const int b = hm.b;
-        static thread_local DeviceVec dbuf;
         const size_t nd = static_cast<size_t>(n) * b * b, nu = static_cast<size_t>(n > 1 ? n - 1 : 0) * b * b;
-        double* d_t = dbuf.get(2 * n + nd + nu + n * b);
+        double* d_t = ctx->host_io.get(2 * n + nd + nu + n * b);
         double* d_y = d_t + n;
         double* d_d = d_y + n;
         double* d_u = d_d + nd;
@@ -631,21 +614,26 @@ int spingp_seg_finalize_device(spingp_ctx* ctx, int32_t n_theta, int64_t n_total
     });
 }
 
+static void cr_solve_locked(spingp_ctx* ctx, int64_t n, int32_t b, const double* d_diag, const double* d_upper,
+                            const double* d_rhs, int32_t k, double* d_x, double* d_logdet) {
+    if (!d_diag || (n > 1 && !d_upper) || k < 0 || (k > 0 && (!d_rhs || !d_x)))
+        throw std::invalid_argument("bad argument");
+    if (k == 0) {
+        btd_dispatch(ctx, n, b, d_diag, d_upper, nullptr, 1, 0, nullptr, nullptr, nullptr, d_logdet, false);
+        return;
+    }
+    for (int col = 0; col < k; ++col)
+        btd_dispatch(ctx, n, b, d_diag, d_upper, d_rhs, k, col, d_x, nullptr, nullptr, col == 0 ? d_logdet : nullptr,
+                     false);
+}
+
 int spingp_btd_cr_solve_device(spingp_ctx* ctx, int64_t n, int32_t b, const double* d_diag,
                                const double* d_upper, const double* d_rhs, int32_t k, double* d_x,
                                double* d_logdet) {
     return guarded(nullptr, [&] {
         checked(ctx);
-        if (!d_diag || (n > 1 && !d_upper) || k < 0 || (k > 0 && (!d_rhs || !d_x)))
-            throw std::invalid_argument("bad argument");
         std::lock_guard<std::mutex> lk(ctx->mu);
-        if (k == 0) {
-            btd_dispatch(ctx, n, b, d_diag, d_upper, nullptr, 1, 0, nullptr, nullptr, nullptr, d_logdet, false);
-            return SPINGP_OK;
-        }
-        for (int col = 0; col < k; ++col)
-            btd_dispatch(ctx, n, b, d_diag, d_upper, d_rhs, k, col, d_x, nullptr, nullptr,
-                         col == 0 ? d_logdet : nullptr, false);
+        cr_solve_locked(ctx, n, b, d_diag, d_upper, d_rhs, k, d_x, d_logdet);
         return SPINGP_OK;
     });
 }
@@ -655,28 +643,30 @@ int spingp_btd_cr_solve(spingp_ctx* ctx, int64_t n, int32_t b, const double* dia
                         double* logdet, int64_t* fail_block) {
     return guarded(fail_block, [&] {
         checked(ctx);
-        if (!diag || n < 1 || b < 1 || k < 0) throw std::invalid_argument("bad argument");
-        static thread_local DeviceVec dbuf;
+        if (!diag || n < 1 || b < 1 || k < 0 || (n > 1 && !upper) || (k > 0 && !rhs))
+            throw std::invalid_argument("bad argument");
+        std::lock_guard<std::mutex> lk(ctx->mu);
         const size_t nd = static_cast<size_t>(n) * b * b, nu = static_cast<size_t>(n - 1) * b * b;
         const size_t nr = static_cast<size_t>(n) * b * k;
-        double* d_d = dbuf.get(nd + nu + 2 * nr + 1);
+        double* d_d = ctx->host_io.get(nd + nu + 2 * nr + 1);
         double* d_u = d_d + nd;
         double* d_r = d_u + nu;
         double* d_x = d_r + nr;
         double* d_ld = d_x + nr;
-        {
-            std::lock_guard<std::mutex> lk(ctx->mu);
-            CUDA_OK(cudaMemcpyAsync(d_d, diag, nd * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-            if (nu) CUDA_OK(cudaMemcpyAsync(d_u, upper, nu * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-            if (nr) CUDA_OK(cudaMemcpyAsync(d_r, rhs, nr * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        }
-        const int st = spingp_btd_cr_solve_device(ctx, n, b, d_d, d_u, nr ? d_r : nullptr, k, nr ? d_x : nullptr, d_ld);
-        if (st != SPINGP_OK) return st;
-        std::lock_guard<std::mutex> lk(ctx->mu);
+        CUDA_OK(cudaMemcpyAsync(d_d, diag, nd * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        if (nu) CUDA_OK(cudaMemcpyAsync(d_u, upper, nu * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        if (nr) CUDA_OK(cudaMemcpyAsync(d_r, rhs, nr * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        cr_solve_locked(ctx, n, b, d_d, d_u, nr ? d_r : nullptr, k, nr ? d_x : nullptr, d_ld);
         if (nr && x) CUDA_OK(cudaMemcpyAsync(x, d_x, nr * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         if (logdet) CUDA_OK(cudaMemcpyAsync(logdet, d_ld, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         return take_status(ctx, fail_block);
     });
+}
+
+static void selinv_locked(spingp_ctx* ctx, int64_t n, int32_t b, const double* d_diag, const double* d_upper,
+                          double* d_cdiag, double* d_cupper, double* d_logdet) {
+    if (!d_diag || !d_cdiag || (n > 1 && (!d_upper || !d_cupper))) throw std::invalid_argument("bad argument");
+    btd_dispatch(ctx, n, b, d_diag, d_upper, nullptr, 1, 0, nullptr, d_cdiag, d_cupper, d_logdet, true);
 }
 
 int spingp_btd_selinv_device(spingp_ctx* ctx, int64_t n, int32_t b, const double* d_diag,
@@ -684,9 +674,8 @@ int spingp_btd_selinv_device(spingp_ctx* ctx, int64_t n, int32_t b, const double
                              double* d_logdet) {
     return guarded(nullptr, [&] {
         checked(ctx);
-        if (!d_diag || !d_cdiag || (n > 1 && (!d_upper || !d_cupper))) throw std::invalid_argument("bad argument");
         std::lock_guard<std::mutex> lk(ctx->mu);
-        btd_dispatch(ctx, n, b, d_diag, d_upper, nullptr, 1, 0, nullptr, d_cdiag, d_cupper, d_logdet, true);
+        selinv_locked(ctx, n, b, d_diag, d_upper, d_cdiag, d_cupper, d_logdet);
         return SPINGP_OK;
     });
 }
@@ -696,22 +685,17 @@ int spingp_btd_selinv(spingp_ctx* ctx, int64_t n, int32_t b, const double* diag,
                       int64_t* fail_block) {
     return guarded(fail_block, [&] {
         checked(ctx);
-        if (!diag || !cdiag || n < 1 || b < 1) throw std::invalid_argument("bad argument");
-        static thread_local DeviceVec dbuf;
+        if (!diag || !cdiag || n < 1 || b < 1 || (n > 1 && !upper)) throw std::invalid_argument("bad argument");
+        std::lock_guard<std::mutex> lk(ctx->mu);
         const size_t nd = static_cast<size_t>(n) * b * b, nu = static_cast<size_t>(n - 1) * b * b;
-        double* d_d = dbuf.get(2 * nd + 2 * nu + 1);
+        double* d_d = ctx->host_io.get(2 * nd + 2 * nu + 1);
         double* d_u = d_d + nd;
         double* d_cd = d_u + nu;
         double* d_cu = d_cd + nd;
         double* d_ld = d_cu + nu;
-        {
-            std::lock_guard<std::mutex> lk(ctx->mu);
-            CUDA_OK(cudaMemcpyAsync(d_d, diag, nd * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-            if (nu) CUDA_OK(cudaMemcpyAsync(d_u, upper, nu * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        }
-        const int st = spingp_btd_selinv_device(ctx, n, b, d_d, d_u, d_cd, d_cu, d_ld);
-        if (st != SPINGP_OK) return st;
-        std::lock_guard<std::mutex> lk(ctx->mu);
+        CUDA_OK(cudaMemcpyAsync(d_d, diag, nd * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        if (nu) CUDA_OK(cudaMemcpyAsync(d_u, upper, nu * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        selinv_locked(ctx, n, b, d_d, d_u, d_cd, d_cu, d_ld);
         CUDA_OK(cudaMemcpyAsync(cdiag, d_cd, nd * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         if (nu && cupper) CUDA_OK(cudaMemcpyAsync(cupper, d_cu, nu * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         if (logdet) CUDA_OK(cudaMemcpyAsync(logdet, d_ld, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -725,10 +709,9 @@ int spingp_btd_matvec(spingp_ctx* ctx, int64_t n, int32_t b, const double* diag,
         checked(ctx);
         if (!diag || !v || !out || n < 1 || b < 1) throw std::invalid_argument("bad argument");
         std::lock_guard<std::mutex> lk(ctx->mu);
-        static thread_local DeviceVec dbuf;
         const size_t nd = static_cast<size_t>(n) * b * b, nu = static_cast<size_t>(n - 1) * b * b;
         const size_t nv = static_cast<size_t>(n) * b;
-        double* d_d = dbuf.get(nd + nu + 2 * nv);
+        double* d_d = ctx->host_io.get(nd + nu + 2 * nv);
         double* d_u = d_d + nd;
         double* d_v = d_u + nu;
         double* d_o = d_v + nv;

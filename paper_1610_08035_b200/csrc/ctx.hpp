@@ -64,6 +64,27 @@ inline size_t arena_bytes(size_t count) { return (count * sizeof(double) + 255) 
 
 inline unsigned blocks_for(long long n, int tpb) { return static_cast<unsigned>((n + tpb - 1) / tpb); }
 
+// device scratch of the host-pointer entry points (owned by the context, used under its mutex)
+struct DeviceVec {
+    double* p = nullptr;
+    size_t n = 0;
+    double* get(size_t count) {
+        if (count > n) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            n = 0;
+            CUDA_OK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double)));
+            n = count;
+        }
+        return p;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
 }  // namespace spingp_host
 
 struct spingp_ctx {
@@ -71,6 +92,7 @@ struct spingp_ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     spingp_host::Arena ws;
+    spingp_host::DeviceVec host_io;  // H2D/D2H landing buffers of the host-pointer entry points
     unsigned long long* d_status = nullptr;
     unsigned long long* h_status = nullptr;  // pinned landing slot of the status word
     double* h_stage[2] = {nullptr, nullptr};
@@ -229,6 +251,15 @@ void eval_generic_6(spingp_ctx* ctx, const EvalArgs& a);
 void eval_generic_8(spingp_ctx* ctx, const EvalArgs& a);
 void eval_generic_12(spingp_ctx* ctx, const EvalArgs& a);
 void eval_generic_16(spingp_ctx* ctx, const EvalArgs& a);
+int64_t rev0_wave_threads_m3();  // inst_m3.cu
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute
+// is per device, so the cache is a per-kernel bitmask of devices
+inline void opt_in_smem(const void* kern, unsigned long long& done_mask, int device, int bytes) {
+    const unsigned long long bit = 1ULL << (device & 63);
+    if (done_mask & bit) return;
+    CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done_mask |= bit;
+}
 void eval_s_eq6(spingp_ctx* ctx, const EvalArgs& a);       // inst_s_eq6.cu
 void eval_s_eq10(spingp_ctx* ctx, const EvalArgs& a);      // inst_s_eq10.cu
 void eval_s_m32qp6(spingp_ctx* ctx, const EvalArgs& a);    // inst_s_m32qp6.cu

@@ -1058,6 +1058,7 @@ constexpr int kMaxNC = P_GRAD + kMaxTheta;
 struct FinalArgs {
     const double* part;    // [NC][S*K] level-0 per-chunk partial sums
     long long K;           // chunks per series
+    long long S;           // series (grid = nseg * S blocks on x: no 65535 cap on S)
     int NC;
     double* seg;           // [S][nseg][NC] scratch
     unsigned int* arrive;  // [S] zero-initialised counters
@@ -1082,9 +1083,10 @@ SP_DEV double warp_sum(double v) {
 static __global__ void __launch_bounds__(kRedThreads) k_reduce(FinalArgs a) {
     __shared__ double acc[kMaxNC];
     __shared__ int last;
-    const int s = blockIdx.y, sg = blockIdx.x, nseg = gridDim.x;
+    const int nseg = static_cast<int>((a.K + kSeg - 1) / kSeg);
+    const int s = static_cast<int>(blockIdx.x / nseg), sg = static_cast<int>(blockIdx.x % nseg);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long SK = a.K * gridDim.y;
+    const long long SK = a.K * a.S;
     const long long base = static_cast<long long>(s) * a.K + static_cast<long long>(sg) * kSeg;
     const int lim = static_cast<int>(min(static_cast<long long>(kSeg), a.K - static_cast<long long>(sg) * kSeg));
     for (int c = warp; c < a.NC; c += kRedThreads / 32) {

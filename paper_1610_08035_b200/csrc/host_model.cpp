@@ -2,6 +2,7 @@
 // model description and per-series parameter records, plus the host-only C ABI
 // entry points (spingp_kernel_dims, spingp_state_space).  Uses the drop-in
 // C++ API of include/spingp/kernels.hpp for the reference's state_space_of.
+#include <atomic>
 #include <cstdlib>
 #include "host_model.hpp"
 
@@ -368,6 +369,16 @@ bool upper_tree() {
     return t;
 }
 
+namespace {
+// resident threads of one k_rev0 wave at b = 3 (set from an occupancy query when a context
+// is created, spingp_ctx_create -> set_plan_wave; 296 x 128 = 2 CTAs x 148 SMs on a B200)
+std::atomic<int64_t> g_wave{296 * 128};
+}  // namespace
+
+void set_plan_wave(int64_t threads) {
+    if (threads > 0) g_wave.store(threads);
+}
+
 Plan make_plan(int64_t n, int64_t S, int Bsz, int64_t m0_override, int tree, int64_t g_override) {
     if (n < 1 || S < 1) throw std::invalid_argument("need at least one point and one series");
     Plan p;
@@ -392,7 +403,7 @@ Plan make_plan(int64_t n, int64_t S, int Bsz, int64_t m0_override, int tree, int
     // a B200): a plan a few CTAs past a full wave pays a whole extra wave, so lengthen the
     // chunks until the last wave is full (cfg3: 608 -> 576 CTAs, 2.26 -> 1.81 ms per step).
     if (m0_override <= 0 && env_target <= 0 && Bsz == 3) {
-        constexpr int64_t kWave = 296 * 128;
+        const int64_t kWave = g_wave.load();
         const auto chunks = [&](int64_t m) { return S * ((n + m - 1) / m); };
         const int64_t w = chunks(m0) / kWave, rem = chunks(m0) % kWave;
         if (w >= 1 && rem > 0 && rem < kWave / 4)

@@ -47,6 +47,9 @@ struct Plan {
 bool upper_tree();
 // g_override (testing knob): a smaller tree group size than tree_group_size(Bsz).
 Plan make_plan(int64_t n, int64_t S, int Bsz, int64_t m0_override = 0, int tree = -1, int64_t g_override = 0);
+// Resident threads of one level-0 reverse wave on the current device (occupancy query at
+// context creation); make_plan's wave rule uses it.
+void set_plan_wave(int64_t threads);
 
 // predict at test times: the merged grid of n training points (strictly
 // increasing t) and m test times (any order).  Test points carry no observation term

@@ -77,7 +77,8 @@ inline bool upper_fused() {
 template <int B>
 void launch_upper(spingp_ctx* ctx, const Geom& g, UpperArgs& ua) {
     constexpr int tpb = 128;
-    static int resident = 0;  // co-resident CTAs of k_upper<B> on this device type
+    static int resident_dev[64] = {};  // co-resident CTAs of k_upper<B>, per device
+    int& resident = resident_dev[ctx->device & 63];
     if (!resident) {
         int per = 0, dev = 0, sms = 0;
         CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_upper<B>, tpb, 0));
@@ -131,12 +132,9 @@ template <int B>
 void launch_tree(spingp_ctx* ctx, TreeKind kind, TreeArgs& ta) {
     using TR = Tree<B>;
     void (*kern)(TreeArgs) = kind == TREE_FWD ? k_tree_fwd<B> : kind == TREE_REV ? k_tree_rev<B> : k_tree_one<B>;
-    static bool attr[3] = {false, false, false};
-    if (!attr[kind]) {  // opt in to the full 227 KB of shared memory once per kernel
-        CUDA_OK(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(tree_smem_bytes(B, tree_group_size(B)))));
-        attr[kind] = true;
-    }
+    static unsigned long long attr[3] = {0, 0, 0};  // opt in to 227 KB of shared memory per device
+    opt_in_smem(reinterpret_cast<const void*>(kern), attr[kind], ctx->device,
+                static_cast<int>(tree_smem_bytes(B, tree_group_size(B))));
     const size_t smem = 8 * (static_cast<size_t>(TR::NR) * ta.RS + (kind == TREE_FWD ? 0 : static_cast<size_t>(TR::NS) * ta.ES));
     const int half = std::min(ta.G, static_cast<int>(ta.RS)) / 2 + 1;  // nodes of the first round
     const int tpb = std::min(kTreeMaxThreads, std::max(32, (half + 31) / 32 * 32));
@@ -167,25 +165,12 @@ bool launch_tree_coop(spingp_ctx* ctx, TreeArgs& a1, TreeArgs& a2) {
     const int half2 = static_cast<int>(a2.RS) / 2 + 1;
     const int tpb = std::min(kTreeMaxThreads, std::max(32, (std::max(half, half2) + 31) / 32 * 32));
     if ((a2.RS + 1) / 2 > tpb) return false;
-    static int set = 0;
-    if (!set) {
-        CUDA_OK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_tree_coop<B>),
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(tree_smem_bytes(B, tree_group_size(B)))));
-        set = 1;
-    }
-    static int sms = 0, occ_tpb = -1, per = 0;  // device SMs, occupancy of the last shape
-    static size_t occ_smem = 0;
-    if (!sms) {
-        int dev = 0;
-        CUDA_OK(cudaGetDevice(&dev));
-        CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    }
-    if (occ_tpb != tpb || occ_smem != smem) {
-        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tree_coop<B>, tpb, smem));
-        occ_tpb = tpb;
-        occ_smem = smem;
-    }
+    static unsigned long long set = 0;
+    opt_in_smem(reinterpret_cast<const void*>(k_tree_coop<B>), set, ctx->device,
+                static_cast<int>(tree_smem_bytes(B, tree_group_size(B))));
+    int sms = 0, per = 0;  // device SMs, co-resident CTAs of this shape (cheap queries)
+    CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tree_coop<B>, tpb, smem));
     const long long groups = static_cast<long long>(a1.S) * a1.nG;
     if (groups > static_cast<long long>(per) * sms) return false;
     a1.stamps = ctx->upper_stamps;
@@ -365,7 +350,8 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     fa.grad = grad ? a.d_grad : nullptr;
     fa.partials = a.mode == 3 ? a.d_seg_out : nullptr;
     ctx->pre();
-    k_reduce<<<dim3(eb.nseg, g.S), kRedThreads, 0, ctx->stream>>>(fa);
+    fa.S = g.S;
+    k_reduce<<<static_cast<unsigned>(static_cast<long long>(eb.nseg) * g.S), kRedThreads, 0, ctx->stream>>>(fa);
     ctx->launched("k_reduce");
 }
 
