@@ -276,6 +276,28 @@ int oracle_btd_selinv(int64_t n, int32_t b, const double* diag, const double* up
 }
 
 // expm through the oracle's Padé path (for the ported reference tests).
+// Kalman filter + RTS smoother over a (merged, observation-masked) grid: SPEC.md:379-396.
+int oracle_kf_rts(const int32_t* leaves, int32_t n_leaves, const double* theta, int32_t n_theta,
+                  const double* t, const double* y, const unsigned char* observed, int64_t n, double sigma,
+                  double* loglik, double* mean, double* var, double* fvar, int64_t* fail_block, int precision) {
+    return guarded(fail_block, [&] {
+        auto run = [&](auto tag) {
+            using R = decltype(tag);
+            oracle::check_times<R>(t, n);
+            const auto m = oracle::state_space_of<R>(leaves_of(leaves, n_leaves), vec_of<R>(theta, n_theta));
+            const auto o = oracle::kf_rts(m, t, y, observed, n, R(sigma));
+            if (loglik) *loglik = static_cast<double>(o.loglik);
+            for (int64_t i = 0; i < n; ++i) {
+                if (mean) mean[i] = static_cast<double>(o.mean[i]);
+                if (var) var[i] = static_cast<double>(o.var[i]);
+                if (fvar) fvar[i] = static_cast<double>(o.fvar[i]);
+            }
+        };
+        if (precision) run((long double)0);
+        else run(0.0);
+    });
+}
+
 int oracle_expm(int32_t b, const double* A, double* out, int precision) {
     return guarded(nullptr, [&] {
         if (precision) put(oracle::expm(mat_of<long double>(A, b, b)), out);

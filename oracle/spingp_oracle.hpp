@@ -1009,4 +1009,97 @@ EvalOut<R> evaluate(const Model<R>& m, const double* t, const double* y, int64_t
     return out;
 }
 
+
+// ------------------------------------------------------------- Kalman / RTS ----
+// The sequential state-space oracle of SPEC.md:379-396 (kf_mll, kf_rts_predict): a
+// Kalman filter over the (merged) time grid, observations masked by `observed` (a test
+// time is a missing observation: the update is skipped, SPEC.md DESIGN DECISIONS), MLL by
+// the prediction-error decomposition Σ ln N(y_i; H m_i^-, H P_i^- H^T + σ²), then a
+// Rauch-Tung-Striebel backward pass.  The transition is the same jittered discretisation
+// the precision uses (Q̃_i = Q_i + jit I, Q̃_0 = P∞ + jit I), so the
+// three oracles (dense, KF/RTS, sparse precision) describe one model.  Covariances are
+// symmetrised after every update (SPEC.md DESIGN DECISIONS).
+template <class R>
+struct KfOut {
+    R loglik = 0;
+    std::vector<R> mean, var, fvar;  // smoothed H m^s, H P^s H^T; filtered H P H^T
+};
+
+template <class R>
+KfOut<R> kf_rts(const Model<R>& m, const double* t, const double* y, const unsigned char* observed,
+                int64_t n, R sigma) {
+    const int b = m.b;
+    const R s2 = sigma * sigma;
+    const R jit = R(kJitter) * trace(m.Pinf) / R(b);
+    std::vector<Mat<R>> Phi(n), mf(n), Pf(n), mp(n), Pp(n);
+    auto HPH = [&](const Mat<R>& P) {
+        R v = 0;
+        for (int i = 0; i < b; ++i)
+            for (int j = 0; j < b; ++j) v += m.H[i] * P(i, j) * m.H[j];
+        return v;
+    };
+    KfOut<R> out;
+    const R kLog2Pi = R(1.8378770664093454835606594728112L);
+    for (int64_t i = 0; i < n; ++i) {
+        Mat<R> Qt;
+        if (i == 0) {
+            Phi[0] = Mat<R>::identity(b);
+            Qt = m.Pinf;
+            mp[0] = Mat<R>(b, 1);
+        } else {
+            const R dt = R(t[i]) - R(t[i - 1]);
+            if (!(dt > R(0))) throw Failure{DUPLICATE_TIME, i, "duplicate training timestamp"};
+            const Step<R> st = discretize(m, dt, false);
+            Phi[i] = st.Phi;
+            Qt = st.Q;
+            mp[i] = Phi[i] * mf[i - 1];
+        }
+        for (int k = 0; k < b; ++k) Qt(k, k) += jit;
+        Pp[i] = i == 0 ? Qt : sym(Phi[i] * Pf[i - 1] * tr(Phi[i]) + Qt);
+        if (observed && !observed[i]) {
+            mf[i] = mp[i];
+            Pf[i] = Pp[i];
+            continue;
+        }
+        Mat<R> PH(b, 1);
+        for (int a = 0; a < b; ++a)
+            for (int c = 0; c < b; ++c) PH(a, 0) += Pp[i](a, c) * m.H[c];
+        R hm = 0, S = s2;
+        for (int a = 0; a < b; ++a) {
+            hm += m.H[a] * mp[i](a, 0);
+            S += m.H[a] * PH(a, 0);
+        }
+        if (!(S > R(0))) throw Failure{NOT_PD, i, "innovation variance <= 0"};
+        const R v = R(y[i]) - hm;
+        out.loglik += R(-0.5) * (kLog2Pi + std::log(S) + v * v / S);
+        mf[i] = mp[i];
+        Pf[i] = Pp[i];
+        for (int a = 0; a < b; ++a) {
+            mf[i](a, 0) += PH(a, 0) * v / S;
+            for (int c = 0; c < b; ++c) Pf[i](a, c) -= PH(a, 0) * PH(c, 0) / S;
+        }
+        Pf[i] = sym(Pf[i]);
+    }
+    out.mean.resize(n);
+    out.var.resize(n);
+    out.fvar.resize(n);
+    Mat<R> ms = mf[n - 1], Ps = Pf[n - 1];
+    for (int64_t i = n - 1; i >= 0; --i) {
+        if (i < n - 1) {
+            // G = P_i Φ_{i+1}^T (P^-_{i+1})^{-1}:  G^T = (P^-_{i+1})^{-1} Φ_{i+1} P_i
+            Mat<R> Lp;
+            if (!cholesky(Pp[i + 1], Lp)) throw Failure{NOT_PD, i + 1, "predictive covariance not PD"};
+            const Mat<R> G = tr(chol_solve(Lp, Phi[i + 1] * Pf[i]));
+            ms = mf[i] + G * (ms - mp[i + 1]);
+            Ps = sym(Pf[i] + G * (Ps - Pp[i + 1]) * tr(G));
+        }
+        R hm = 0;
+        for (int a = 0; a < b; ++a) hm += m.H[a] * ms(a, 0);
+        out.mean[i] = hm;
+        out.var[i] = HPH(Ps);
+        out.fvar[i] = HPH(Pf[i]);
+    }
+    return out;
+}
+
 }  // namespace oracle
