@@ -45,6 +45,8 @@ def lib():
                                       ctypes.c_int, ctypes.c_int]
         L.oracle_btd_solve.argtypes = [ctypes.c_int64, ctypes.c_int32, _d, _d, _d, ctypes.c_int32, _d, _d, _i64, ctypes.c_int]
         L.oracle_btd_selinv.argtypes = [ctypes.c_int64, ctypes.c_int32, _d, _d, _d, _d, _d, _i64, ctypes.c_int]
+        L.oracle_kf_rts.argtypes = [_i32, ctypes.c_int32, _d, ctypes.c_int32, _d, _d, ctypes.c_void_p, ctypes.c_int64,
+                                    ctypes.c_double, _d, _d, _d, _d, _i64, ctypes.c_int]
         L.oracle_expm.argtypes = [ctypes.c_int32, _d, _d, ctypes.c_int]
         _lib = L
     return _lib
@@ -191,3 +193,40 @@ def btd_selinv(diag, upper, precision=0):
     cd = np.zeros_like(diag); cu = np.zeros((max(n - 1, 0), b, b)); ld = ctypes.c_double(); fb = ctypes.c_int64()
     _check(lib().oracle_btd_selinv(n, b, _p(diag), _p(upper), _p(cd), _p(cu), ctypes.byref(ld), ctypes.byref(fb), precision), fb)
     return cd, cu, ld.value
+
+
+def kf_rts(leaves, theta, t, y, sigma, observed=None, precision=0):
+    """Kalman filter + RTS smoother over the grid t; observed: optional
+    bool mask (False = a test time, processed as a missing observation).  Returns loglik
+    (prediction-error decomposition over the observed points), the smoothed mean H m^s
+    and variance H P^s H^T, and the filtered variance H P H^T, per grid point."""
+    lv = _leaves(leaves)
+    th = np.ascontiguousarray(theta, dtype=np.float64)
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    n = len(t)
+    obs = None if observed is None else np.ascontiguousarray(observed, dtype=np.uint8)
+    ll = ctypes.c_double()
+    mu, v, fv = np.zeros(n), np.zeros(n), np.zeros(n)
+    fb = ctypes.c_int64()
+    st = lib().oracle_kf_rts(lv.ctypes.data_as(_i32), len(leaves), _p(th), len(th), _p(t), _p(y),
+                             None if obs is None else obs.ctypes.data, n, float(sigma), ctypes.byref(ll), _p(mu), _p(v),
+                             _p(fv), ctypes.byref(fb), precision)
+    _check(st, fb)
+    return dict(loglik=ll.value, mean=mu, var=v, fvar=fv)
+
+
+def kf_rts_predict(leaves, theta, t, y, test_t, sigma, precision=0):
+    """kf_rts_predict: the filter over the merged train+test grid with the
+    test times as missing observations; returns (loglik, mean, var) at test_t (input order)."""
+    t = np.asarray(t, float)
+    ts = np.asarray(test_t, float)
+    grid = np.concatenate([t, ts])
+    obs = np.concatenate([np.ones(len(t), bool), np.zeros(len(ts), bool)])
+    yy = np.concatenate([np.asarray(y, float), np.zeros(len(ts))])
+    order = np.argsort(grid, kind="stable")
+    r = kf_rts(leaves, theta, grid[order], yy[order], sigma, observed=obs[order], precision=precision)
+    pos = np.empty(len(grid), dtype=np.int64)
+    pos[order] = np.arange(len(grid))
+    at = pos[len(t):]
+    return r["loglik"], r["mean"][at], r["var"][at]
