@@ -183,6 +183,24 @@ bool launch_tree_coop(spingp_ctx* ctx, TreeArgs& a1, TreeArgs& a2) {
     return true;
 }
 
+// b >= 6: the level-0 kernels run one team of lanes per chunk (team.cuh);
+// SPINGP_TEAM=0 selects the thread-per-chunk kernels (A/B knob).
+inline bool team_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SPINGP_TEAM");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    return on;
+}
+
+// b >= 6 team kernels: launchers defined in the fully inlined team_*.cu units (team_launch.cuh)
+template <class T>
+void launch_fwd0_team(spingp_ctx* ctx, const ModelDesc& md, const EvalBufs& eb, const EvalArgs& a, const Geom& g,
+                      const double* halo, long long c0, long long c1);
+template <class T>
+void launch_rev0_team(spingp_ctx* ctx, const ModelDesc& md, const EvalBufs& eb, const EvalArgs& a, const Geom& g,
+                      const double* halo, const Outs& outs, long long c0, long long c1);
+
 template <class T>
 void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     constexpr int B = T::B;
@@ -224,6 +242,12 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
             const long long c0 = a.in_pieces > 0 ? a.in_chunk[p] : 0, c1 = a.in_pieces > 0 ? a.in_chunk[p + 1] : SK0;
             if (a.in_pieces > 0) CUDA_OK(cudaStreamWaitEvent(ctx->stream, a.in_ready[p], 0));
             if (c1 <= c0) continue;
+            if constexpr (B >= 6) {
+                if (team_enabled()) {
+                    launch_fwd0_team<T>(ctx, md, eb, a, g, halo, c0, c1);
+                    continue;
+                }
+            }
             ctx->pre();
             k_fwd0<T><<<blocks_for(c1 - c0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
                                                                          eb.rec[0], eb.part, ctx->d_status, halo,
@@ -326,7 +350,14 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
     const int nq = a.out_pieces > 0 ? a.out_pieces : 1;
     for (int q = 0; q < nq; ++q) {
         const long long c0 = a.out_pieces > 0 ? a.out_chunk[q] : 0, c1 = a.out_pieces > 0 ? a.out_chunk[q + 1] : SK0;
-        if (c1 > c0) {
+        bool done = false;
+        if constexpr (B >= 6) {
+            if (c1 > c0 && team_enabled()) {
+                launch_rev0_team<T>(ctx, md, eb, a, g, halo, outs, c0, c1);
+                done = true;
+            }
+        }
+        if (c1 > c0 && !done) {
             ctx->pre();
             k_rev0<T><<<blocks_for(c1 - c0, tpb), tpb, 0, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0],
                                                                          eb.sol[1], eb.part, outs, ctx->d_status,

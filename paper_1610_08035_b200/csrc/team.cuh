@@ -1,0 +1,790 @@
+// team.cuh — level-0 kernels for the large state dimensions (b >= 6): one TEAM of
+// TS lanes per chunk instead of one thread per chunk.
+//
+// Why.  A b x b block costs b^2 doubles; with one thread per chunk the ~12 live blocks
+// of the elimination (S, L, X, Y, T, W, accLL, Φ, Q̃, L_Q, ...) need 400 (b = 6) to
+// 3000 (b = 16) doubles per thread, i.e. local memory: the round-1 kernels ran 18.5 k
+// LDL/STL against 3.2 k DFMA (k_revL<16>) and cfg4 / cfg5 reached 1.2 % / 0.5 % of the
+// FP64 peak.  Here lane l of a team owns COLUMN l of every working block (b doubles in
+// registers), and the blocks that serve as the broadcast operand of a product or a
+// triangular solve are staged in shared memory:
+//
+//   y = A c        lane l: y = A (c = column l of the right operand)      A broadcast
+//   y = A^T c      lane l: y = A^T c                                      A broadcast
+//   c <- L^{-1} c  forward substitution on the lane's own column          L broadcast
+//   chol(S)        right-looking: lane k scales column k, the other lanes
+//                  update theirs from it (one team barrier per column)
+//   transpose      column put, team barrier, row get (odd row stride b+1:
+//                  both column and row accesses are bank-conflict free)
+//
+// Every per-block operation of the thread-per-chunk kernels (engine.cuh: elim_block,
+// step_assembly, back_step, step_terms, point_out) is restated column by column, in
+// the same arithmetic order (fma chains over k ascending, inverted Cholesky pivots,
+// pivot / covariance symmetrisation), so results agree with them to rounding.
+// The level-0 record, solution and partial-sum layouts are the ones engine.cuh's upper
+// levels and k_reduce read; only the level-0 factor layout is private:
+//   fac[(chunk * m0 + step) * NF + comp],  NF = b(b+1)/2 (L, inverted diagonal) + b^2 (Y) + b (z)
+//
+// References: SPEC.md:143-205 (btd_core factorize / solve / selective_inverse),
+// :262-306 (assembly, MLL, gradient, posterior); SURVEY.md App. B (formulas).
+#pragma once
+
+#include "engine.cuh"
+
+namespace spingp_dev {
+
+#define TP_INL __device__ __forceinline__
+
+template <int B>
+struct TeamCfg {
+    static constexpr int TS = B <= 8 ? 8 : 16;  // lanes per team: one per column (power of two)
+    static constexpr int LD = B + 1;             // odd smem row stride
+    static constexpr int MAT = B * LD;           // doubles per staged block
+    static constexpr int VEC = (B + 1) & ~1;
+    static constexpr int FWD = 6 * MAT + 2 * VEC;   // per-team smem, forward (doubles)
+    static constexpr int REV = 9 * MAT + 2 * VEC;   // per-team smem, reverse
+    static constexpr int CTA = B <= 8 ? 128 : 64;   // threads per CTA
+    static constexpr int TPC = CTA / TS;            // teams per CTA
+};
+
+struct Team {
+    int l;          // column owned (lane within the team)
+    int base;       // first lane of the team in the warp
+    unsigned mask;  // the team's lanes
+};
+
+template <int TS>
+TP_INL Team make_team() {
+    const int lane = threadIdx.x & 31;
+    Team t;
+    t.l = lane & (TS - 1);
+    t.base = lane & ~(TS - 1);
+    t.mask = (TS == 32 ? 0xffffffffu : ((1u << TS) - 1u)) << t.base;
+    return t;
+}
+TP_INL void tsync(const Team& t) { __syncwarp(t.mask); }
+TP_INL double tshfl(const Team& t, double v, int src) { return __shfl_sync(t.mask, v, t.base + src); }
+template <int TS>
+TP_INL double tsum(const Team& t, double v) {
+#pragma unroll
+    for (int o = TS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(t.mask, v, o);
+    return v;
+}
+
+// ---- column primitives (stride S of the staged block: LD, or B for model blocks) ----
+template <int B, int S>
+TP_INL void colget(double (&c)[B], const double* M, int l) {
+#pragma unroll
+    for (int i = 0; i < B; ++i) c[i] = l < B ? M[i * S + l] : 0.0;
+}
+template <int B, int S>
+TP_INL void colput(double* M, const double (&c)[B], int l) {
+    if (l < B)
+#pragma unroll
+        for (int i = 0; i < B; ++i) M[i * S + l] = c[i];
+}
+template <int B, int S>
+TP_INL void rowget(double (&c)[B], const double* M, int l) {
+#pragma unroll
+    for (int i = 0; i < B; ++i) c[i] = l < B ? M[l * S + i] : 0.0;
+}
+template <int B, int S>
+TP_INL void rowput(double* M, const double (&c)[B], int l) {
+    if (l < B)
+#pragma unroll
+        for (int i = 0; i < B; ++i) M[l * S + i] = c[i];
+}
+template <int B>
+TP_INL void unitcol(double (&c)[B], int l) {
+#pragma unroll
+    for (int i = 0; i < B; ++i) c[i] = i == l ? 1.0 : 0.0;
+}
+template <int B>
+TP_INL double pick(const double (&c)[B], int l) {  // c[l] without dynamic register indexing
+    double v = 0.0;
+#pragma unroll
+    for (int i = 0; i < B; ++i) v = i == l ? c[i] : v;
+    return v;
+}
+// o = A c
+template <int B, int S>
+TP_INL void tmv(double (&o)[B], const double* A, const double (&c)[B]) {
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < B; ++k) s = fma(A[i * S + k], c[k], s);
+        o[i] = s;
+    }
+}
+// o = A^T c
+template <int B, int S>
+TP_INL void tmtv(double (&o)[B], const double* A, const double (&c)[B]) {
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < B; ++k) s = fma(A[k * S + i], c[k], s);
+        o[i] = s;
+    }
+}
+// c <- L^{-1} c  (L lower, inverted pivots on the diagonal; devmat.cuh lsolve order)
+template <int B, int S>
+TP_INL void tlsolve(double (&c)[B], const double* L) {
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+        double s = c[i];
+#pragma unroll
+        for (int k = 0; k < i; ++k) s = fma(-L[i * S + k], c[k], s);
+        c[i] = s * L[i * S + i];
+    }
+}
+// c <- L^{-T} c  (devmat.cuh ltsolve order)
+template <int B, int S>
+TP_INL void tltsolve(double (&c)[B], const double* L) {
+#pragma unroll
+    for (int i = B - 1; i >= 0; --i) {
+        double s = c[i];
+#pragma unroll
+        for (int k = i + 1; k < B; ++k) s = fma(-L[k * S + i], c[k], s);
+        c[i] = s * L[i * S + i];
+    }
+}
+// Cholesky of the symmetric block whose column l is c (lower part read): L (inverted
+// pivots, devmat.cuh chol_nolog arithmetic) staged at Ls; team-uniform success flag.
+// The per-element fma order (k ascending from S[i][l]) equals the left-looking one.
+template <int B>
+TP_INL bool tchol(const Team& tm, double (&c)[B], double* Ls, LogDetAcc* acc) {
+    constexpr int LD = TeamCfg<B>::LD;
+    const int l = tm.l;
+    bool ok = true;
+    double p4 = 1.0;
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+        const double piv = tshfl(tm, c[k], k);
+        ok = ok && (piv > 0.0) && isfinite(piv);
+        const double inv = rsqrt(piv);
+        if (l == k) {
+            Ls[k * LD + k] = inv;
+#pragma unroll
+            for (int i = k + 1; i < B; ++i) Ls[i * LD + k] = c[i] * inv;
+        }
+        tsync(tm);
+        if (l > k && l < B) {
+            const double lk = Ls[l * LD + k];
+#pragma unroll
+            for (int i = k + 1; i < B; ++i) c[i] = fma(-Ls[i * LD + k], lk, c[i]);
+        }
+        p4 *= inv;
+        if (acc && ((k & 3) == 3 || k == B - 1)) {
+            acc->mul(p4);
+            p4 = 1.0;
+        }
+    }
+    return ok;
+}
+// symmetrise the block whose column l is c: c <- (c + row l) / 2 through the scratch block
+template <int B>
+TP_INL void tsym(const Team& tm, double (&c)[B], double* scratch) {
+    constexpr int LD = TeamCfg<B>::LD;
+    tsync(tm);
+    colput<B, LD>(scratch, c, tm.l);
+    tsync(tm);
+    double r[B];
+    rowget<B, LD>(r, scratch, tm.l);
+#pragma unroll
+    for (int i = 0; i < B; ++i) c[i] = 0.5 * (c[i] + r[i]);
+}
+// column l of the transpose of the block whose column l is c
+template <int B>
+TP_INL void ttrans(const Team& tm, double (&o)[B], const double (&c)[B], double* scratch) {
+    constexpr int LD = TeamCfg<B>::LD;
+    tsync(tm);
+    colput<B, LD>(scratch, c, tm.l);
+    tsync(tm);
+    rowget<B, LD>(o, scratch, tm.l);
+}
+
+// Φ, Q for step dt into PhiS, QS (row stride B, written by the model code of lane 0),
+// then L_Q = chol(Q + jit I) into LQ.  Team-uniform success.
+template <class T>
+TP_INL bool tmodel(const Team& tm, const ModelDesc& md, const double* rp, double dt, double jit, double* PhiS,
+                   double* QS, double* LQ, LogDetAcc* ldq) {
+    constexpr int B = T::B;
+    if (tm.l == 0) T::step(md, rp, dt, PhiS, QS);
+    tsync(tm);
+    double c[B];
+    colget<B, B>(c, QS, tm.l);
+#pragma unroll
+    for (int i = 0; i < B; ++i)
+        if (i == tm.l && i < md.b) c[i] += jit;
+    return tchol<B>(tm, c, LQ, ldq);
+}
+
+// Assembly pieces of one step (engine.cuh step_assembly): column l of
+//   PQP = Φ^T Q̃^{-1} Φ = Z^T Z (Z = L_Q^{-1} Φ)   and   U = -Φ^T Q̃^{-1} = -(L_Q^{-T} Z)^T;
+// optionally column l of W0 = U^T = -Q̃^{-1} Φ (the first block's left coupling).
+template <int B>
+TP_INL void tassembly(const Team& tm, const double* PhiS, const double* LQ, double* ZS, double* WS, double (&pqp)[B],
+                      double (&U)[B], double* W0) {
+    constexpr int LD = TeamCfg<B>::LD;
+    double z[B];
+    colget<B, B>(z, PhiS, tm.l);
+    tlsolve<B, LD>(z, LQ);
+    colput<B, LD>(ZS, z, tm.l);
+    tsync(tm);
+    tmtv<B, LD>(pqp, ZS, z);
+    tltsolve<B, LD>(z, LQ);  // column l of Q̃^{-1} Φ
+    if (W0)
+#pragma unroll
+        for (int i = 0; i < B; ++i) W0[i] = -z[i];
+    colput<B, LD>(WS, z, tm.l);
+    tsync(tm);
+    rowget<B, LD>(U, WS, tm.l);
+#pragma unroll
+    for (int i = 0; i < B; ++i) U[i] = -U[i];
+}
+
+// column l of Q̃^{-1} (engine.cuh chol_inv_solve, symmetrised)
+template <int B>
+TP_INL void tqinv(const Team& tm, double (&q)[B], const double* LQ, double* scratch) {
+    constexpr int LD = TeamCfg<B>::LD;
+    unitcol<B>(q, tm.l);
+    tlsolve<B, LD>(q, LQ);
+    tltsolve<B, LD>(q, LQ);
+    tsym<B>(tm, q, scratch);
+}
+
+// ======================================================== forward, level 0 ====
+template <class T>
+__global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_fwd0_team(
+    ModelDesc md, const double* __restrict__ params, const double* __restrict__ t, const double* __restrict__ y,
+    Geom geo, double* __restrict__ fac, double* __restrict__ rec, double* __restrict__ part,
+    unsigned long long* status, const double* __restrict__ halo, long long g0, long long g1,
+    const unsigned char* __restrict__ obs) {
+    constexpr int B = T::B;
+    using C = TeamCfg<B>;
+    constexpr int LD = C::LD;
+    constexpr int NLI = B * (B + 1) / 2, NF = NLI + B * B + B;
+    extern __shared__ double smem_team[];
+    const Team tm = make_team<C::TS>();
+    const int tid = threadIdx.x / C::TS;
+    double* R = smem_team + static_cast<size_t>(tid) * C::FWD;
+    double* PhiS = R;               // model blocks (row stride B)
+    double* QS = R + C::MAT;
+    double* LQ = R + 2 * C::MAT;    // chol(Q̃)
+    double* LS = R + 3 * C::MAT;    // chol(S)
+    double* XS = R + 4 * C::MAT;
+    double* YS = R + 5 * C::MAT;
+    double* vS = R + 6 * C::MAT;    // rc gather
+    double* hS = vS + C::VEC;       // accrL gather
+    const long long g = g0 + static_cast<long long>(blockIdx.x) * C::TPC + tid;
+    if (g >= g1) return;
+    const int l = tm.l;
+    const long long K = geo.K[0], SK = K * geo.S;
+    const int s = static_cast<int>(g / K);
+    const long long c = g - s * K;
+    const long long n = geo.n[0];
+    const int m = geo.m[0];
+    const long long st = c * m, en = min(n, st + m);
+    const double* ts = t + s * n;
+    const double* ys = y + s * n;
+    const double* rp = params + static_cast<long long>(s) * md.rec_stride;
+    const double sig = rp[0], jit = rp[1], is2 = 1.0 / (sig * sig);
+    const long long gbase = static_cast<long long>(s) * n;
+    const bool hasL = c > 0 || geo.segL;
+    const double Hl = l < B ? T::H(md, l) : 0.0;
+    double H[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) H[i] = T::H(md, i);
+
+    double dt = -1.0;
+    if (st > 0 || geo.segL) {
+        dt = ts[st] - (st > 0 ? ts[st - 1] : halo[2 * s]);
+        if (!(dt > 0.0) || !isfinite(dt)) {
+            if (l == 0) report(status, gbase + st, dt == 0.0 ? ST_DUPLICATE : ST_BAD_ARG);
+            return;
+        }
+    }
+    if (!tmodel<T>(tm, md, rp, dt, jit, PhiS, QS, LQ, nullptr)) {
+        if (l == 0) report(status, gbase + st, ST_SINGULAR_Q);
+        return;
+    }
+    double Qinv[B], W[B], Tc[B], acc[B], rc[B];
+    tqinv<B>(tm, Qinv, LQ, XS);
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+        W[i] = 0.0;
+        Tc[i] = 0.0;
+        acc[i] = 0.0;
+        rc[i] = 0.0;
+    }
+    if (hasL) {  // P_{st, st-1} = U_{st-1}^T = -Q̃_st^{-1} Φ_st
+        double pqp[B], U[B];
+        tassembly<B>(tm, PhiS, LQ, XS, YS, pqp, U, W);
+    }
+    double accrL = 0.0;  // component l of the carried left rhs
+    LogDetAcc piv;
+    piv.init();
+
+    for (long long j = st; j < en - 1; ++j) {
+        const double dtn = ts[j + 1] - ts[j];
+        if (!(dtn > 0.0) || !isfinite(dtn)) {
+            if (l == 0) report(status, gbase + j + 1, dtn == 0.0 ? ST_DUPLICATE : ST_BAD_ARG);
+            return;
+        }
+        tsync(tm);  // the previous step's reads of the staged blocks are done
+        if (!tmodel<T>(tm, md, rp, dtn, jit, PhiS, QS, LQ, nullptr)) {
+            if (l == 0) report(status, gbase + j + 1, ST_SINGULAR_Q);
+            return;
+        }
+        double D[B], U[B];
+        tassembly<B>(tm, PhiS, LQ, XS, YS, D, U, nullptr);
+        const double wo = (!obs || obs[gbase + j]) ? 1.0 : 0.0;
+        const double yj = wo != 0.0 ? ys[j] : 0.0;
+        if (!isfinite(yj)) {
+            if (l == 0) report(status, gbase + j, ST_BAD_ARG);
+            return;
+        }
+#pragma unroll
+        for (int i = 0; i < B; ++i) D[i] = (D[i] + (Qinv[i] + wo * (H[i] * Hl * is2))) - Tc[i];
+        // S = D - T; pivot symmetrisation — D and T are exactly symmetric
+        // up to Q̃^{-1}, which tqinv symmetrised already
+        if (!tchol<B>(tm, D, LS, &piv)) {
+            if (l == 0) report(status, gbase + j, ST_NOT_PD);
+            return;
+        }
+        tqinv<B>(tm, Qinv, LQ, PhiS);  // Q̃_{j+1}^{-1}: the next block's diagonal term
+        double z[B];
+#pragma unroll
+        for (int i = 0; i < B; ++i) z[i] = H[i] * yj * is2 - rc[i];
+        tlsolve<B, LD>(z, LS);
+        tlsolve<B, LD>(U, LS);  // X = L^{-1} U
+        if (hasL) tlsolve<B, LD>(W, LS);  // Y = L^{-1} W
+        tsync(tm);
+        colput<B, LD>(XS, U, l);
+        if (hasL) colput<B, LD>(YS, W, l);
+        tsync(tm);
+        tmtv<B, LD>(Tc, XS, U);  // T' = X^T X
+        double rcl = 0.0, yz = 0.0;
+#pragma unroll
+        for (int i = 0; i < B; ++i) rcl = fma(U[i], z[i], rcl);  // (X^T z)_l
+        if (hasL) {
+            double G[B];
+            tmtv<B, LD>(G, YS, W);  // Y^T Y
+#pragma unroll
+            for (int i = 0; i < B; ++i) acc[i] -= G[i];
+#pragma unroll
+            for (int i = 0; i < B; ++i) yz = fma(W[i], z[i], yz);
+            accrL -= yz;
+        }
+        // factor of step j for the reverse sweep: L (packed, inverted pivots), Y, z
+        double* fp = fac + (g * m + (j - st)) * static_cast<long long>(NF);
+        if (l < B) {
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+                if (i >= l) fp[i * (i + 1) / 2 + l] = LS[i * LD + l];
+            if (hasL)
+#pragma unroll
+                for (int i = 0; i < B; ++i) fp[NLI + i * B + l] = W[i];
+            fp[NLI + B * B + l] = pick<B>(z, l);
+        }
+        if (hasL) {  // W' = -X^T Y
+            double G[B];
+            tmtv<B, LD>(G, XS, W);
+#pragma unroll
+            for (int i = 0; i < B; ++i) W[i] = -G[i];
+        }
+        if (l < B) vS[l] = rcl;
+        tsync(tm);
+#pragma unroll
+        for (int i = 0; i < B; ++i) rc[i] = vS[i];
+    }
+    // separator R = en - 1
+    const double woR = (!obs || obs[gbase + en - 1]) ? 1.0 : 0.0;
+    double D[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) D[i] = Qinv[i] + woR * (H[i] * Hl * is2);
+    if (en < n || geo.segR) {
+        const double dte = (en < n ? ts[en] : halo[2 * s + 1]) - ts[en - 1];
+        if (!(dte > 0.0) || !isfinite(dte)) {
+            if (l == 0) report(status, gbase + en, dte == 0.0 ? ST_DUPLICATE : ST_BAD_ARG);
+            return;
+        }
+        tsync(tm);
+        if (!tmodel<T>(tm, md, rp, dte, jit, PhiS, QS, LQ, nullptr)) {
+            if (l == 0) report(status, gbase + en, ST_SINGULAR_Q);
+            return;
+        }
+        double pqp[B], U[B];
+        tassembly<B>(tm, PhiS, LQ, XS, YS, pqp, U, nullptr);
+#pragma unroll
+        for (int i = 0; i < B; ++i) D[i] += pqp[i];
+    }
+    const double yR = woR != 0.0 ? ys[en - 1] : 0.0;
+    if (!isfinite(yR)) {
+        if (l == 0) report(status, gbase + en - 1, ST_BAD_ARG);
+        return;
+    }
+    // record (engine.cuh write_rec layout, component-major over chunks)
+    double* r = rec + g;
+    if (l < B) {
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            r[(Rec<B>::RDIAG + i * B + l) * SK] = D[i] - Tc[i];
+            r[(Rec<B>::LDIAG + i * B + l) * SK] = acc[i];
+            r[(Rec<B>::LR + l * B + i) * SK] = hasL ? W[i] : 0.0;  // LR = W^T
+        }
+        r[(Rec<B>::RRHS + l) * SK] = Hl * yR * is2 - pick<B>(rc, l);
+        r[(Rec<B>::LRHS + l) * SK] = accrL;
+    }
+    if (l == 0) {
+        r[Rec<B>::LOGDET * SK] = piv.logdet();
+        part[P_LOGDET * SK + g] = piv.logdet();
+    }
+}
+
+// ======================================================== reverse, level 0 ====
+
+// Likelihood / gradient terms of one step (engine.cuh step_terms) for the team: the
+// current block (xc, column l of Ccc), the previous block (xp, column l of Cpp) and
+// column l of Cpc = C_{p,c}; Φ, Q (raw) at PhiS, QS (stride B), L_Q at LQ.  Scratch
+// blocks S0..S3 (S0, S1 also the stride-B M and Bm handed to T::grad).  fe and g are
+// accumulated by lane 0.
+template <class T>
+TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, double dt, const double* PhiS,
+                        const double* QS, const double* LQ, const double (&xc)[T::B], const double (&Ccc)[T::B],
+                        const double (&xp)[T::B], const double (&Cpp)[T::B], const double (&Cpc)[T::B], bool anchor,
+                        bool grad, double& fe, double* g, double* S0, double* S1, double* S2, double* S3) {
+    constexpr int B = T::B;
+    constexpr int LD = TeamCfg<B>::LD;
+    const int l = tm.l;
+    double e[B];
+    if (anchor) {
+#pragma unroll
+        for (int i = 0; i < B; ++i) e[i] = xc[i];
+    } else {
+        double tmp[B];
+        tmv<B, B>(tmp, PhiS, xp);
+#pragma unroll
+        for (int i = 0; i < B; ++i) e[i] = xc[i] - tmp[i];
+    }
+    {
+        double u[B];
+#pragma unroll
+        for (int i = 0; i < B; ++i) u[i] = e[i];
+        tlsolve<B, LD>(u, LQ);
+        double q = 0.0;
+#pragma unroll
+        for (int i = 0; i < B; ++i) q += u[i] * u[i];
+        if (l == 0) fe += q;
+    }
+    if (!grad) return;
+    const double jit = rp[1];
+    const double el = pick<B>(e, l);
+    double E[B], Zc[B];
+    if (anchor) {
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            E[i] = Ccc[i] + e[i] * el;
+            Zc[i] = 0.0;
+        }
+    } else {
+        double X1[B], Y1[B], ph[B], Z2[B], x1r[B], y1r[B];
+        tmv<B, B>(X1, PhiS, Cpc);  // Φ C_pc
+        tmv<B, B>(Y1, PhiS, Cpp);  // Φ C_pp
+        tsync(tm);
+        colput<B, LD>(S2, X1, l);
+        colput<B, LD>(S3, Y1, l);
+        tsync(tm);
+        rowget<B, B>(ph, PhiS, l);
+        tmv<B, LD>(Z2, S3, ph);    // Φ C_pp Φ^T
+        rowget<B, LD>(x1r, S2, l);
+        rowget<B, LD>(y1r, S3, l);  // C_pp Φ^T = (Φ C_pp)^T
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            E[i] = Ccc[i] - X1[i] - x1r[i] + Z2[i] + e[i] * el;
+            Zc[i] = Cpc[i] - y1r[i] + xp[i] * el;
+        }
+    }
+    // E - Q̃ (padding states have Q̃ = 1 and E = 0; their rows of M are never read)
+    {
+        double q[B];
+        colget<B, B>(q, QS, l);
+#pragma unroll
+        for (int i = 0; i < B; ++i) E[i] -= q[i];
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+            if (i == l && i < md.b) E[i] -= jit;
+    }
+    tsym<B>(tm, E, S2);
+    // M = Q̃^{-1}(E - Q̃)Q̃^{-1}: G = Q̃^{-1}(E - Q̃) by columns, then M = (Q̃^{-1} G^T)^T by rows
+    tlsolve<B, LD>(E, LQ);
+    tltsolve<B, LD>(E, LQ);
+    double v[B];
+    ttrans<B>(tm, v, E, S3);  // column l of G^T
+    tlsolve<B, LD>(v, LQ);
+    tltsolve<B, LD>(v, LQ);   // = row l of M
+    // symmetrise M (row l in v) and hand it to T::grad at row stride B
+    tsync(tm);
+    rowput<B, B>(S0, v, l);
+    tsync(tm);
+    {
+        double cm[B];
+        colget<B, B>(cm, S0, l);
+#pragma unroll
+        for (int i = 0; i < B; ++i) v[i] = 0.5 * (v[i] + cm[i]);
+    }
+    tsync(tm);
+    rowput<B, B>(S0, v, l);
+    // Bm = Z Q̃^{-1} = (Q̃^{-1} Z^T)^T: row l of Bm from column l of Z^T
+    if (anchor) {
+#pragma unroll
+        for (int i = 0; i < B; ++i) v[i] = 0.0;
+    } else {
+        ttrans<B>(tm, v, Zc, S2);
+        tlsolve<B, LD>(v, LQ);
+        tltsolve<B, LD>(v, LQ);
+    }
+    rowput<B, B>(S1, v, l);
+    tsync(tm);
+    if (l == 0) T::grad(md, rp, dt, PhiS, QS, S0, S1, g);
+}
+
+template <class T>
+__global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_rev0_team(
+    ModelDesc md, const double* __restrict__ params, const double* __restrict__ t, const double* __restrict__ y,
+    Geom geo, const double* __restrict__ fac, const double* __restrict__ solU, double* __restrict__ part, Outs outs,
+    unsigned long long* status, const double* __restrict__ halo, long long g0, long long g1,
+    const unsigned char* __restrict__ obs) {
+    constexpr int B = T::B;
+    using C = TeamCfg<B>;
+    constexpr int LD = C::LD;
+    constexpr int NLI = B * (B + 1) / 2, NF = NLI + B * B + B;
+    extern __shared__ double smem_team[];
+    const Team tm = make_team<C::TS>();
+    const int tid = threadIdx.x / C::TS;
+    double* R = smem_team + static_cast<size_t>(tid) * C::REV;
+    double* PhiS = R;
+    double* QS = R + C::MAT;
+    double* LQ = R + 2 * C::MAT;
+    double* LS = R + 3 * C::MAT;
+    double* XS = R + 4 * C::MAT;
+    double* YS = R + 5 * C::MAT;
+    double* S6 = R + 6 * C::MAT;
+    double* S7 = R + 7 * C::MAT;
+    double* CLLS = R + 8 * C::MAT;
+    double* xLS = R + 9 * C::MAT;
+    double* zS = xLS + C::VEC;
+    const long long g = g0 + static_cast<long long>(blockIdx.x) * C::TPC + tid;
+    if (g >= g1) return;
+    const int l = tm.l;
+    const long long K = geo.K[0], SK = K * geo.S;
+    const int s = static_cast<int>(g / K);
+    const long long c = g - s * K;
+    const long long n = geo.n[0];
+    const int m = geo.m[0];
+    const long long st = c * m, en = min(n, st + m);
+    const double* ts = t + s * n;
+    const double* ys = y + s * n;
+    const double* rp = params + static_cast<long long>(s) * md.rec_stride;
+    const double sig = rp[0], jit = rp[1], is2 = 1.0 / (sig * sig);
+    const long long gbase = static_cast<long long>(s) * n;
+    const bool hasL = c > 0 || geo.segL;
+    const bool needC = outs.need_c != 0, grad = outs.want_grad != 0;
+    double H[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) H[i] = T::H(md, i);
+    const double Hl = pick<B>(H, l);
+
+    // separators (engine.cuh load_sep): right = this chunk's last block, left = the
+    // previous chunk's (x, C_LL, C_LR)
+    const long long SnU = static_cast<long long>(geo.S) * (geo.n[1] + geo.segL), iR = g + geo.segL * (s + 1);
+    double xn[B], Cnn[B], CnL[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+        xn[i] = solU[(Sol<B>::X + i) * SnU + iR];
+        Cnn[i] = (needC && l < B) ? solU[(Sol<B>::CD + i * B + l) * SnU + iR] : 0.0;
+        // C_{n,L} = C_LR^T: column l = row l of C_LR
+        CnL[i] = (hasL && needC && l < B) ? solU[(Sol<B>::CU + l * B + i) * SnU + iR - 1] : 0.0;
+    }
+    if (l < B) {
+        xLS[l] = hasL ? solU[(Sol<B>::X + l) * SnU + iR - 1] : 0.0;
+#pragma unroll
+        for (int i = 0; i < B; ++i) CLLS[i * LD + l] = (hasL && needC) ? solU[(Sol<B>::CD + i * B + l) * SnU + iR - 1] : 0.0;
+    }
+    tsync(tm);
+
+    double fy = 0.0, fe = 0.0, noise = 0.0;
+    LogDetAcc ldq;  // log det of every Q̃ of the chunk
+    ldq.init();
+    double gr[kMaxTheta];
+    for (int p = 0; p < md.nt; ++p) gr[p] = 0.0;
+
+    auto point = [&](long long i0) {  // engine.cuh point_out for block i0 = (xn, Cnn)
+        const bool ob = !obs || obs[gbase + i0];
+        const double yv = ob ? ys[i0] : 0.0;
+        double mu = 0.0;
+#pragma unroll
+        for (int k = 0; k < B; ++k) mu += H[k] * xn[k];
+        const double rr = yv - mu;
+        if (l == 0 && ob) fy += rr * rr * is2;
+        if (l == 0 && outs.mean) outs.mean[gbase + i0] = mu;
+        if (outs.need_c) {
+            double hc = 0.0;
+#pragma unroll
+            for (int a = 0; a < B; ++a) hc += H[a] * Cnn[a];
+            double v = tsum<C::TS>(tm, Hl * hc);
+            if (l == 0) {
+                if (ob) noise += rr * rr + v;
+                if (outs.var) {
+                    if (v < -1e-10) report(status, gbase + i0, ST_NEG_VAR);
+                    if (v < 0.0) v = 0.0;  // clamp [-1e-10, 0) -> 0
+                    outs.var[gbase + i0] = outs.include_noise ? v + sig * sig : v;
+                }
+            }
+        }
+    };
+
+    for (long long j = en - 2; j >= st; --j) {
+        const long long nb = j + 1;
+        const double dt = ts[nb] - ts[j];
+        tsync(tm);
+        tmodel<T>(tm, md, rp, dt, jit, PhiS, QS, LQ, &ldq);
+        double U[B];
+        {
+            double pqp[B];
+            tassembly<B>(tm, PhiS, LQ, XS, S6, pqp, U, nullptr);
+        }
+        // factor of step j
+        const double* fp = fac + (g * m + (j - st)) * static_cast<long long>(NF);
+        double Y[B];
+        if (l < B) {
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                if (i >= l) LS[i * LD + l] = fp[i * (i + 1) / 2 + l];
+                Y[i] = hasL ? fp[NLI + i * B + l] : 0.0;
+            }
+            zS[l] = fp[NLI + B * B + l];
+        } else {
+#pragma unroll
+            for (int i = 0; i < B; ++i) Y[i] = 0.0;
+        }
+        tsync(tm);
+        double X[B];
+#pragma unroll
+        for (int i = 0; i < B; ++i) X[i] = U[i];
+        tlsolve<B, LD>(X, LS);  // X = L^{-1} U
+        colput<B, LD>(XS, X, l);
+        if (hasL) colput<B, LD>(YS, Y, l);
+        tsync(tm);
+        // back substitution: x_j = L^{-T}(z - X x_n - Y x_L)
+        double a[B], tmp[B];
+        tmv<B, LD>(tmp, XS, xn);
+#pragma unroll
+        for (int i = 0; i < B; ++i) a[i] = zS[i] - tmp[i];
+        if (hasL) {
+            double xL[B];
+#pragma unroll
+            for (int i = 0; i < B; ++i) xL[i] = xLS[i];
+            tmv<B, LD>(tmp, YS, xL);
+#pragma unroll
+            for (int i = 0; i < B; ++i) a[i] -= tmp[i];
+        }
+        double xj[B];
+#pragma unroll
+        for (int i = 0; i < B; ++i) xj[i] = a[i];
+        tltsolve<B, LD>(xj, LS);
+        double CjL[B], Cjn[B], Cjj[B];
+        if (needC) {
+            // P1 = X C_nL + Y C_LL,  P2 = X C_nn + Y C_Ln   (engine.cuh back_step)
+            double P1[B], P2[B];
+            tmv<B, LD>(P1, XS, CnL);
+            tmv<B, LD>(P2, XS, Cnn);
+            if (hasL) {
+                double q[B];
+                colget<B, LD>(q, CLLS, l);
+                tmv<B, LD>(tmp, YS, q);
+#pragma unroll
+                for (int i = 0; i < B; ++i) P1[i] += tmp[i];
+                ttrans<B>(tm, q, CnL, S6);  // column l of C_{L,n} = C_{n,L}^T
+                tmv<B, LD>(tmp, YS, q);
+#pragma unroll
+                for (int i = 0; i < B; ++i) P2[i] += tmp[i];
+            }
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                CjL[i] = P1[i];
+                Cjn[i] = P2[i];
+            }
+            tltsolve<B, LD>(CjL, LS);
+            tltsolve<B, LD>(Cjn, LS);
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                CjL[i] = -CjL[i];
+                Cjn[i] = -Cjn[i];
+            }
+            // M = I + P2 X^T + P1 Y^T (column l: P2 (row l of X) + P1 (row l of Y))
+            tsync(tm);
+            colput<B, LD>(S6, P2, l);
+            colput<B, LD>(S7, P1, l);
+            tsync(tm);
+            double M[B], r[B];
+            rowget<B, LD>(r, XS, l);
+            tmv<B, LD>(M, S6, r);
+            if (hasL) {
+                rowget<B, LD>(r, YS, l);
+                tmv<B, LD>(tmp, S7, r);
+#pragma unroll
+                for (int i = 0; i < B; ++i) M[i] += tmp[i];
+            }
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+                if (i == l) M[i] += 1.0;
+            tsym<B>(tm, M, S6);
+            // C_jj = L^{-T} M L^{-1} = L^{-T} (L^{-T} M)^T
+            tltsolve<B, LD>(M, LS);
+            ttrans<B>(tm, Cjj, M, S7);
+            tltsolve<B, LD>(Cjj, LS);
+            tsym<B>(tm, Cjj, S6);
+        } else {
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                CjL[i] = 0.0;
+                Cjn[i] = 0.0;
+                Cjj[i] = 0.0;
+            }
+        }
+        point(nb);
+        tstep_terms<T>(tm, md, rp, dt, PhiS, QS, LQ, xn, Cnn, xj, Cjj, Cjn, false, grad, fe, gr, XS, YS, S6, S7);
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            xn[i] = xj[i];
+            Cnn[i] = Cjj[i];
+            CnL[i] = CjL[i];
+        }
+    }
+    // block st: previous block is the left separator (or the anchor at st = 0)
+    point(st);
+    {
+        const bool anchor = st == 0 && !geo.segL;
+        const double dt = anchor ? -1.0 : ts[st] - (st > 0 ? ts[st - 1] : halo[2 * s]);
+        tsync(tm);
+        tmodel<T>(tm, md, rp, dt, jit, PhiS, QS, LQ, &ldq);
+        double xL[B], CLL[B], CLs[B];
+#pragma unroll
+        for (int i = 0; i < B; ++i) xL[i] = xLS[i];
+        colget<B, LD>(CLL, CLLS, l);
+        ttrans<B>(tm, CLs, CnL, S6);  // C_{L,st} = C_{st,L}^T
+        tstep_terms<T>(tm, md, rp, dt, PhiS, QS, LQ, xn, Cnn, xL, CLL, CLs, anchor, grad, fe, gr, XS, YS, S6, S7);
+    }
+    if (l == 0) {
+        part[P_FITY * SK + g] = fy;
+        part[P_FITE * SK + g] = fe;
+        part[P_LDQ * SK + g] = ldq.logdet();
+        part[P_NOISE * SK + g] = noise;
+        for (int p = 0; p < md.nt; ++p) part[(P_GRAD + p) * SK + g] = gr[p];
+    }
+}
+
+}  // namespace spingp_dev
