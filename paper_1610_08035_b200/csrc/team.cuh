@@ -41,8 +41,8 @@ struct TeamCfg {
     static constexpr int LD = B + 1;             // odd smem row stride
     static constexpr int MAT = B * LD;           // doubles per staged block
     static constexpr int VEC = (B + 1) & ~1;
-    static constexpr int FWD = 6 * MAT + 2 * VEC;   // per-team smem, forward (doubles)
-    static constexpr int REV = 9 * MAT + 2 * VEC;   // per-team smem, reverse
+    static constexpr int FWD = 10 * MAT + VEC;      // per-team smem, forward (doubles)
+    static constexpr int REV = 10 * MAT + 4 * VEC;  // per-team smem, reverse
     static constexpr int CTA = B <= 8 ? 128 : 64;   // threads per CTA
     static constexpr int TPC = CTA / TS;            // teams per CTA
 };
@@ -225,15 +225,20 @@ TP_INL bool tmodel(const Team& tm, const ModelDesc& md, const double* rp, double
 //   PQP = Φ^T Q̃^{-1} Φ = Z^T Z (Z = L_Q^{-1} Φ)   and   U = -Φ^T Q̃^{-1} = -(L_Q^{-T} Z)^T;
 // optionally column l of W0 = U^T = -Q̃^{-1} Φ (the first block's left coupling).
 template <int B>
-TP_INL void tassembly(const Team& tm, const double* PhiS, const double* LQ, double* ZS, double* WS, double (&pqp)[B],
+TP_INL void tassembly(const Team& tm, const double* PhiS, const double* LQ, double* ZS, double* WS, double* pqp,
                       double (&U)[B], double* W0) {
     constexpr int LD = TeamCfg<B>::LD;
     double z[B];
     colget<B, B>(z, PhiS, tm.l);
     tlsolve<B, LD>(z, LQ);
-    colput<B, LD>(ZS, z, tm.l);
-    tsync(tm);
-    tmtv<B, LD>(pqp, ZS, z);
+    if (pqp) {
+        colput<B, LD>(ZS, z, tm.l);
+        tsync(tm);
+        double q[B];
+        tmtv<B, LD>(q, ZS, z);
+#pragma unroll
+        for (int i = 0; i < B; ++i) pqp[i] = q[i];
+    }
     tltsolve<B, LD>(z, LQ);  // column l of Q̃^{-1} Φ
     if (W0)
 #pragma unroll
@@ -253,6 +258,17 @@ TP_INL void tqinv(const Team& tm, double (&q)[B], const double* LQ, double* scra
     tlsolve<B, LD>(q, LQ);
     tltsolve<B, LD>(q, LQ);
     tsym<B>(tm, q, scratch);
+}
+
+// A lane-private column kept in shared memory between uses (frees registers; lane l
+// only ever touches column l, so no team barrier is needed around these)
+template <int B>
+TP_INL void pget(double (&c)[B], const double* M, int l) {
+    colget<B, TeamCfg<B>::LD>(c, M, l);
+}
+template <int B>
+TP_INL void pput(double* M, const double (&c)[B], int l) {
+    colput<B, TeamCfg<B>::LD>(M, c, l);
 }
 
 // ======================================================== forward, level 0 ====
@@ -276,8 +292,11 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_fwd0_team(
     double* LS = R + 3 * C::MAT;    // chol(S)
     double* XS = R + 4 * C::MAT;
     double* YS = R + 5 * C::MAT;
-    double* vS = R + 6 * C::MAT;    // rc gather
-    double* hS = vS + C::VEC;       // accrL gather
+    double* QiS = R + 6 * C::MAT;   // lane-private carried columns: Q̃^{-1} of the current block,
+    double* WS = R + 7 * C::MAT;    //   the left coupling W,
+    double* TcS = R + 8 * C::MAT;   //   the Schur update T = X^T X,
+    double* AcS = R + 9 * C::MAT;   //   acc_LL
+    double* vS = R + 10 * C::MAT;   // rc (vector)
     const long long g = g0 + static_cast<long long>(blockIdx.x) * C::TPC + tid;
     if (g >= g1) return;
     const int l = tm.l;
@@ -294,9 +313,6 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_fwd0_team(
     const long long gbase = static_cast<long long>(s) * n;
     const bool hasL = c > 0 || geo.segL;
     const double Hl = l < B ? T::H(md, l) : 0.0;
-    double H[B];
-#pragma unroll
-    for (int i = 0; i < B; ++i) H[i] = T::H(md, i);
 
     double dt = -1.0;
     if (st > 0 || geo.segL) {
@@ -310,18 +326,22 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_fwd0_team(
         if (l == 0) report(status, gbase + st, ST_SINGULAR_Q);
         return;
     }
-    double Qinv[B], W[B], Tc[B], acc[B], rc[B];
-    tqinv<B>(tm, Qinv, LQ, XS);
+    {
+        double q[B];
+        tqinv<B>(tm, q, LQ, XS);
+        pput<B>(QiS, q, l);
 #pragma unroll
-    for (int i = 0; i < B; ++i) {
-        W[i] = 0.0;
-        Tc[i] = 0.0;
-        acc[i] = 0.0;
-        rc[i] = 0.0;
-    }
-    if (hasL) {  // P_{st, st-1} = U_{st-1}^T = -Q̃_st^{-1} Φ_st
-        double pqp[B], U[B];
-        tassembly<B>(tm, PhiS, LQ, XS, YS, pqp, U, W);
+        for (int i = 0; i < B; ++i) q[i] = 0.0;
+        pput<B>(TcS, q, l);
+        pput<B>(AcS, q, l);
+        if (hasL) {  // P_{st, st-1} = U_{st-1}^T = -Q̃_st^{-1} Φ_st
+            double U[B], W[B];
+            tassembly<B>(tm, PhiS, LQ, XS, YS, nullptr, U, W);
+            pput<B>(WS, W, l);
+        } else {
+            pput<B>(WS, q, l);
+        }
+        if (l < B) vS[l] = 0.0;
     }
     double accrL = 0.0;  // component l of the carried left rhs
     LogDetAcc piv;
@@ -346,38 +366,45 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_fwd0_team(
             if (l == 0) report(status, gbase + j, ST_BAD_ARG);
             return;
         }
+        {
+            double q[B], tc[B];
+            pget<B>(q, QiS, l);
+            pget<B>(tc, TcS, l);
 #pragma unroll
-        for (int i = 0; i < B; ++i) D[i] = (D[i] + (Qinv[i] + wo * (H[i] * Hl * is2))) - Tc[i];
-        // S = D - T; pivot symmetrisation — D and T are exactly symmetric
-        // up to Q̃^{-1}, which tqinv symmetrised already
+            for (int i = 0; i < B; ++i) D[i] = (D[i] + (q[i] + wo * (T::H(md, i) * Hl * is2))) - tc[i];
+        }
+        // S = D - T (Q̃^{-1} symmetrised by tqinv; PQP and T exactly symmetric)
         if (!tchol<B>(tm, D, LS, &piv)) {
             if (l == 0) report(status, gbase + j, ST_NOT_PD);
             return;
         }
-        tqinv<B>(tm, Qinv, LQ, PhiS);  // Q̃_{j+1}^{-1}: the next block's diagonal term
+        {
+            double q[B];
+            tqinv<B>(tm, q, LQ, PhiS);  // Q̃_{j+1}^{-1}: the next block's diagonal term
+            pput<B>(QiS, q, l);
+        }
         double z[B];
 #pragma unroll
-        for (int i = 0; i < B; ++i) z[i] = H[i] * yj * is2 - rc[i];
+        for (int i = 0; i < B; ++i) z[i] = T::H(md, i) * yj * is2 - vS[i];
         tlsolve<B, LD>(z, LS);
         tlsolve<B, LD>(U, LS);  // X = L^{-1} U
-        if (hasL) tlsolve<B, LD>(W, LS);  // Y = L^{-1} W
+        double Y[B];
+        if (hasL) {
+            pget<B>(Y, WS, l);
+            tlsolve<B, LD>(Y, LS);  // Y = L^{-1} W
+        }
         tsync(tm);
         colput<B, LD>(XS, U, l);
-        if (hasL) colput<B, LD>(YS, W, l);
+        if (hasL) colput<B, LD>(YS, Y, l);
         tsync(tm);
-        tmtv<B, LD>(Tc, XS, U);  // T' = X^T X
-        double rcl = 0.0, yz = 0.0;
+        {
+            double tc[B];
+            tmtv<B, LD>(tc, XS, U);  // T' = X^T X
+            pput<B>(TcS, tc, l);
+        }
+        double rcl = 0.0;
 #pragma unroll
         for (int i = 0; i < B; ++i) rcl = fma(U[i], z[i], rcl);  // (X^T z)_l
-        if (hasL) {
-            double G[B];
-            tmtv<B, LD>(G, YS, W);  // Y^T Y
-#pragma unroll
-            for (int i = 0; i < B; ++i) acc[i] -= G[i];
-#pragma unroll
-            for (int i = 0; i < B; ++i) yz = fma(W[i], z[i], yz);
-            accrL -= yz;
-        }
         // factor of step j for the reverse sweep: L (packed, inverted pivots), Y, z
         double* fp = fac + (g * m + (j - st)) * static_cast<long long>(NF);
         if (l < B) {
@@ -386,25 +413,35 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_fwd0_team(
                 if (i >= l) fp[i * (i + 1) / 2 + l] = LS[i * LD + l];
             if (hasL)
 #pragma unroll
-                for (int i = 0; i < B; ++i) fp[NLI + i * B + l] = W[i];
+                for (int i = 0; i < B; ++i) fp[NLI + i * B + l] = Y[i];
             fp[NLI + B * B + l] = pick<B>(z, l);
         }
-        if (hasL) {  // W' = -X^T Y
-            double G[B];
-            tmtv<B, LD>(G, XS, W);
+        if (hasL) {
+            double G[B], a[B];
+            tmtv<B, LD>(G, YS, Y);  // acc_LL -= Y^T Y
+            pget<B>(a, AcS, l);
 #pragma unroll
-            for (int i = 0; i < B; ++i) W[i] = -G[i];
+            for (int i = 0; i < B; ++i) a[i] -= G[i];
+            pput<B>(AcS, a, l);
+            double yz = 0.0;
+#pragma unroll
+            for (int i = 0; i < B; ++i) yz = fma(Y[i], z[i], yz);
+            accrL -= yz;
+            tmtv<B, LD>(G, XS, Y);  // W' = -X^T Y
+#pragma unroll
+            for (int i = 0; i < B; ++i) G[i] = -G[i];
+            pput<B>(WS, G, l);
         }
+        tsync(tm);
         if (l < B) vS[l] = rcl;
         tsync(tm);
-#pragma unroll
-        for (int i = 0; i < B; ++i) rc[i] = vS[i];
     }
     // separator R = en - 1
     const double woR = (!obs || obs[gbase + en - 1]) ? 1.0 : 0.0;
     double D[B];
+    pget<B>(D, QiS, l);
 #pragma unroll
-    for (int i = 0; i < B; ++i) D[i] = Qinv[i] + woR * (H[i] * Hl * is2);
+    for (int i = 0; i < B; ++i) D[i] += woR * (T::H(md, i) * Hl * is2);
     if (en < n || geo.segR) {
         const double dte = (en < n ? ts[en] : halo[2 * s + 1]) - ts[en - 1];
         if (!(dte > 0.0) || !isfinite(dte)) {
@@ -429,13 +466,17 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_fwd0_team(
     // record (engine.cuh write_rec layout, component-major over chunks)
     double* r = rec + g;
     if (l < B) {
+        double tc[B], a[B], w[B];
+        pget<B>(tc, TcS, l);
+        pget<B>(a, AcS, l);
+        pget<B>(w, WS, l);
 #pragma unroll
         for (int i = 0; i < B; ++i) {
-            r[(Rec<B>::RDIAG + i * B + l) * SK] = D[i] - Tc[i];
-            r[(Rec<B>::LDIAG + i * B + l) * SK] = acc[i];
-            r[(Rec<B>::LR + l * B + i) * SK] = hasL ? W[i] : 0.0;  // LR = W^T
+            r[(Rec<B>::RDIAG + i * B + l) * SK] = D[i] - tc[i];
+            r[(Rec<B>::LDIAG + i * B + l) * SK] = a[i];
+            r[(Rec<B>::LR + l * B + i) * SK] = hasL ? w[i] : 0.0;  // LR = W^T
         }
-        r[(Rec<B>::RRHS + l) * SK] = Hl * yR * is2 - pick<B>(rc, l);
+        r[(Rec<B>::RRHS + l) * SK] = Hl * yR * is2 - vS[l];
         r[(Rec<B>::LRHS + l) * SK] = accrL;
     }
     if (l == 0) {
@@ -448,13 +489,13 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_fwd0_team(
 
 // Likelihood / gradient terms of one step (engine.cuh step_terms) for the team: the
 // current block (xc, column l of Ccc), the previous block (xp, column l of Cpp) and
-// column l of Cpc = C_{p,c}; Φ, Q (raw) at PhiS, QS (stride B), L_Q at LQ.  Scratch
-// blocks S0..S3 (S0, S1 also the stride-B M and Bm handed to T::grad).  fe and g are
-// accumulated by lane 0.
+// column l of Cpc = C_{p,c}; Φ, Q (raw) at PhiS, QS (stride B), L_Q at LQ; xc, xp are
+// smem vectors.  Scratch blocks S0..S3 (S0, S1 also the stride-B M and Bm handed to
+// T::grad).  fe and g are accumulated by lane 0.
 template <class T>
 TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, double dt, const double* PhiS,
-                        const double* QS, const double* LQ, const double (&xc)[T::B], const double (&Ccc)[T::B],
-                        const double (&xp)[T::B], const double (&Cpp)[T::B], const double (&Cpc)[T::B], bool anchor,
+                        const double* QS, const double* LQ, const double* xcS, const double (&Ccc)[T::B],
+                        const double* xpS, const double (&Cpp)[T::B], const double (&Cpc)[T::B], bool anchor,
                         bool grad, double& fe, double* g, double* S0, double* S1, double* S2, double* S3) {
     constexpr int B = T::B;
     constexpr int LD = TeamCfg<B>::LD;
@@ -462,12 +503,14 @@ TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, d
     double e[B];
     if (anchor) {
 #pragma unroll
-        for (int i = 0; i < B; ++i) e[i] = xc[i];
+        for (int i = 0; i < B; ++i) e[i] = xcS[i];
     } else {
-        double tmp[B];
-        tmv<B, B>(tmp, PhiS, xp);
+        double xp[B];
 #pragma unroll
-        for (int i = 0; i < B; ++i) e[i] = xc[i] - tmp[i];
+        for (int i = 0; i < B; ++i) xp[i] = xpS[i];
+        tmv<B, B>(e, PhiS, xp);
+#pragma unroll
+        for (int i = 0; i < B; ++i) e[i] = xcS[i] - e[i];
     }
     {
         double u[B];
@@ -482,30 +525,30 @@ TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, d
     if (!grad) return;
     const double jit = rp[1];
     const double el = pick<B>(e, l);
-    double E[B], Zc[B];
+    double E[B];
     if (anchor) {
 #pragma unroll
-        for (int i = 0; i < B; ++i) {
-            E[i] = Ccc[i] + e[i] * el;
-            Zc[i] = 0.0;
-        }
+        for (int i = 0; i < B; ++i) E[i] = Ccc[i] + e[i] * el;
     } else {
-        double X1[B], Y1[B], ph[B], Z2[B], x1r[B], y1r[B];
-        tmv<B, B>(X1, PhiS, Cpc);  // Φ C_pc
-        tmv<B, B>(Y1, PhiS, Cpp);  // Φ C_pp
-        tsync(tm);
-        colput<B, LD>(S2, X1, l);
-        colput<B, LD>(S3, Y1, l);
-        tsync(tm);
-        rowget<B, B>(ph, PhiS, l);
-        tmv<B, LD>(Z2, S3, ph);    // Φ C_pp Φ^T
-        rowget<B, LD>(x1r, S2, l);
-        rowget<B, LD>(y1r, S3, l);  // C_pp Φ^T = (Φ C_pp)^T
+        {
+            double X1[B], Y1[B];
+            tmv<B, B>(X1, PhiS, Cpc);  // Φ C_pc
+            tmv<B, B>(Y1, PhiS, Cpp);  // Φ C_pp
+            tsync(tm);
+            colput<B, LD>(S2, X1, l);
+            colput<B, LD>(S3, Y1, l);
 #pragma unroll
-        for (int i = 0; i < B; ++i) {
-            E[i] = Ccc[i] - X1[i] - x1r[i] + Z2[i] + e[i] * el;
-            Zc[i] = Cpc[i] - y1r[i] + xp[i] * el;
+            for (int i = 0; i < B; ++i) E[i] = Ccc[i] - X1[i];
         }
+        tsync(tm);
+        double r[B], ph[B];
+        rowget<B, LD>(r, S2, l);
+        rowget<B, B>(ph, PhiS, l);
+#pragma unroll
+        for (int i = 0; i < B; ++i) E[i] -= r[i];
+        tmv<B, LD>(r, S3, ph);  // Φ C_pp Φ^T
+#pragma unroll
+        for (int i = 0; i < B; ++i) E[i] = (E[i] + r[i]) + e[i] * el;
     }
     // E - Q̃ (padding states have Q̃ = 1 and E = 0; their rows of M are never read)
     {
@@ -517,36 +560,44 @@ TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, d
         for (int i = 0; i < B; ++i)
             if (i == l && i < md.b) E[i] -= jit;
     }
-    tsym<B>(tm, E, S2);
+    tsym<B>(tm, E, S0);
     // M = Q̃^{-1}(E - Q̃)Q̃^{-1}: G = Q̃^{-1}(E - Q̃) by columns, then M = (Q̃^{-1} G^T)^T by rows
     tlsolve<B, LD>(E, LQ);
     tltsolve<B, LD>(E, LQ);
-    double v[B];
-    ttrans<B>(tm, v, E, S3);  // column l of G^T
-    tlsolve<B, LD>(v, LQ);
-    tltsolve<B, LD>(v, LQ);   // = row l of M
-    // symmetrise M (row l in v) and hand it to T::grad at row stride B
-    tsync(tm);
-    rowput<B, B>(S0, v, l);
-    tsync(tm);
     {
+        double v[B];
+        ttrans<B>(tm, v, E, S1);  // column l of G^T
+        tlsolve<B, LD>(v, LQ);
+        tltsolve<B, LD>(v, LQ);   // = row l of M
+        // symmetrise M (row l in v) and hand it to T::grad at row stride B
+        tsync(tm);
+        rowput<B, B>(S0, v, l);
+        tsync(tm);
         double cm[B];
         colget<B, B>(cm, S0, l);
 #pragma unroll
         for (int i = 0; i < B; ++i) v[i] = 0.5 * (v[i] + cm[i]);
+        tsync(tm);
+        rowput<B, B>(S0, v, l);
     }
-    tsync(tm);
-    rowput<B, B>(S0, v, l);
-    // Bm = Z Q̃^{-1} = (Q̃^{-1} Z^T)^T: row l of Bm from column l of Z^T
-    if (anchor) {
+    // Bm = Z Q̃^{-1} = (Q̃^{-1} Z^T)^T with Z = C_pc - C_pp Φ^T + x_p e^T: row l of Bm
+    // from column l of Z^T = row l of Z
+    {
+        double v[B];
+        if (anchor) {
 #pragma unroll
-        for (int i = 0; i < B; ++i) v[i] = 0.0;
-    } else {
-        ttrans<B>(tm, v, Zc, S2);
-        tlsolve<B, LD>(v, LQ);
-        tltsolve<B, LD>(v, LQ);
+            for (int i = 0; i < B; ++i) v[i] = 0.0;
+        } else {
+            double y1r[B];
+            rowget<B, LD>(y1r, S3, l);  // C_pp Φ^T = (Φ C_pp)^T: column l = row l of Φ C_pp
+#pragma unroll
+            for (int i = 0; i < B; ++i) v[i] = Cpc[i] - y1r[i] + xpS[i] * el;
+            ttrans<B>(tm, v, v, S2);
+            tlsolve<B, LD>(v, LQ);
+            tltsolve<B, LD>(v, LQ);
+        }
+        rowput<B, B>(S1, v, l);
     }
-    rowput<B, B>(S1, v, l);
     tsync(tm);
     if (l == 0) T::grad(md, rp, dt, PhiS, QS, S0, S1, g);
 }
@@ -573,8 +624,11 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_rev0_team(
     double* YS = R + 5 * C::MAT;
     double* S6 = R + 6 * C::MAT;
     double* S7 = R + 7 * C::MAT;
-    double* CLLS = R + 8 * C::MAT;
-    double* xLS = R + 9 * C::MAT;
+    double* CnnS = R + 8 * C::MAT;  // C_{n,n}: lane-private columns
+    double* CnLS = R + 9 * C::MAT;  // C_{n,L}: columns written lane-privately, rows read after a barrier
+    double* xnS = R + 10 * C::MAT;  // x_n, x_j (swapped every step), x_L, z (vectors)
+    double* xjS = xnS + C::VEC;
+    double* xLS = xjS + C::VEC;
     double* zS = xLS + C::VEC;
     const long long g = g0 + static_cast<long long>(blockIdx.x) * C::TPC + tid;
     if (g >= g1) return;
@@ -592,27 +646,22 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_rev0_team(
     const long long gbase = static_cast<long long>(s) * n;
     const bool hasL = c > 0 || geo.segL;
     const bool needC = outs.need_c != 0, grad = outs.want_grad != 0;
-    double H[B];
-#pragma unroll
-    for (int i = 0; i < B; ++i) H[i] = T::H(md, i);
-    const double Hl = pick<B>(H, l);
+    const double Hl = l < B ? T::H(md, l) : 0.0;
 
     // separators (engine.cuh load_sep): right = this chunk's last block, left = the
     // previous chunk's (x, C_LL, C_LR)
     const long long SnU = static_cast<long long>(geo.S) * (geo.n[1] + geo.segL), iR = g + geo.segL * (s + 1);
-    double xn[B], Cnn[B], CnL[B];
-#pragma unroll
-    for (int i = 0; i < B; ++i) {
-        xn[i] = solU[(Sol<B>::X + i) * SnU + iR];
-        Cnn[i] = (needC && l < B) ? solU[(Sol<B>::CD + i * B + l) * SnU + iR] : 0.0;
-        // C_{n,L} = C_LR^T: column l = row l of C_LR
-        CnL[i] = (hasL && needC && l < B) ? solU[(Sol<B>::CU + l * B + i) * SnU + iR - 1] : 0.0;
-    }
     if (l < B) {
+        xnS[l] = solU[(Sol<B>::X + l) * SnU + iR];
         xLS[l] = hasL ? solU[(Sol<B>::X + l) * SnU + iR - 1] : 0.0;
 #pragma unroll
-        for (int i = 0; i < B; ++i) CLLS[i * LD + l] = (hasL && needC) ? solU[(Sol<B>::CD + i * B + l) * SnU + iR - 1] : 0.0;
+        for (int i = 0; i < B; ++i) {
+            CnnS[i * LD + l] = needC ? solU[(Sol<B>::CD + i * B + l) * SnU + iR] : 0.0;
+            // C_{n,L} = C_LR^T: column l = row l of C_LR
+            CnLS[i * LD + l] = (hasL && needC) ? solU[(Sol<B>::CU + l * B + i) * SnU + iR - 1] : 0.0;
+        }
     }
+    const double* CLLg = solU + Sol<B>::CD * SnU + iR - 1;  // C_LL[i][l] at CLLg[(i * B + l) * SnU]
     tsync(tm);
 
     double fy = 0.0, fe = 0.0, noise = 0.0;
@@ -621,19 +670,20 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_rev0_team(
     double gr[kMaxTheta];
     for (int p = 0; p < md.nt; ++p) gr[p] = 0.0;
 
-    auto point = [&](long long i0) {  // engine.cuh point_out for block i0 = (xn, Cnn)
+    // engine.cuh point_out for block i0 with mean x (smem vector) and column l of C
+    auto point = [&](long long i0, const double* xS, const double (&Cc)[B]) {
         const bool ob = !obs || obs[gbase + i0];
         const double yv = ob ? ys[i0] : 0.0;
         double mu = 0.0;
 #pragma unroll
-        for (int k = 0; k < B; ++k) mu += H[k] * xn[k];
+        for (int k = 0; k < B; ++k) mu += T::H(md, k) * xS[k];
         const double rr = yv - mu;
         if (l == 0 && ob) fy += rr * rr * is2;
         if (l == 0 && outs.mean) outs.mean[gbase + i0] = mu;
         if (outs.need_c) {
             double hc = 0.0;
 #pragma unroll
-            for (int a = 0; a < B; ++a) hc += H[a] * Cnn[a];
+            for (int a = 0; a < B; ++a) hc += T::H(md, a) * Cc[a];
             double v = tsum<C::TS>(tm, Hl * hc);
             if (l == 0) {
                 if (ob) noise += rr * rr + v;
@@ -651,11 +701,8 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_rev0_team(
         const double dt = ts[nb] - ts[j];
         tsync(tm);
         tmodel<T>(tm, md, rp, dt, jit, PhiS, QS, LQ, &ldq);
-        double U[B];
-        {
-            double pqp[B];
-            tassembly<B>(tm, PhiS, LQ, XS, S6, pqp, U, nullptr);
-        }
+        double X[B];
+        tassembly<B>(tm, PhiS, LQ, XS, S6, nullptr, X, nullptr);  // X <- U
         // factor of step j
         const double* fp = fac + (g * m + (j - st)) * static_cast<long long>(NF);
         double Y[B];
@@ -671,70 +718,66 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_rev0_team(
             for (int i = 0; i < B; ++i) Y[i] = 0.0;
         }
         tsync(tm);
-        double X[B];
-#pragma unroll
-        for (int i = 0; i < B; ++i) X[i] = U[i];
         tlsolve<B, LD>(X, LS);  // X = L^{-1} U
         colput<B, LD>(XS, X, l);
         if (hasL) colput<B, LD>(YS, Y, l);
         tsync(tm);
         // back substitution: x_j = L^{-T}(z - X x_n - Y x_L)
-        double a[B], tmp[B];
-        tmv<B, LD>(tmp, XS, xn);
+        {
+            double a[B], tmp[B], v[B];
 #pragma unroll
-        for (int i = 0; i < B; ++i) a[i] = zS[i] - tmp[i];
-        if (hasL) {
-            double xL[B];
+            for (int i = 0; i < B; ++i) v[i] = xnS[i];
+            tmv<B, LD>(tmp, XS, v);
 #pragma unroll
-            for (int i = 0; i < B; ++i) xL[i] = xLS[i];
-            tmv<B, LD>(tmp, YS, xL);
+            for (int i = 0; i < B; ++i) a[i] = zS[i] - tmp[i];
+            if (hasL) {
 #pragma unroll
-            for (int i = 0; i < B; ++i) a[i] -= tmp[i];
+                for (int i = 0; i < B; ++i) v[i] = xLS[i];
+                tmv<B, LD>(tmp, YS, v);
+#pragma unroll
+                for (int i = 0; i < B; ++i) a[i] -= tmp[i];
+            }
+            tltsolve<B, LD>(a, LS);
+            if (l < B) xjS[l] = pick<B>(a, l);
         }
-        double xj[B];
-#pragma unroll
-        for (int i = 0; i < B; ++i) xj[i] = a[i];
-        tltsolve<B, LD>(xj, LS);
-        double CjL[B], Cjn[B], Cjj[B];
+        double Cjn[B], Cjj[B];
         if (needC) {
             // P1 = X C_nL + Y C_LL,  P2 = X C_nn + Y C_Ln   (engine.cuh back_step)
-            double P1[B], P2[B];
-            tmv<B, LD>(P1, XS, CnL);
-            tmv<B, LD>(P2, XS, Cnn);
+            double P[B], tmp[B], q[B];
+            pget<B>(q, CnLS, l);
+            tmv<B, LD>(P, XS, q);
             if (hasL) {
-                double q[B];
-                colget<B, LD>(q, CLLS, l);
+#pragma unroll
+                for (int i = 0; i < B; ++i) q[i] = l < B ? CLLg[(i * B + l) * SnU] : 0.0;
                 tmv<B, LD>(tmp, YS, q);
 #pragma unroll
-                for (int i = 0; i < B; ++i) P1[i] += tmp[i];
-                ttrans<B>(tm, q, CnL, S6);  // column l of C_{L,n} = C_{n,L}^T
+                for (int i = 0; i < B; ++i) P[i] += tmp[i];
+            }
+            colput<B, LD>(S7, P, l);  // P1 (S7 free: its last readers passed two barriers)
+            pget<B>(q, CnnS, l);
+            tmv<B, LD>(Cjn, XS, q);
+            if (hasL) {
+                rowget<B, LD>(q, CnLS, l);  // column l of C_{L,n} = row l of C_{n,L}
                 tmv<B, LD>(tmp, YS, q);
 #pragma unroll
-                for (int i = 0; i < B; ++i) P2[i] += tmp[i];
+                for (int i = 0; i < B; ++i) Cjn[i] += tmp[i];
             }
+            colput<B, LD>(S6, Cjn, l);  // P2
+            tsync(tm);                  // all rows of C_{n,L} read; P1, P2 staged
+            tltsolve<B, LD>(P, LS);
 #pragma unroll
-            for (int i = 0; i < B; ++i) {
-                CjL[i] = P1[i];
-                Cjn[i] = P2[i];
-            }
-            tltsolve<B, LD>(CjL, LS);
+            for (int i = 0; i < B; ++i) P[i] = -P[i];
+            pput<B>(CnLS, P, l);  // C_{j,L}: the next step's C_{n,L}
             tltsolve<B, LD>(Cjn, LS);
 #pragma unroll
-            for (int i = 0; i < B; ++i) {
-                CjL[i] = -CjL[i];
-                Cjn[i] = -Cjn[i];
-            }
+            for (int i = 0; i < B; ++i) Cjn[i] = -Cjn[i];
             // M = I + P2 X^T + P1 Y^T (column l: P2 (row l of X) + P1 (row l of Y))
-            tsync(tm);
-            colput<B, LD>(S6, P2, l);
-            colput<B, LD>(S7, P1, l);
-            tsync(tm);
-            double M[B], r[B];
-            rowget<B, LD>(r, XS, l);
-            tmv<B, LD>(M, S6, r);
+            double M[B];
+            rowget<B, LD>(q, XS, l);
+            tmv<B, LD>(M, S6, q);
             if (hasL) {
-                rowget<B, LD>(r, YS, l);
-                tmv<B, LD>(tmp, S7, r);
+                rowget<B, LD>(q, YS, l);
+                tmv<B, LD>(tmp, S7, q);
 #pragma unroll
                 for (int i = 0; i < B; ++i) M[i] += tmp[i];
             }
@@ -750,33 +793,37 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_rev0_team(
         } else {
 #pragma unroll
             for (int i = 0; i < B; ++i) {
-                CjL[i] = 0.0;
                 Cjn[i] = 0.0;
                 Cjj[i] = 0.0;
             }
         }
-        point(nb);
-        tstep_terms<T>(tm, md, rp, dt, PhiS, QS, LQ, xn, Cnn, xj, Cjj, Cjn, false, grad, fe, gr, XS, YS, S6, S7);
-#pragma unroll
-        for (int i = 0; i < B; ++i) {
-            xn[i] = xj[i];
-            Cnn[i] = Cjj[i];
-            CnL[i] = CjL[i];
+        tsync(tm);
+        {
+            double q[B];
+            pget<B>(q, CnnS, l);
+            point(nb, xnS, q);
+            tstep_terms<T>(tm, md, rp, dt, PhiS, QS, LQ, xnS, q, xjS, Cjj, Cjn, false, grad, fe, gr, XS, YS, S6, S7);
         }
+        pput<B>(CnnS, Cjj, l);
+        tsync(tm);
+        double* sw = xnS;  // x_n <- x_j
+        xnS = xjS;
+        xjS = sw;
     }
     // block st: previous block is the left separator (or the anchor at st = 0)
-    point(st);
     {
+        double q[B];
+        pget<B>(q, CnnS, l);
+        point(st, xnS, q);
         const bool anchor = st == 0 && !geo.segL;
         const double dt = anchor ? -1.0 : ts[st] - (st > 0 ? ts[st - 1] : halo[2 * s]);
         tsync(tm);
         tmodel<T>(tm, md, rp, dt, jit, PhiS, QS, LQ, &ldq);
-        double xL[B], CLL[B], CLs[B];
+        double CLL[B], CLs[B];
 #pragma unroll
-        for (int i = 0; i < B; ++i) xL[i] = xLS[i];
-        colget<B, LD>(CLL, CLLS, l);
-        ttrans<B>(tm, CLs, CnL, S6);  // C_{L,st} = C_{st,L}^T
-        tstep_terms<T>(tm, md, rp, dt, PhiS, QS, LQ, xn, Cnn, xL, CLL, CLs, anchor, grad, fe, gr, XS, YS, S6, S7);
+        for (int i = 0; i < B; ++i) CLL[i] = (hasL && needC && l < B) ? CLLg[(i * B + l) * SnU] : 0.0;
+        rowget<B, LD>(CLs, CnLS, l);  // C_{L,st} = C_{st,L}^T: column l = row l of C_{st,L}
+        tstep_terms<T>(tm, md, rp, dt, PhiS, QS, LQ, xnS, q, xLS, CLL, CLs, anchor, grad, fe, gr, XS, YS, S6, S7);
     }
     if (l == 0) {
         part[P_FITY * SK + g] = fy;
