@@ -470,6 +470,155 @@ SP_DEV void qp_grad(int o, int J, const double* lr, double dt, const double* Phi
     }
 }
 
+
+#ifndef SPINGP_HOST_EMU
+// ---------------------------------------------------- team-parallel leaves --
+// The same closed forms, with the independent pieces of one leaf (EQ rotation blocks and
+// (p, q) covariance pairs, QP harmonics) spread over the `nl` lanes of a team (team.cuh):
+// lane `ln` computes pieces ln, ln + nl, ...  The block has been zero-filled by the team.
+template <int LD>
+SP_DEV void eq_block_team(int o, int J, const double* ac, const double* lr, double dt, double* Phi, double* Q,
+                          int ln, int nl) {
+    const double var = lr[0];
+    const double* P1 = ac + J;
+    const double s0 = P1[J * J];
+    if (dt < 0.0) {
+        for (int k = ln; k < J * J; k += nl) Q[(o + k / J) * LD + o + k % J] = var * P1[k];
+        return;
+    }
+    const double tau = dt * lr[2];
+    for (int p = ln; p < J / 2; p += nl) {
+        const double a = ac[2 * p], c = ac[2 * p + 1];
+        const double rho = exp(a * tau);
+        double sn, cs;
+        sincos(c * tau, &sn, &cs);
+        const int k = o + 2 * p;
+        Phi[k * LD + k] = rho * cs;
+        Phi[k * LD + k + 1] = rho * sn;
+        Phi[(k + 1) * LD + k] = -rho * sn;
+        Phi[(k + 1) * LD + k + 1] = rho * cs;
+    }
+    const double w = 0.5 * var * s0;
+    const int np = (J / 2) * (J / 2 + 1) / 2;
+    for (int k = ln; k < np; k += nl) {
+        int p = 0;
+        while ((p + 1) * (p + 2) / 2 <= k) ++p;
+        const int q = k - p * (p + 1) / 2;
+        const double al = ac[2 * p] + ac[2 * q];
+        double cm, sm, cp, sp;
+        phi1_int(al, ac[2 * p + 1] - ac[2 * q + 1], tau, cm, sm);
+        phi1_int(al, ac[2 * p + 1] + ac[2 * q + 1], tau, cp, sp);
+        const double g00 = w * (cm + cp), g01 = w * (sm - sp), g10 = -w * (sp + sm), g11 = w * (cm - cp);
+        const int r = o + 2 * p, s = o + 2 * q;
+        Q[r * LD + s] = g00;
+        Q[r * LD + s + 1] = g01;
+        Q[(r + 1) * LD + s] = g10;
+        Q[(r + 1) * LD + s + 1] = g11;
+        Q[s * LD + r] = g00;
+        Q[(s + 1) * LD + r] = g01;
+        Q[s * LD + r + 1] = g10;
+        Q[(s + 1) * LD + r + 1] = g11;
+    }
+}
+
+template <int LD>
+SP_DEV void eq_grad_team(int o, int J, const double* ac, const double* lr, double dt, const double* Phi,
+                         const double* Q, const double* M, const double* Bm, double& gvar, double& glen, int ln,
+                         int nl) {
+    const double var = lr[0];
+    const double s0 = ac[J + J * J];
+    double s = 0.0;
+    for (int i = ln; i < J; i += nl)
+        for (int k = 0; k < J; ++k) s += M[(o + i) * LD + o + k] * Q[(o + k) * LD + o + i];
+    const double ilen = lr[2], ivar = lr[3];
+    gvar += 0.5 * s * ivar;
+    if (dt < 0.0) return;
+    const double tau = dt * ilen;
+    double z0[kMaxB / 2], z1[kMaxB / 2];
+    for (int p = 0; p < J / 2; ++p) {
+        const double rho = exp(ac[2 * p] * tau);
+        double sn, cs;
+        sincos(ac[2 * p + 1] * tau, &sn, &cs);
+        z0[p] = rho * cs;
+        z1[p] = -rho * sn;
+    }
+    double tq = 0.0, tb = 0.0;
+    const double cdt = -dt * ilen;
+    for (int p = ln; p < J / 2; p += nl) {
+        const double a = ac[2 * p], c = ac[2 * p + 1];
+        const int k = o + 2 * p;
+        const double zp0 = z0[p], zp1 = z1[p];
+        for (int q = 0; q < J / 2; ++q) {
+            const int kq = o + 2 * q;
+            const double zq0 = z0[q], zq1 = z1[q];
+            tq += M[kq * LD + k] * zp0 * zq0 + M[(kq + 1) * LD + k] * zp0 * zq1 +
+                  M[kq * LD + k + 1] * zp1 * zq0 + M[(kq + 1) * LD + k + 1] * zp1 * zq1;
+        }
+        const double f00 = a * ilen, f01 = c * ilen, f10 = -c * ilen, f11 = a * ilen;
+        const double p00 = Phi[k * LD + k], p01 = Phi[k * LD + k + 1];
+        const double p10 = Phi[(k + 1) * LD + k], p11 = Phi[(k + 1) * LD + k + 1];
+        const double d00 = cdt * (f00 * p00 + f01 * p10), d01 = cdt * (f00 * p01 + f01 * p11);
+        const double d10 = cdt * (f10 * p00 + f11 * p10), d11 = cdt * (f10 * p01 + f11 * p11);
+        tb += d00 * Bm[k * LD + k] + d01 * Bm[(k + 1) * LD + k] + d10 * Bm[k * LD + k + 1] +
+              d11 * Bm[(k + 1) * LD + k + 1];
+    }
+    glen += 0.5 * (-var * s0 * dt * ilen * ilen) * tq + tb;
+}
+
+// harmonic j by its own sincos (the thread-per-chunk qp_block uses the angle-addition
+// recurrence from one sincos; the two agree to a few ulp)
+template <int LD>
+SP_DEV void qp_block_team(int o, int J, const double* lr, double dt, double* Phi, double* Q, int ln, int nl) {
+    const double var = lr[0], w0 = lr[4];
+    const double* q2 = lr + 5;
+    const double ienv = lr[5 + 2 * (J + 1)];
+    const double rho = dt < 0.0 ? 0.0 : exp(-dt * ienv);
+    const double one_m = dt < 0.0 ? 1.0 : -expm1(-2.0 * dt * ienv);
+    for (int j = ln; j <= J; j += nl) {
+        const int k = o + 2 * j;
+        if (dt >= 0.0) {
+            double sn = 0.0, cs = 1.0;
+            if (j > 0) sincos(double(j) * (w0 * dt), &sn, &cs);
+            Phi[k * LD + k] = rho * cs;
+            Phi[k * LD + k + 1] = -rho * sn;
+            Phi[(k + 1) * LD + k] = rho * sn;
+            Phi[(k + 1) * LD + k + 1] = rho * cs;
+        }
+        const double qv = var * q2[j] * one_m;
+        Q[k * LD + k] = qv;
+        Q[(k + 1) * LD + k + 1] = qv;
+    }
+}
+
+template <int LD>
+SP_DEV void qp_grad_team(int o, int J, const double* lr, double dt, const double* Phi, const double* M,
+                         const double* Bm, double* g4, int ln, int nl) {
+    const double var = lr[0];
+    const double* q2 = lr + 5;
+    const double* dq2 = lr + 5 + (J + 1);
+    const double ienv = lr[5 + 2 * (J + 1)], dwp = lr[5 + 2 * (J + 1) + 1];
+    const double rho2 = dt < 0.0 ? 0.0 : exp(-2.0 * dt * ienv);
+    const double one_m = dt < 0.0 ? 1.0 : -expm1(-2.0 * dt * ienv);
+    for (int j = ln; j <= J; j += nl) {
+        const int k = o + 2 * j;
+        const double trM = M[k * LD + k] + M[(k + 1) * LD + k + 1];
+        g4[0] += 0.5 * trM * q2[j] * one_m;
+        g4[1] += 0.5 * trM * var * dq2[j] * one_m;
+        if (dt < 0.0) continue;
+        const double ce = dt * ienv * ienv;
+        const double trPB = Phi[k * LD + k] * Bm[k * LD + k] + Phi[k * LD + k + 1] * Bm[(k + 1) * LD + k] +
+                            Phi[(k + 1) * LD + k] * Bm[k * LD + k + 1] +
+                            Phi[(k + 1) * LD + k + 1] * Bm[(k + 1) * LD + k + 1];
+        g4[3] += 0.5 * trM * (-2.0 * var * q2[j] * ce * rho2) + ce * trPB;
+        const double sj = double(j) * (-dwp) * dt;
+        const double d00 = -sj * Phi[(k + 1) * LD + k], d01 = -sj * Phi[(k + 1) * LD + k + 1];
+        const double d10 = sj * Phi[k * LD + k], d11 = sj * Phi[k * LD + k + 1];
+        g4[2] += d00 * Bm[k * LD + k] + d01 * Bm[(k + 1) * LD + k] + d10 * Bm[k * LD + k + 1] +
+                 d11 * Bm[(k + 1) * LD + k + 1];
+    }
+}
+#endif
+
 // ------------------------------------------------------------------ traits --
 // A Traits type provides B (block size of the instantiation), the emission row
 // and the two per-step model functions used by the elimination kernels.
@@ -498,6 +647,7 @@ struct MaternTraits {
 template <int BB>
 struct GenericTraits {
     static constexpr int B = BB;
+    static constexpr int NP = kMaxTheta;  // gradient slots of the team reduction
     SP_DEV static double H(const ModelDesc& md, int i) { return i < md.b ? md.H[i] : 0.0; }
     SP_DEV static void step(const ModelDesc& md, const double* rec, double dt, double* Phi,
                             double* Q) {
@@ -557,6 +707,17 @@ struct GenericTraits {
         }
         for (int p = 0; p < md.nt; ++p) g[p] += hm * rec[2 + p];
     }
+#ifndef SPINGP_HOST_EMU
+    // team versions (team.cuh): the dynamically offset leaves run on lane 0
+    SP_DEV static void step_team(const ModelDesc& md, const double* rec, double dt, double* Phi, double* Q, int ln,
+                                 int, unsigned) {
+        if (ln == 0) step(md, rec, dt, Phi, Q);
+    }
+    SP_DEV static void grad_team(const ModelDesc& md, const double* rec, double dt, const double* Phi,
+                                 const double* Q, const double* M, const double* Bm, int ln, int, double* g) {
+        if (ln == 0) grad(md, rec, dt, Phi, Q, M, Bm, g);
+    }
+#endif
 };
 
 // Static-structure models: leaf types and offsets are template constants, so every
@@ -574,6 +735,19 @@ struct SMatern {
                             const double* Q, const double* M, const double* Bm, double* g) {
         matern_grad<D, LD>(lr, dt, O, Phi, Q, M, Bm, g[0], g[1]);
     }
+#ifndef SPINGP_HOST_EMU
+    // the last lane of the team (the other leaf's pieces start at lane 0)
+    template <int O, int LD>
+    SP_DEV static void step_team(const ModelDesc& md, int l, const double* lr, double dt, double* Phi, double* Q,
+                                 int ln, int nl) {
+        if (ln == nl - 1) matern_block<D, LD>(lr, dt, O, Phi, Q);
+    }
+    template <int O, int LD>
+    SP_DEV static void grad_team(const ModelDesc& md, int l, const double* lr, double dt, const double* Phi,
+                                 const double* Q, const double* M, const double* Bm, double* g, int ln, int nl) {
+        if (ln == nl - 1) matern_grad<D, LD>(lr, dt, O, Phi, Q, M, Bm, g[0], g[1]);
+    }
+#endif
 };
 template <int J>
 struct SEQ {
@@ -587,6 +761,18 @@ struct SEQ {
                             const double* Q, const double* M, const double* Bm, double* g) {
         eq_grad<LD>(O, J, md.eqconst + md.eqc[l], lr, dt, Phi, Q, M, Bm, g[0], g[1]);
     }
+#ifndef SPINGP_HOST_EMU
+    template <int O, int LD>
+    SP_DEV static void step_team(const ModelDesc& md, int l, const double* lr, double dt, double* Phi, double* Q,
+                                 int ln, int nl) {
+        eq_block_team<LD>(O, J, md.eqconst + md.eqc[l], lr, dt, Phi, Q, ln, nl);
+    }
+    template <int O, int LD>
+    SP_DEV static void grad_team(const ModelDesc& md, int l, const double* lr, double dt, const double* Phi,
+                                 const double* Q, const double* M, const double* Bm, double* g, int ln, int nl) {
+        eq_grad_team<LD>(O, J, md.eqconst + md.eqc[l], lr, dt, Phi, Q, M, Bm, g[0], g[1], ln, nl);
+    }
+#endif
 };
 template <int J>
 struct SQP {
@@ -600,12 +786,25 @@ struct SQP {
                             const double*, const double* M, const double* Bm, double* g) {
         qp_grad<LD>(O, J, lr, dt, Phi, M, Bm, g);
     }
+#ifndef SPINGP_HOST_EMU
+    template <int O, int LD>
+    SP_DEV static void step_team(const ModelDesc&, int, const double* lr, double dt, double* Phi, double* Q, int ln,
+                                 int nl) {
+        qp_block_team<LD>(O, J, lr, dt, Phi, Q, ln, nl);
+    }
+    template <int O, int LD>
+    SP_DEV static void grad_team(const ModelDesc&, int, const double* lr, double dt, const double* Phi,
+                                 const double*, const double* M, const double* Bm, double* g, int ln, int nl) {
+        qp_grad_team<LD>(O, J, lr, dt, Phi, M, Bm, g, ln, nl);
+    }
+#endif
 };
 
 // One or two static leaves (the second at offset dim of the first).
 template <class L0, class L1 = void>
 struct StaticTraits {
     static constexpr int B = L0::dim + L1::dim;
+    static constexpr int NP = L0::np + L1::np;
     SP_DEV static double H(const ModelDesc& md, int i) { return md.H[i]; }
     SP_DEV static void step(const ModelDesc& md, const double* rec, double dt, double* Phi, double* Q) {
         mzero<B>(Phi);
@@ -630,10 +829,36 @@ struct StaticTraits {
 #pragma unroll
         for (int p = 0; p < L1::np; ++p) g[L0::np + p] += g1[p] + hm * rec[2 + L0::np + p];
     }
+#ifndef SPINGP_HOST_EMU
+    // team versions (team.cuh): zero-fill spread over the lanes, a team barrier, then
+    // every leaf's pieces spread over the lanes; gradient partials per lane in g[NP]
+    SP_DEV static void step_team(const ModelDesc& md, const double* rec, double dt, double* Phi, double* Q, int ln,
+                                 int nl, unsigned mask) {
+        for (int i = ln; i < B * B; i += nl) {
+            Phi[i] = 0.0;
+            Q[i] = 0.0;
+        }
+        __syncwarp(mask);
+        L0::template step_team<0, B>(md, 0, rec + md.rec[0], dt, Phi, Q, ln, nl);
+        L1::template step_team<L0::dim, B>(md, 1, rec + md.rec[1], dt, Phi, Q, ln, nl);
+    }
+    SP_DEV static void grad_team(const ModelDesc& md, const double* rec, double dt, const double* Phi,
+                                 const double* Q, const double* M, const double* Bm, int ln, int nl, double* g) {
+        double g0[4] = {0.0, 0.0, 0.0, 0.0}, g1[4] = {0.0, 0.0, 0.0, 0.0};
+        L0::template grad_team<0, B>(md, 0, rec + md.rec[0], dt, Phi, Q, M, Bm, g0, ln, nl);
+        L1::template grad_team<L0::dim, B>(md, 1, rec + md.rec[1], dt, Phi, Q, M, Bm, g1, ln, nl);
+        const double hm = ln < B ? 0.5 * M[ln * B + ln] : 0.0;  // lane ln's share of ½Tr(M)
+#pragma unroll
+        for (int p = 0; p < L0::np; ++p) g[p] += g0[p] + hm * rec[2 + p];
+#pragma unroll
+        for (int p = 0; p < L1::np; ++p) g[L0::np + p] += g1[p] + hm * rec[2 + L0::np + p];
+    }
+#endif
 };
 template <class L0>
 struct StaticTraits<L0, void> {
     static constexpr int B = L0::dim;
+    static constexpr int NP = L0::np;
     SP_DEV static double H(const ModelDesc& md, int i) { return md.H[i]; }
     SP_DEV static void step(const ModelDesc& md, const double* rec, double dt, double* Phi, double* Q) {
         mzero<B>(Phi);
@@ -652,6 +877,25 @@ struct StaticTraits<L0, void> {
 #pragma unroll
         for (int p = 0; p < L0::np; ++p) g[p] += g0[p] + hm * rec[2 + p];
     }
+#ifndef SPINGP_HOST_EMU
+    SP_DEV static void step_team(const ModelDesc& md, const double* rec, double dt, double* Phi, double* Q, int ln,
+                                 int nl, unsigned mask) {
+        for (int i = ln; i < B * B; i += nl) {
+            Phi[i] = 0.0;
+            Q[i] = 0.0;
+        }
+        __syncwarp(mask);
+        L0::template step_team<0, B>(md, 0, rec + md.rec[0], dt, Phi, Q, ln, nl);
+    }
+    SP_DEV static void grad_team(const ModelDesc& md, const double* rec, double dt, const double* Phi,
+                                 const double* Q, const double* M, const double* Bm, int ln, int nl, double* g) {
+        double g0[4] = {0.0, 0.0, 0.0, 0.0};
+        L0::template grad_team<0, B>(md, 0, rec + md.rec[0], dt, Phi, Q, M, Bm, g0, ln, nl);
+        const double hm = ln < B ? 0.5 * M[ln * B + ln] : 0.0;
+#pragma unroll
+        for (int p = 0; p < L0::np; ++p) g[p] += g0[p] + hm * rec[2 + p];
+    }
+#endif
 };
 
 }  // namespace spingp_dev

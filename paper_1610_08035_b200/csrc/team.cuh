@@ -211,7 +211,7 @@ template <class T>
 TP_INL bool tmodel(const Team& tm, const ModelDesc& md, const double* rp, double dt, double jit, double* PhiS,
                    double* QS, double* LQ, LogDetAcc* ldq) {
     constexpr int B = T::B;
-    if (tm.l == 0) T::step(md, rp, dt, PhiS, QS);
+    T::step_team(md, rp, dt, PhiS, QS, tm.l, TeamCfg<B>::TS, tm.mask);
     tsync(tm);
     double c[B];
     colget<B, B>(c, QS, tm.l);
@@ -599,7 +599,15 @@ TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, d
         rowput<B, B>(S1, v, l);
     }
     tsync(tm);
-    if (l == 0) T::grad(md, rp, dt, PhiS, QS, S0, S1, g);
+    double gp[T::NP];
+#pragma unroll
+    for (int p = 0; p < T::NP; ++p) gp[p] = 0.0;
+    T::grad_team(md, rp, dt, PhiS, QS, S0, S1, l, TeamCfg<B>::TS, gp);
+#pragma unroll
+    for (int p = 0; p < T::NP; ++p) {
+        const double v = tsum<TeamCfg<B>::TS>(tm, gp[p]);
+        if (l == 0 && p < md.nt) g[p] += v;
+    }
 }
 
 template <class T>
