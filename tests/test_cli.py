@@ -85,14 +85,21 @@ def test_fit_and_predict_on_gpu(cli, tmp_path):
 @pytest.mark.gpu
 def test_scaling_sweeps_on_gpu(cli, tmp_path):
     """spingp vs kf at the SPEC sizes (b = 12), and the GPU's own linear
-    regime (N = 1M..8M points, where it is throughput-bound): slope in [0.75, 1.3]."""
-    run(cli, "scaling-n", "--method", "spingp,kf", "--ns", "1000,2000,4000,8000", "--out", tmp_path / "n")
+    regime (N = 1M..8M points, where it is throughput-bound): slope in [0.75, 1.3].
+    The cross-method audit uses a b = 12 sum of Matérn leaves: with the CLI default
+    (matern32 + eq(order=10)) the SPEC's jitter on the ill-conditioned EQ-10 process noise
+    (cond(P_inf) ~ 1e12) moves the sparse-precision MLL away from the
+    jitter-free Kalman filter by design."""
+    k12 = "matern32(len=5) + matern52(len=3) + matern32(len=20) + matern52(len=8) + matern32(len=2)"
+    run(cli, "scaling-n", "--method", "spingp,kf", "--kernel", k12, "--ns", "1000,2000,4000,8000", "--out",
+        tmp_path / "n")
     rs = rows(tmp_path / "n" / "report.csv")
     assert len(rs) == 8 and all(r["error"] == "" for r in rs)
     by = {(r["method"], float(r["N"])): float(r["mll"]) for r in rs}
     for n in (1000, 2000, 4000, 8000):
         assert by[("spingp", n)] == pytest.approx(by[("kf", n)], rel=1e-6)
-    run(cli, "scaling-n", "--method", "spingp", "--ns", "1000000,2000000,4000000,8000000", "--out", tmp_path / "big")
+    run(cli, "scaling-n", "--method", "spingp", "--kernel", k12, "--ns", "1000000,2000000,4000000,8000000", "--out",
+        tmp_path / "big")
     s = json.loads((tmp_path / "big" / "metrics.json").read_text())["slopes"]["spingp"]
     assert 0.75 <= s <= 1.3, s
     run(cli, "scaling-b", "--method", "spingp", "--bs", "4,8,16", "--n", 1000, "--out", tmp_path / "b")
