@@ -93,39 +93,51 @@ inline void pack(const SymBTD& m, std::vector<double>& d, std::vector<double>& u
 }
 }  // namespace detail
 
-// The factor of a SymBTD.  On the B200 the factorisation is the partitioned
-// (hierarchical cyclic-reduction) LDL^T; it is recomputed on the device by the
-// operations that need it, so the factor keeps the matrix and the log-determinant.
+// The factor of a SymBTD: pivot Cholesky factors L_i (lower, positive
+// diagonal), multipliers M_i = U_i^T S_i^{-1}, the cached log-determinant — and the
+// device-resident factor they were read from (spingp_btd_factorize), which solve and
+// selective_inverse reuse without re-factorising.
 struct BTDFactor {
-    SymBTD matrix;
+    Index n_blocks = 0;
+    Index block_dim = 0;
+    std::vector<Matrix> L;  // n
+    std::vector<Matrix> M;  // n - 1
     double logdet = 0.0;
+    std::shared_ptr<spingp_btd_factor> device;
 };
 
-inline BTDFactor factorize(const SymBTD& m, Device& dev = default_device()) {
+inline BTDFactor factorize(const SymBTD& m, Device& dev = default_device()) {  // SPEC.md:143-151
     std::vector<double> d, u;
     detail::pack(m, d, u);
-    BTDFactor f{m, 0.0};
+    const Index n = m.n_blocks, b = m.block_dim;
+    spingp_btd_factor* raw = nullptr;
+    BTDFactor f;
     int64_t fb = -1;
-    const int st_ = spingp_btd_cr_solve(dev.get(), m.n_blocks, static_cast<int32_t>(m.block_dim), d.data(),
-                                      u.data(), nullptr, 0, nullptr, &f.logdet, &fb);
-    Device::check(st_, fb);
+    Device::check(spingp_btd_factorize(dev.get(), n, static_cast<int32_t>(b), d.data(), n > 1 ? u.data() : nullptr,
+                                       &raw, &f.logdet, &fb),
+                  fb);
+    f.device.reset(raw, [](spingp_btd_factor* p) { spingp_btd_factor_destroy(p); });
+    f.n_blocks = n;
+    f.block_dim = b;
+    std::vector<double> L(static_cast<size_t>(n * b * b)), M(static_cast<size_t>((n - 1) * b * b));
+    Device::check(spingp_btd_factor_blocks(dev.get(), raw, L.data(), n > 1 ? M.data() : nullptr), -1);
+    f.L.assign(static_cast<size_t>(n), Matrix(b, b));
+    f.M.assign(static_cast<size_t>(n - 1), Matrix(b, b));
+    for (Index i = 0; i < n; ++i) std::copy(L.begin() + i * b * b, L.begin() + (i + 1) * b * b, f.L[i].data());
+    for (Index i = 0; i + 1 < n; ++i) std::copy(M.begin() + i * b * b, M.begin() + (i + 1) * b * b, f.M[i].data());
     return f;
 }
 
-inline double logdet(const BTDFactor& f) { return f.logdet; }
+inline double logdet(const BTDFactor& f) { return f.logdet; }  // SPEC.md:161-169
 
-// X = M^{-1} rhs for an (n b) x k right-hand side.
+// X = M^{-1} rhs for an (n b) x k right-hand side, from the kept factor.
 inline Matrix solve(const BTDFactor& f, const Matrix& rhs, Device& dev = default_device()) {
-    const Index n = f.matrix.n_blocks, b = f.matrix.block_dim;
-    if (rhs.rows() != n * b) throw std::invalid_argument("solve: rhs row count must be n*b");
-    std::vector<double> d, u;
-    detail::pack(f.matrix, d, u);
+    if (!f.device) throw std::invalid_argument("solve: factor has no device state (use factorize)");
+    if (rhs.rows() != f.n_blocks * f.block_dim) throw std::invalid_argument("solve: rhs row count must be n*b");
     Matrix x(rhs.rows(), rhs.cols());
-    double ld = 0.0;
-    int64_t fb = -1;
-    const int st_ = spingp_btd_cr_solve(dev.get(), n, static_cast<int32_t>(b), d.data(), u.data(), rhs.data(),
-                                      static_cast<int32_t>(rhs.cols()), x.data(), &ld, &fb);
-    Device::check(st_, fb);
+    Device::check(spingp_btd_factor_solve(dev.get(), f.device.get(), rhs.data(), static_cast<int32_t>(rhs.cols()),
+                                          x.data()),
+                  -1);
     return x;
 }
 
@@ -134,22 +146,26 @@ struct CrSolveResult {
     double logdet;
 };
 
+// cr_solve: one partitioned-elimination pass gives x and log det.
 inline CrSolveResult cr_solve(const SymBTD& m, const Matrix& rhs, Device& dev = default_device()) {
-    BTDFactor f{m, 0.0};
-    Matrix x = solve(f, rhs, dev);
-    return {std::move(x), factorize(m, dev).logdet};
+    const Index n = m.n_blocks, b = m.block_dim;
+    if (rhs.rows() != n * b) throw std::invalid_argument("cr_solve: rhs row count must be n*b");
+    std::vector<double> d, u;
+    detail::pack(m, d, u);
+    CrSolveResult r{Matrix(rhs.rows(), rhs.cols()), 0.0};
+    int64_t fb = -1;
+    Device::check(spingp_btd_cr_solve(dev.get(), n, static_cast<int32_t>(b), d.data(), u.data(), rhs.data(),
+                                      static_cast<int32_t>(rhs.cols()), r.x.data(), &r.logdet, &fb),
+                  fb);
+    return r;
 }
 
-// The BTD-pattern blocks of M^{-1}.
+// The BTD-pattern blocks of M^{-1}, kept by factorize.
 inline SymBTD selective_inverse(const BTDFactor& f, Device& dev = default_device()) {
-    const Index n = f.matrix.n_blocks, b = f.matrix.block_dim;
-    std::vector<double> d, u, cd(static_cast<size_t>(n * b * b)), cu(static_cast<size_t>((n - 1) * b * b));
-    detail::pack(f.matrix, d, u);
-    double ld = 0.0;
-    int64_t fb = -1;
-    const int st_ = spingp_btd_selinv(dev.get(), n, static_cast<int32_t>(b), d.data(), u.data(), cd.data(),
-                                    n > 1 ? cu.data() : nullptr, &ld, &fb);
-    Device::check(st_, fb);
+    if (!f.device) throw std::invalid_argument("selective_inverse: factor has no device state (use factorize)");
+    const Index n = f.n_blocks, b = f.block_dim;
+    std::vector<double> cd(static_cast<size_t>(n * b * b)), cu(static_cast<size_t>((n - 1) * b * b));
+    Device::check(spingp_btd_factor_selinv(dev.get(), f.device.get(), cd.data(), n > 1 ? cu.data() : nullptr), -1);
     SymBTD out(n, b);
     for (Index i = 0; i < n; ++i) std::copy(cd.begin() + i * b * b, cd.begin() + (i + 1) * b * b, out.diag[i].data());
     for (Index i = 0; i + 1 < n; ++i)

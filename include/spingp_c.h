@@ -18,6 +18,8 @@
  *   spingp_btd_cr_solve[...]  cr_solve (+ solve/logdet)
  *   spingp_btd_selinv[...]    selective_inverse
  *   spingp_btd_matvec[...]    matvec
+ *   spingp_btd_factorize / _factor_{solve,selinv,blocks}   BTDFactor + factorize / solve /
+ *                             selective_inverse on a kept factor
  * Error convention: every function returns a spingp_status; NOT_PD carries the
  * failing block index through `fail_block` (errors.hpp:12-20 NotPositiveDefinite),
  * SINGULAR_Q likewise (errors.hpp:23-27 SingularProcessNoise).  The C++ layer
@@ -229,6 +231,25 @@ int spingp_btd_selinv(spingp_ctx* ctx, int64_t n, int32_t b, const double* diag,
 int spingp_btd_selinv_device(spingp_ctx* ctx, int64_t n, int32_t b, const double* d_diag,
                              const double* d_upper, double* d_cdiag, double* d_cupper,
                              double* d_logdet);
+
+/* ---- BTDFactor: factorize once, reuse ------------------------
+ * spingp_btd_factorize    factorize(SymBTD) -> BTDFactor
+ *   A device-resident factor: the pivot Cholesky factors L_i (lower, positive
+ *   diagonal, [n][b][b]), the multipliers M_i = U_i^T S_i^{-1} ([n-1][b][b]), the
+ *   cached log det and the selected inverse.  One partitioned
+ *   elimination pass, then every L_i, M_i in parallel from the Takahashi identities.
+ * spingp_btd_factor_solve  solve(BTDFactor, rhs[(n b) x k])
+ * spingp_btd_factor_selinv selective_inverse(BTDFactor)
+ * spingp_btd_factor_blocks the L_i, M_i blocks (host copies)
+ * Block size b <= 16.  The factor is bound to the context's device. */
+typedef struct spingp_btd_factor spingp_btd_factor;
+int spingp_btd_factorize(spingp_ctx* ctx, int64_t n, int32_t b, const double* diag, const double* upper,
+                         spingp_btd_factor** out, double* logdet, int64_t* fail_block);
+int spingp_btd_factor_destroy(spingp_btd_factor* f);
+int spingp_btd_factor_info(const spingp_btd_factor* f, int64_t* n, int32_t* b, double* logdet);
+int spingp_btd_factor_blocks(spingp_ctx* ctx, const spingp_btd_factor* f, double* L, double* M);
+int spingp_btd_factor_solve(spingp_ctx* ctx, const spingp_btd_factor* f, const double* rhs, int32_t k, double* x);
+int spingp_btd_factor_selinv(spingp_ctx* ctx, const spingp_btd_factor* f, double* cdiag, double* cupper);
 
 /* matvec: y = M v (one vector). */
 int spingp_btd_matvec(spingp_ctx* ctx, int64_t n, int32_t b, const double* diag,

@@ -107,6 +107,12 @@ SIGNATURES = {
     "spingp_btd_selinv": (ctypes.c_int, [_vp, _i64, _i32, _d, _d, _d, _d, _d, _i64p]),
     "spingp_btd_selinv_device": (ctypes.c_int, [_vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
     "spingp_btd_matvec": (ctypes.c_int, [_vp, _i64, _i32, _d, _d, _d, _d]),
+    "spingp_btd_factorize": (ctypes.c_int, [_vp, _i64, _i32, _d, _d, _P(_vp), _d, _i64p]),
+    "spingp_btd_factor_destroy": (ctypes.c_int, [_vp]),
+    "spingp_btd_factor_info": (ctypes.c_int, [_vp, _i64p, _i32p, _d]),
+    "spingp_btd_factor_blocks": (ctypes.c_int, [_vp, _vp, _d, _d]),
+    "spingp_btd_factor_solve": (ctypes.c_int, [_vp, _vp, _d, _i32, _d]),
+    "spingp_btd_factor_selinv": (ctypes.c_int, [_vp, _vp, _d, _d]),
 }
 
 _lib = None
@@ -411,5 +417,56 @@ class Context:
         _raise(lib().spingp_seg_finalize_device(self._h, int(n_theta), int(n_total), float(sigma), int(flags),
                                                 d_partials, d_loglik, d_grad or None))
 
+    def btd_factorize(self, diag, upper):
+        """factorize: a device-resident BTDFactor bound to this context."""
+        return BTDFactor(self, diag, upper)
+
     def btd_cr_solve_device(self, n, b, d_diag, d_upper, d_rhs, k, d_x, d_logdet):
         _raise(lib().spingp_btd_cr_solve_device(self._h, int(n), int(b), d_diag, d_upper, d_rhs, int(k), d_x, d_logdet))
+
+
+class BTDFactor:
+    """BTDFactor on the device: L_i, M_i, log det and the selected
+    inverse, kept for solve / selective_inverse (spingp_btd_factorize)."""
+
+    def __init__(self, ctx, diag, upper):
+        d = _f64(diag)
+        n, b = d.shape[0], d.shape[1]
+        u = _f64(upper) if n > 1 else None
+        self._ctx, self.n, self.b = ctx, n, b
+        self._h = _vp()
+        ld = _dbl()
+        fb = _i64()
+        _raise(lib().spingp_btd_factorize(ctx._h, n, b, _p(d), _p(u), ctypes.byref(self._h), ctypes.byref(ld),
+                                          ctypes.byref(fb)), fb)
+        self.logdet = ld.value
+
+    def blocks(self):
+        L = np.empty((self.n, self.b, self.b))
+        M = np.empty((max(self.n - 1, 0), self.b, self.b))
+        _raise(lib().spingp_btd_factor_blocks(self._ctx._h, self._h, _p(L), _p(M) if self.n > 1 else None))
+        return L, M
+
+    def solve(self, rhs):
+        r = _f64(rhs)
+        k = 1 if r.ndim == 1 else r.shape[1]
+        x = np.empty_like(r)
+        _raise(lib().spingp_btd_factor_solve(self._ctx._h, self._h, _p(r), k, _p(x)))
+        return x
+
+    def selective_inverse(self):
+        cd = np.empty((self.n, self.b, self.b))
+        cu = np.empty((max(self.n - 1, 0), self.b, self.b))
+        _raise(lib().spingp_btd_factor_selinv(self._ctx._h, self._h, _p(cd), _p(cu) if self.n > 1 else None))
+        return cd, cu
+
+    def close(self):
+        if self._h:
+            lib().spingp_btd_factor_destroy(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

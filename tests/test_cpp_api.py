@@ -42,3 +42,12 @@ def test_optimize_hyperparameters_api_on_gpu():
     exe = build("test_optimize_api", True)
     r = subprocess.run([exe], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_btd_factor_api_on_gpu():
+    """The device-resident BTDFactor: SPEC.md:135-140 reconstruction invariant, known
+    answers, solve / selective_inverse on the kept factor (include/spingp/btd.hpp)."""
+    exe = build("test_factor_api", True)
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
