@@ -56,6 +56,27 @@ private:
     std::unique_ptr<spingp_ctx, Del> ctx_;
 };
 
+// Several devices of one box joined by NCCL (spingp_mctx_create): the engine functions
+// taking a MultiDevice partition one long series into contiguous time segments, one per
+// device (spingp_eval_partitioned).
+class MultiDevice {
+public:
+    explicit MultiDevice(const std::vector<int>& devices) {
+        std::vector<int32_t> ids(devices.begin(), devices.end());
+        spingp_mctx* m = nullptr;
+        Device::check(spingp_mctx_create(static_cast<int32_t>(ids.size()), ids.data(), &m), -1);
+        m_.reset(m);
+    }
+    spingp_mctx* get() const { return m_.get(); }
+    int size() const { return spingp_mctx_size(m_.get()); }
+
+private:
+    struct Del {
+        void operator()(spingp_mctx* m) const { spingp_mctx_destroy(m); }
+    };
+    std::unique_ptr<spingp_mctx, Del> m_;
+};
+
 // Per-thread default device (cuda:0), created on first use.
 inline Device& default_device() {
     thread_local Device d(0);

@@ -87,7 +87,48 @@ inline EvalOut eval(const Dataset& d, const KernelSpec& spec, const Hyperparamet
     return o;
 }
 
+// the same evaluation partitioned over the devices of a MultiDevice (spingp_eval_partitioned)
+inline EvalOut eval(const Dataset& d, const KernelSpec& spec, const HyperparameterSet& theta,
+                    const NoiseModel& noise, uint32_t flags, MultiDevice& md) {
+    check_data(d, noise);
+    const auto lv = leaves_of(spec);
+    EvalOut o;
+    const size_t n = d.times.size();
+    if (flags & SPINGP_WANT_GRAD) o.grad.resize(theta.size() + 1);
+    if (flags & SPINGP_WANT_MEAN) o.mean.resize(n);
+    if (flags & SPINGP_WANT_VAR) o.var.resize(n);
+    int64_t fb = -1;
+    const int st_ = spingp_eval_partitioned(md.get(), lv.data(), static_cast<int32_t>(lv.size()), theta.data(),
+                                            static_cast<int32_t>(theta.size()), d.times.data(), d.values.data(),
+                                            static_cast<int64_t>(n), std::sqrt(noise.sigma_n2), flags, &o.loglik,
+                                            o.grad.empty() ? nullptr : o.grad.data(),
+                                            o.mean.empty() ? nullptr : o.mean.data(),
+                                            o.var.empty() ? nullptr : o.var.data(), &fb);
+    Device::check(st_, fb);
+    return o;
+}
 }  // namespace detail
+
+// Multi-GPU overloads: one long series partitioned over the devices.
+inline double log_marginal_likelihood(const Dataset& data, const KernelSpec& spec, const HyperparameterSet& theta,
+                                      const NoiseModel& noise, MultiDevice& md) {
+    return detail::eval(data, spec, theta, noise, 0u, md).loglik;
+}
+inline std::vector<double> mll_gradient(const Dataset& data, const KernelSpec& spec, const HyperparameterSet& theta,
+                                        const NoiseModel& noise, MultiDevice& md) {
+    return detail::eval(data, spec, theta, noise, SPINGP_WANT_GRAD, md).grad;
+}
+inline PosteriorSummary predict(const Dataset& data, const KernelSpec& spec, const HyperparameterSet& theta,
+                                const NoiseModel& noise, MultiDevice& md) {
+    auto o = detail::eval(data, spec, theta, noise, SPINGP_WANT_GRAD | SPINGP_WANT_MEAN | SPINGP_WANT_VAR, md);
+    PosteriorSummary p;
+    p.times = data.times;
+    p.mean = std::move(o.mean);
+    p.variance = std::move(o.var);
+    p.mll = o.loglik;
+    p.mll_grad = std::move(o.grad);
+    return p;
+}
 
 // 𝒦^{-1}: the prior precision over the N state blocks (no observation term).
 inline SymBTD assemble_prior_precision(const std::vector<double>& times, const KernelSpec& spec,

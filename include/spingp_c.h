@@ -18,6 +18,8 @@
  *   spingp_btd_cr_solve[...]  cr_solve (+ solve/logdet)
  *   spingp_btd_selinv[...]    selective_inverse
  *   spingp_btd_matvec[...]    matvec
+ *   spingp_mctx_create + spingp_eval_partitioned   the multi-GPU (NCCL) partition of one
+ *                             long series; data-parallel cr_solve contract SPEC.md:200,224
  *   spingp_btd_factorize / _factor_{solve,selinv,blocks}   BTDFactor + factorize / solve /
  *                             selective_inverse on a kept factor
  * Error convention: every function returns a spingp_status; NOT_PD carries the
@@ -213,6 +215,25 @@ int spingp_seg_reverse_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32_
                               double* d_mean, double* d_var);
 int spingp_seg_finalize_device(spingp_ctx* ctx, int32_t n_theta, int64_t n_total, double sigma, uint32_t flags,
                                const double* d_partials, double* d_loglik, double* d_grad);
+
+/* ---- multi-GPU inside the library -----------------------
+ * A multi-device context: one spingp_ctx per device plus an NCCL communicator
+ * (ncclCommInitAll; NCCL is dlopen'ed on first use — SPINGP_NCCL_ERR without it).
+ * spingp_eval_partitioned evaluates ONE long series over the P devices: contiguous time
+ * segments, each reduced to a 2-separator Schur record, NCCL all-gather of the records,
+ * the P-block reduced system solved on every device, back substitution + selected
+ * inverse per segment, NCCL all-reduce of the partial sums.  Host pointers, synchronous;
+ * results equal spingp_eval's to rounding.  Replaces the data-parallel cr_solve
+ * contract of SPEC.md:200,224 at the scale of one box. */
+typedef struct spingp_mctx spingp_mctx;
+int spingp_mctx_create(int32_t n_gpus, const int32_t* device_ids, spingp_mctx** out);
+int spingp_mctx_destroy(spingp_mctx* m);
+int32_t spingp_mctx_size(const spingp_mctx* m);
+spingp_ctx* spingp_mctx_rank_ctx(spingp_mctx* m, int32_t rank);
+int spingp_eval_partitioned(spingp_mctx* m, const spingp_leaf* leaves, int32_t n_leaves, const double* theta,
+                            int32_t n_theta, const double* t, const double* y, int64_t n, double sigma,
+                            uint32_t flags, double* out_loglik, double* out_grad, double* out_mean, double* out_var,
+                            int64_t* fail_block);
 
 /* ---- btd_core on a materialised symmetric BTD --------------- */
 

@@ -14,13 +14,13 @@ from ._capi import (  # noqa: F401
     WANT_GRAD, WANT_MEAN, WANT_VAR, INCLUDE_NOISE,
     SpingpError, NotPositiveDefinite, SingularProcessNoise, DuplicateTimestamp, DeviceError,
     NegativeVariance, Unsupported,
-    Context, lib, lib_path, kernel_dims, state_space, n_theta, seg_sizes,
+    Context, MultiContext, BTDFactor, lib, lib_path, kernel_dims, state_space, n_theta, seg_sizes,
 )
 
 __all__ = [
     "MATERN12", "MATERN32", "MATERN52", "EQ", "QP", "LEAF_NPARAMS",
     "WANT_GRAD", "WANT_MEAN", "WANT_VAR", "INCLUDE_NOISE",
     "SpingpError", "NotPositiveDefinite", "SingularProcessNoise", "DuplicateTimestamp", "DeviceError",
-    "NegativeVariance", "Unsupported", "Context", "lib", "lib_path", "kernel_dims", "state_space", "n_theta",
+    "NegativeVariance", "Unsupported", "Context", "MultiContext", "BTDFactor", "lib", "lib_path", "kernel_dims", "state_space", "n_theta",
     "seg_sizes",
 ]

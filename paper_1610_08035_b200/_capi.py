@@ -107,6 +107,12 @@ SIGNATURES = {
     "spingp_btd_selinv": (ctypes.c_int, [_vp, _i64, _i32, _d, _d, _d, _d, _d, _i64p]),
     "spingp_btd_selinv_device": (ctypes.c_int, [_vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
     "spingp_btd_matvec": (ctypes.c_int, [_vp, _i64, _i32, _d, _d, _d, _d]),
+    "spingp_mctx_create": (ctypes.c_int, [_i32, _i32p, _P(_vp)]),
+    "spingp_mctx_destroy": (ctypes.c_int, [_vp]),
+    "spingp_mctx_size": (_i32, [_vp]),
+    "spingp_mctx_rank_ctx": (_vp, [_vp, _i32]),
+    "spingp_eval_partitioned": (ctypes.c_int, [_vp, _vp, _i32, _d, _i32, _d, _d, _i64, _dbl, _u32, _d, _d, _d, _d,
+                                               _i64p]),
     "spingp_btd_factorize": (ctypes.c_int, [_vp, _i64, _i32, _d, _d, _P(_vp), _d, _i64p]),
     "spingp_btd_factor_destroy": (ctypes.c_int, [_vp]),
     "spingp_btd_factor_info": (ctypes.c_int, [_vp, _i64p, _i32p, _d]),
@@ -470,3 +476,40 @@ class BTDFactor:
             self.close()
         except Exception:
             pass
+
+
+class MultiContext:
+    """spingp_mctx: P devices of one box joined by NCCL (spingp_mctx_create); eval()
+    partitions one long series over them (spingp_eval_partitioned)."""
+
+    def __init__(self, devices):
+        devs = np.ascontiguousarray(devices, dtype=np.int32)
+        self._h = _vp()
+        _raise(lib().spingp_mctx_create(len(devs), devs.ctypes.data_as(_i32p), ctypes.byref(self._h)))
+        self.size = len(devs)
+
+    def eval(self, leaves, theta, t, y, sigma, grad=True, mean=False, var=False):
+        lv = _leaves(leaves)
+        th = _f64(theta); t = _f64(t); y = _f64(y)
+        n = len(t)
+        flags = (WANT_GRAD if grad else 0) | (WANT_MEAN if mean else 0) | (WANT_VAR if var else 0)
+        ll = _dbl()
+        g = np.zeros(len(th) + 1) if grad else None
+        mu = np.zeros(n) if mean else None
+        v = np.zeros(n) if var else None
+        fb = _i64()
+        _raise(lib().spingp_eval_partitioned(self._h, lv.ctypes.data, len(leaves), _p(th), len(th), _p(t), _p(y), n,
+                                             float(sigma), flags, ctypes.byref(ll), _p(g), _p(mu), _p(v),
+                                             ctypes.byref(fb)), fb)
+        return dict(loglik=ll.value, grad=g, mean=mu, var=v)
+
+    def close(self):
+        if self._h:
+            lib().spingp_mctx_destroy(self._h)
+            self._h = _vp()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

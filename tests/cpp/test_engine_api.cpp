@@ -112,4 +112,27 @@ TEST(Engine, PredictAtTestTimesInterpolatesAndReverts) {
     EXPECT_EQ(p.mll_grad.size(), 3u);
 }
 
+TEST(Engine, MultiDeviceOneGpuEqualsSingle) {  // spingp_eval_partitioned, P = 1
+    std::mt19937_64 g(42);
+    std::uniform_real_distribution<double> u(0.05, 0.15);
+    std::normal_distribution<double> z;
+    Dataset d;
+    double tt = 0.0;
+    for (int i = 0; i < 5000; ++i) {
+        tt += u(g);
+        d.times.push_back(tt);
+        d.values.push_back(std::sin(0.5 * tt) + 0.3 * z(g));
+    }
+    const auto spec = KernelSpec::matern52(2.0, 1.5);
+    const HyperparameterSet th{2.0, 1.5};
+    MultiDevice md({0});
+    EXPECT_TRUE(md.size() == 1);
+    const double a = log_marginal_likelihood(d, spec, th, NoiseModel{0.09}, md);
+    const double b = log_marginal_likelihood(d, spec, th, NoiseModel{0.09});
+    EXPECT_NEAR(a, b, 1e-10 * std::abs(b));
+    const auto ga = mll_gradient(d, spec, th, NoiseModel{0.09}, md);
+    const auto gb = mll_gradient(d, spec, th, NoiseModel{0.09});
+    for (size_t i = 0; i < ga.size(); ++i) EXPECT_NEAR(ga[i], gb[i], 1e-9 * std::abs(gb[i]) + 1e-12);
+}
+
 int main() { return minitest::run_all(); }
