@@ -134,9 +134,10 @@ inline BTDFactor factorize(const SymBTD& m, Device& dev = default_device()) {  /
     spingp_btd_factor* raw = nullptr;
     BTDFactor f;
     int64_t fb = -1;
-    Device::check(spingp_btd_factorize(dev.get(), n, static_cast<int32_t>(b), d.data(), n > 1 ? u.data() : nullptr,
-                                       &raw, &f.logdet, &fb),
-                  fb);
+    // status first, then the failing block it set (argument evaluation order is unspecified)
+    const int st_ = spingp_btd_factorize(dev.get(), n, static_cast<int32_t>(b), d.data(), n > 1 ? u.data() : nullptr,
+                                         &raw, &f.logdet, &fb);
+    Device::check(st_, fb);
     f.device.reset(raw, [](spingp_btd_factor* p) { spingp_btd_factor_destroy(p); });
     f.n_blocks = n;
     f.block_dim = b;
@@ -175,9 +176,9 @@ inline CrSolveResult cr_solve(const SymBTD& m, const Matrix& rhs, Device& dev = 
     detail::pack(m, d, u);
     CrSolveResult r{Matrix(rhs.rows(), rhs.cols()), 0.0};
     int64_t fb = -1;
-    Device::check(spingp_btd_cr_solve(dev.get(), n, static_cast<int32_t>(b), d.data(), u.data(), rhs.data(),
-                                      static_cast<int32_t>(rhs.cols()), r.x.data(), &r.logdet, &fb),
-                  fb);
+    const int st_ = spingp_btd_cr_solve(dev.get(), n, static_cast<int32_t>(b), d.data(), u.data(), rhs.data(),
+                                        static_cast<int32_t>(rhs.cols()), r.x.data(), &r.logdet, &fb);
+    Device::check(st_, fb);
     return r;
 }
 
