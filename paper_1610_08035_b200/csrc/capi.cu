@@ -378,7 +378,13 @@ int spingp_eval_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_lea
 // back while the next piece computes.  Results are identical to the unpipelined call (the
 // kernels and their per-chunk arithmetic do not change; only launch boundaries do).
 constexpr int64_t kPipeMin = 1 << 18;
-constexpr int kPipeIn = 4, kPipeOut = 2;
+constexpr int kPipeMax = 16;
+// pieces of the input / output pipeline (SPINGP_PIPE_IN / SPINGP_PIPE_OUT override, <= kPipeMax)
+static int pipe_pieces(const char* env, int dflt) {
+    const char* e = std::getenv(env);
+    const int v = e ? std::atoi(e) : dflt;
+    return std::max(1, std::min(kPipeMax, v));
+}
 
 static int eval_host_pipelined(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves, const double* theta,
                                int32_t n_theta, int64_t n, const double* t, const double* y, double sigma,
@@ -402,7 +408,8 @@ static int eval_host_pipelined(spingp_ctx* ctx, const spingp_leaf* leaves, int32
         std::vector<double> params(hm.rec_stride, 0.0);
         fill_record(hm, theta, sigma, params.data());
         const long long K0 = plan.geo.K[0], m0 = plan.geo.m[0];
-        long long ic[kPipeIn + 1], oc[kPipeOut + 1];
+        static const int kPipeIn = pipe_pieces("SPINGP_PIPE_IN", 4), kPipeOut = pipe_pieces("SPINGP_PIPE_OUT", 2);
+        long long ic[kPipeMax + 1], oc[kPipeMax + 1];
         for (int p = 0; p <= kPipeIn; ++p) ic[p] = K0 * p / kPipeIn;
         for (int q = 0; q <= kPipeOut; ++q) oc[q] = K0 * q / kPipeOut;
         if (!ctx->copy_stream) {

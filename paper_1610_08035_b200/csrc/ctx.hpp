@@ -108,7 +108,7 @@ struct spingp_ctx {
     spingp_host::HostModel model;
     // host-input pipelining: copy stream + events (created on first use)
     cudaStream_t copy_stream = nullptr;
-    cudaEvent_t pipe_ev[16] = {};
+    cudaEvent_t pipe_ev[40] = {};
     std::mutex mu;
     // optional per-launch CUDA-event timing (spingp_ctx_set_profiling)
     bool profiling = false;

@@ -19,3 +19,7 @@ PY
 ncu --set full --import-source on --clock-control none -k regex:k_rev0_team -s 1 -c 1 -o gpurun_out/ncu_rev0_team_cfg4 python /tmp/prof_team.py cfg4 1000000 > gpurun_out/ncu_rev0_team_cfg4.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:k_fwd0_team -s 1 -c 1 -o gpurun_out/ncu_fwd0_team_cfg4 python /tmp/prof_team.py cfg4 1000000 > gpurun_out/ncu_fwd0_team_cfg4.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:k_rev0_team -s 1 -c 1 -o gpurun_out/ncu_rev0_team_cfg5 python /tmp/prof_team.py cfg5 200000 > gpurun_out/ncu_rev0_team_cfg5.log 2>&1
+# e2e pipeline pieces (cfg2 host-pointer call)
+for pp in "4 2" "4 4" "8 4" "8 8" "16 8"; do set -- $pp
+  SPINGP_PIPE_IN=$1 SPINGP_PIPE_OUT=$2 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-per-config > gpurun_out/e2e_pipe_$1_$2.json 2>&1
+done
