@@ -649,6 +649,7 @@ struct GenericTraits {
     static constexpr int B = BB;
     static constexpr int NP = kMaxTheta;  // gradient slots of the team reduction
     SP_DEV static double H(const ModelDesc& md, int i) { return i < md.b ? md.H[i] : 0.0; }
+    template <int LD = BB>  // row stride of Phi, Q (the team kernels use an odd one)
     SP_DEV static void step(const ModelDesc& md, const double* rec, double dt, double* Phi,
                             double* Q) {
         // Zero-fill with a rolled loop: statically unrolled (vectorised) zero stores
@@ -656,28 +657,29 @@ struct GenericTraits {
         // were reordered by nvcc 12.9 / sm_100a (lost Q[0..1]; tools/dbg/dbg_generic.cu).
 #pragma unroll 1
         for (int i = 0; i < BB * BB; ++i) {
-            Phi[i] = 0.0;
-            Q[i] = 0.0;
+            Phi[(i / BB) * LD + i % BB] = 0.0;
+            Q[(i / BB) * LD + i % BB] = 0.0;
         }
-        for (int i = md.b; i < BB; ++i) Q[i * BB + i] = 1.0;  // padding
+        for (int i = md.b; i < BB; ++i) Q[i * LD + i] = 1.0;  // padding
         SP_MEMFENCE();
         for (int l = 0; l < md.nleaves; ++l) {
             const double* lr = rec + md.rec[l];
             SP_MEMFENCE();
             switch (md.type[l]) {
-                case MATERN12: matern_block<1, BB>(lr, dt, md.off[l], Phi, Q); break;
-                case MATERN32: matern_block<2, BB>(lr, dt, md.off[l], Phi, Q); break;
-                case MATERN52: matern_block<3, BB>(lr, dt, md.off[l], Phi, Q); break;
-                case EQ: eq_block<BB>(md.off[l], md.dim[l], md.eqconst + md.eqc[l], lr, dt, Phi, Q); break;
-                case QP: qp_block<BB>(md.off[l], md.order[l], lr, dt, Phi, Q); break;
+                case MATERN12: matern_block<1, LD>(lr, dt, md.off[l], Phi, Q); break;
+                case MATERN32: matern_block<2, LD>(lr, dt, md.off[l], Phi, Q); break;
+                case MATERN52: matern_block<3, LD>(lr, dt, md.off[l], Phi, Q); break;
+                case EQ: eq_block<LD>(md.off[l], md.dim[l], md.eqconst + md.eqc[l], lr, dt, Phi, Q); break;
+                case QP: qp_block<LD>(md.off[l], md.order[l], lr, dt, Phi, Q); break;
             }
         }
         SP_MEMFENCE();
     }
+    template <int LD = BB>
     SP_DEV static void grad(const ModelDesc& md, const double* rec, double dt, const double* Phi,
                             const double* Q, const double* M, const double* Bm, double* g) {
         double hm = 0.0;
-        for (int i = 0; i < md.b; ++i) hm += M[i * BB + i];
+        for (int i = 0; i < md.b; ++i) hm += M[i * LD + i];
         hm *= 0.5;
         SP_MEMFENCE();
         for (int l = 0; l < md.nleaves; ++l) {
@@ -686,15 +688,15 @@ struct GenericTraits {
             SP_MEMFENCE();
             double gv = 0.0, gl = 0.0;
             switch (md.type[l]) {
-                case MATERN12: matern_grad<1, BB>(lr, dt, md.off[l], Phi, Q, M, Bm, gv, gl); break;
-                case MATERN32: matern_grad<2, BB>(lr, dt, md.off[l], Phi, Q, M, Bm, gv, gl); break;
-                case MATERN52: matern_grad<3, BB>(lr, dt, md.off[l], Phi, Q, M, Bm, gv, gl); break;
+                case MATERN12: matern_grad<1, LD>(lr, dt, md.off[l], Phi, Q, M, Bm, gv, gl); break;
+                case MATERN32: matern_grad<2, LD>(lr, dt, md.off[l], Phi, Q, M, Bm, gv, gl); break;
+                case MATERN52: matern_grad<3, LD>(lr, dt, md.off[l], Phi, Q, M, Bm, gv, gl); break;
                 case EQ:
-                    eq_grad<BB>(md.off[l], md.dim[l], md.eqconst + md.eqc[l], lr, dt, Phi, Q, M, Bm, gv, gl);
+                    eq_grad<LD>(md.off[l], md.dim[l], md.eqconst + md.eqc[l], lr, dt, Phi, Q, M, Bm, gv, gl);
                     break;
                 case QP: {
                     double g4[4] = {0.0, 0.0, 0.0, 0.0};
-                    qp_grad<BB>(md.off[l], md.order[l], lr, dt, Phi, M, Bm, g4);
+                    qp_grad<LD>(md.off[l], md.order[l], lr, dt, Phi, M, Bm, g4);
                     g[t0 + 2] += g4[2];
                     g[t0 + 3] += g4[3];
                     gv = g4[0];
@@ -709,13 +711,15 @@ struct GenericTraits {
     }
 #ifndef SPINGP_HOST_EMU
     // team versions (team.cuh): the dynamically offset leaves run on lane 0
+    template <int LD>
     SP_DEV static void step_team(const ModelDesc& md, const double* rec, double dt, double* Phi, double* Q, int ln,
                                  int, unsigned) {
-        if (ln == 0) step(md, rec, dt, Phi, Q);
+        if (ln == 0) step<LD>(md, rec, dt, Phi, Q);
     }
+    template <int LD>
     SP_DEV static void grad_team(const ModelDesc& md, const double* rec, double dt, const double* Phi,
                                  const double* Q, const double* M, const double* Bm, int ln, int, double* g) {
-        if (ln == 0) grad(md, rec, dt, Phi, Q, M, Bm, g);
+        if (ln == 0) grad<LD>(md, rec, dt, Phi, Q, M, Bm, g);
     }
 #endif
 };
@@ -832,22 +836,24 @@ struct StaticTraits {
 #ifndef SPINGP_HOST_EMU
     // team versions (team.cuh): zero-fill spread over the lanes, a team barrier, then
     // every leaf's pieces spread over the lanes; gradient partials per lane in g[NP]
+    template <int LD>
     SP_DEV static void step_team(const ModelDesc& md, const double* rec, double dt, double* Phi, double* Q, int ln,
                                  int nl, unsigned mask) {
         for (int i = ln; i < B * B; i += nl) {
-            Phi[i] = 0.0;
-            Q[i] = 0.0;
+            Phi[(i / B) * LD + i % B] = 0.0;
+            Q[(i / B) * LD + i % B] = 0.0;
         }
         __syncwarp(mask);
-        L0::template step_team<0, B>(md, 0, rec + md.rec[0], dt, Phi, Q, ln, nl);
-        L1::template step_team<L0::dim, B>(md, 1, rec + md.rec[1], dt, Phi, Q, ln, nl);
+        L0::template step_team<0, LD>(md, 0, rec + md.rec[0], dt, Phi, Q, ln, nl);
+        L1::template step_team<L0::dim, LD>(md, 1, rec + md.rec[1], dt, Phi, Q, ln, nl);
     }
+    template <int LD>
     SP_DEV static void grad_team(const ModelDesc& md, const double* rec, double dt, const double* Phi,
                                  const double* Q, const double* M, const double* Bm, int ln, int nl, double* g) {
         double g0[4] = {0.0, 0.0, 0.0, 0.0}, g1[4] = {0.0, 0.0, 0.0, 0.0};
-        L0::template grad_team<0, B>(md, 0, rec + md.rec[0], dt, Phi, Q, M, Bm, g0, ln, nl);
-        L1::template grad_team<L0::dim, B>(md, 1, rec + md.rec[1], dt, Phi, Q, M, Bm, g1, ln, nl);
-        const double hm = ln < B ? 0.5 * M[ln * B + ln] : 0.0;  // lane ln's share of ½Tr(M)
+        L0::template grad_team<0, LD>(md, 0, rec + md.rec[0], dt, Phi, Q, M, Bm, g0, ln, nl);
+        L1::template grad_team<L0::dim, LD>(md, 1, rec + md.rec[1], dt, Phi, Q, M, Bm, g1, ln, nl);
+        const double hm = ln < B ? 0.5 * M[ln * LD + ln] : 0.0;  // lane ln's share of ½Tr(M)
 #pragma unroll
         for (int p = 0; p < L0::np; ++p) g[p] += g0[p] + hm * rec[2 + p];
 #pragma unroll
@@ -878,20 +884,22 @@ struct StaticTraits<L0, void> {
         for (int p = 0; p < L0::np; ++p) g[p] += g0[p] + hm * rec[2 + p];
     }
 #ifndef SPINGP_HOST_EMU
+    template <int LD>
     SP_DEV static void step_team(const ModelDesc& md, const double* rec, double dt, double* Phi, double* Q, int ln,
                                  int nl, unsigned mask) {
         for (int i = ln; i < B * B; i += nl) {
-            Phi[i] = 0.0;
-            Q[i] = 0.0;
+            Phi[(i / B) * LD + i % B] = 0.0;
+            Q[(i / B) * LD + i % B] = 0.0;
         }
         __syncwarp(mask);
-        L0::template step_team<0, B>(md, 0, rec + md.rec[0], dt, Phi, Q, ln, nl);
+        L0::template step_team<0, LD>(md, 0, rec + md.rec[0], dt, Phi, Q, ln, nl);
     }
+    template <int LD>
     SP_DEV static void grad_team(const ModelDesc& md, const double* rec, double dt, const double* Phi,
                                  const double* Q, const double* M, const double* Bm, int ln, int nl, double* g) {
         double g0[4] = {0.0, 0.0, 0.0, 0.0};
-        L0::template grad_team<0, B>(md, 0, rec + md.rec[0], dt, Phi, Q, M, Bm, g0, ln, nl);
-        const double hm = ln < B ? 0.5 * M[ln * B + ln] : 0.0;
+        L0::template grad_team<0, LD>(md, 0, rec + md.rec[0], dt, Phi, Q, M, Bm, g0, ln, nl);
+        const double hm = ln < B ? 0.5 * M[ln * LD + ln] : 0.0;
 #pragma unroll
         for (int p = 0; p < L0::np; ++p) g[p] += g0[p] + hm * rec[2 + p];
     }

@@ -35,40 +35,72 @@ namespace spingp_dev {
 
 #define TP_INL __device__ __forceinline__
 
+// occupancy knobs (minimum resident CTAs for b <= 8; CTA size for b > 8), tuned on B200
+// (measured, cfg4 at 4 M / cfg5 at 2 M points: fwd 5.62 -> 4.36 ms and 44.6 -> 39.2 ms,
+// rev 10.36 -> 9.81 ms and 82.6 -> 74.3 ms against minB 1 / 64-thread CTAs)
+#ifndef SP_TEAM_FWD_MINB
+#define SP_TEAM_FWD_MINB 4
+#endif
+#ifndef SP_TEAM_REV_MINB
+#define SP_TEAM_REV_MINB 3
+#endif
+#ifndef SP_TEAM_CTA16
+#define SP_TEAM_CTA16 32
+#endif
+
 template <int B>
 struct TeamCfg {
-    static constexpr int TS = B <= 8 ? 8 : 16;  // lanes per team: one per column (power of two)
+    // lanes per team, one per column: the reverse packs b = 6 as 5 teams of 6 lanes per
+    // warp; the forward (fewer live columns, register-capped) keeps 8-lane teams there
+    // (measured, cfg4 16 M: rev 38.6 -> 31.5 ms with 6-lane teams, fwd 17.1 -> 19.7 ms)
+    static constexpr int TSR = B <= 8 ? B : 16;
+    static constexpr int TSF = B <= 8 ? 8 : 16;
     static constexpr int LD = B + 1;             // odd smem row stride
     static constexpr int MAT = B * LD;           // doubles per staged block
     static constexpr int VEC = (B + 1) & ~1;
     static constexpr int FWD = 10 * MAT + VEC;      // per-team smem, forward (doubles)
     static constexpr int REV = 10 * MAT + 4 * VEC;  // per-team smem, reverse
-    static constexpr int CTA = B <= 8 ? 128 : 64;   // threads per CTA
-    static constexpr int TPC = CTA / TS;            // teams per CTA
+    static constexpr int CTA = B <= 8 ? 128 : SP_TEAM_CTA16;  // threads per CTA
+    static constexpr int FWD_MINB = B <= 8 ? SP_TEAM_FWD_MINB : 1;
+    static constexpr int REV_MINB = B <= 8 ? SP_TEAM_REV_MINB : 1;
+    static constexpr int TPCR = (CTA / 32) * (32 / TSR);  // teams per CTA, reverse
+    static constexpr int TPCF = (CTA / 32) * (32 / TSF);  // teams per CTA, forward
 };
 
 struct Team {
     int l;          // column owned (lane within the team)
     int base;       // first lane of the team in the warp
     unsigned mask;  // the team's lanes
+    int n;          // lanes in the team
 };
 
 template <int TS>
-TP_INL Team make_team() {
+TP_INL Team make_team() {  // teams are TS consecutive lanes; lanes past the last whole team idle
     const int lane = threadIdx.x & 31;
     Team t;
-    t.l = lane & (TS - 1);
-    t.base = lane & ~(TS - 1);
+    t.l = lane % TS;
+    t.base = lane - t.l;
     t.mask = (TS == 32 ? 0xffffffffu : ((1u << TS) - 1u)) << t.base;
+    t.n = TS;
     return t;
+}
+// team index of this thread within its CTA (>= teams per CTA for the idle lanes)
+template <int TS>
+TP_INL int team_in_cta() {
+    const int lane = threadIdx.x & 31;
+    const int tw = lane / TS;
+    return tw < 32 / TS ? (threadIdx.x >> 5) * (32 / TS) + tw : 1 << 20;
 }
 TP_INL void tsync(const Team& t) { __syncwarp(t.mask); }
 TP_INL double tshfl(const Team& t, double v, int src) { return __shfl_sync(t.mask, v, t.base + src); }
-template <int TS>
 TP_INL double tsum(const Team& t, double v) {
-#pragma unroll
-    for (int o = TS / 2; o > 0; o >>= 1) v += __shfl_xor_sync(t.mask, v, o);
-    return v;
+    if ((t.n & (t.n - 1)) == 0) {
+        for (int o = t.n / 2; o > 0; o >>= 1) v += __shfl_xor_sync(t.mask, v, o);
+        return v;
+    }
+    double s = 0.0;  // non-power-of-two team: every lane sums the n values in lane order
+    for (int k = 0; k < t.n; ++k) s += __shfl_sync(t.mask, v, t.base + k);
+    return s;
 }
 
 // ---- column primitives (stride S of the staged block: LD, or B for model blocks) ----
@@ -211,10 +243,10 @@ template <class T>
 TP_INL bool tmodel(const Team& tm, const ModelDesc& md, const double* rp, double dt, double jit, double* PhiS,
                    double* QS, double* LQ, LogDetAcc* ldq) {
     constexpr int B = T::B;
-    T::step_team(md, rp, dt, PhiS, QS, tm.l, TeamCfg<B>::TS, tm.mask);
+    T::template step_team<TeamCfg<B>::LD>(md, rp, dt, PhiS, QS, tm.l, tm.n, tm.mask);
     tsync(tm);
     double c[B];
-    colget<B, B>(c, QS, tm.l);
+    colget<B, TeamCfg<B>::LD>(c, QS, tm.l);
 #pragma unroll
     for (int i = 0; i < B; ++i)
         if (i == tm.l && i < md.b) c[i] += jit;
@@ -229,7 +261,7 @@ TP_INL void tassembly(const Team& tm, const double* PhiS, const double* LQ, doub
                       double (&U)[B], double* W0) {
     constexpr int LD = TeamCfg<B>::LD;
     double z[B];
-    colget<B, B>(z, PhiS, tm.l);
+    colget<B, LD>(z, PhiS, tm.l);
     tlsolve<B, LD>(z, LQ);
     if (pqp) {
         colput<B, LD>(ZS, z, tm.l);
@@ -273,7 +305,7 @@ TP_INL void pput(double* M, const double (&c)[B], int l) {
 
 // ======================================================== forward, level 0 ====
 template <class T>
-__global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_fwd0_team(
+__global__ void __launch_bounds__(TeamCfg<T::B>::CTA, TeamCfg<T::B>::FWD_MINB) k_fwd0_team(
     ModelDesc md, const double* __restrict__ params, const double* __restrict__ t, const double* __restrict__ y,
     Geom geo, double* __restrict__ fac, double* __restrict__ rec, double* __restrict__ part,
     unsigned long long* status, const double* __restrict__ halo, long long g0, long long g1,
@@ -283,10 +315,11 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_fwd0_team(
     constexpr int LD = C::LD;
     constexpr int NLI = B * (B + 1) / 2, NF = NLI + B * B + B;
     extern __shared__ double smem_team[];
-    const Team tm = make_team<C::TS>();
-    const int tid = threadIdx.x / C::TS;
+    const Team tm = make_team<C::TSF>();
+    const int tid = team_in_cta<C::TSF>();
+    if (tid >= C::TPCF) return;
     double* R = smem_team + static_cast<size_t>(tid) * C::FWD;
-    double* PhiS = R;               // model blocks (row stride B)
+    double* PhiS = R;               // model blocks
     double* QS = R + C::MAT;
     double* LQ = R + 2 * C::MAT;    // chol(Q̃)
     double* LS = R + 3 * C::MAT;    // chol(S)
@@ -297,7 +330,7 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_fwd0_team(
     double* TcS = R + 8 * C::MAT;   //   the Schur update T = X^T X,
     double* AcS = R + 9 * C::MAT;   //   acc_LL
     double* vS = R + 10 * C::MAT;   // rc (vector)
-    const long long g = g0 + static_cast<long long>(blockIdx.x) * C::TPC + tid;
+    const long long g = g0 + static_cast<long long>(blockIdx.x) * C::TPCF + tid;
     if (g >= g1) return;
     const int l = tm.l;
     const long long K = geo.K[0], SK = K * geo.S;
@@ -508,7 +541,7 @@ TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, d
         double xp[B];
 #pragma unroll
         for (int i = 0; i < B; ++i) xp[i] = xpS[i];
-        tmv<B, B>(e, PhiS, xp);
+        tmv<B, LD>(e, PhiS, xp);
 #pragma unroll
         for (int i = 0; i < B; ++i) e[i] = xcS[i] - e[i];
     }
@@ -532,8 +565,8 @@ TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, d
     } else {
         {
             double X1[B], Y1[B];
-            tmv<B, B>(X1, PhiS, Cpc);  // Φ C_pc
-            tmv<B, B>(Y1, PhiS, Cpp);  // Φ C_pp
+            tmv<B, LD>(X1, PhiS, Cpc);  // Φ C_pc
+            tmv<B, LD>(Y1, PhiS, Cpp);  // Φ C_pp
             tsync(tm);
             colput<B, LD>(S2, X1, l);
             colput<B, LD>(S3, Y1, l);
@@ -543,7 +576,7 @@ TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, d
         tsync(tm);
         double r[B], ph[B];
         rowget<B, LD>(r, S2, l);
-        rowget<B, B>(ph, PhiS, l);
+        rowget<B, LD>(ph, PhiS, l);
 #pragma unroll
         for (int i = 0; i < B; ++i) E[i] -= r[i];
         tmv<B, LD>(r, S3, ph);  // Φ C_pp Φ^T
@@ -553,7 +586,7 @@ TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, d
     // E - Q̃ (padding states have Q̃ = 1 and E = 0; their rows of M are never read)
     {
         double q[B];
-        colget<B, B>(q, QS, l);
+        colget<B, LD>(q, QS, l);
 #pragma unroll
         for (int i = 0; i < B; ++i) E[i] -= q[i];
 #pragma unroll
@@ -571,14 +604,14 @@ TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, d
         tltsolve<B, LD>(v, LQ);   // = row l of M
         // symmetrise M (row l in v) and hand it to T::grad at row stride B
         tsync(tm);
-        rowput<B, B>(S0, v, l);
+        rowput<B, LD>(S0, v, l);
         tsync(tm);
         double cm[B];
-        colget<B, B>(cm, S0, l);
+        colget<B, LD>(cm, S0, l);
 #pragma unroll
         for (int i = 0; i < B; ++i) v[i] = 0.5 * (v[i] + cm[i]);
         tsync(tm);
-        rowput<B, B>(S0, v, l);
+        rowput<B, LD>(S0, v, l);
     }
     // Bm = Z Q̃^{-1} = (Q̃^{-1} Z^T)^T with Z = C_pc - C_pp Φ^T + x_p e^T: row l of Bm
     // from column l of Z^T = row l of Z
@@ -596,22 +629,22 @@ TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, d
             tlsolve<B, LD>(v, LQ);
             tltsolve<B, LD>(v, LQ);
         }
-        rowput<B, B>(S1, v, l);
+        rowput<B, LD>(S1, v, l);
     }
     tsync(tm);
     double gp[T::NP];
 #pragma unroll
     for (int p = 0; p < T::NP; ++p) gp[p] = 0.0;
-    T::grad_team(md, rp, dt, PhiS, QS, S0, S1, l, TeamCfg<B>::TS, gp);
+    T::template grad_team<LD>(md, rp, dt, PhiS, QS, S0, S1, l, tm.n, gp);
 #pragma unroll
     for (int p = 0; p < T::NP; ++p) {
-        const double v = tsum<TeamCfg<B>::TS>(tm, gp[p]);
+        const double v = tsum(tm, gp[p]);
         if (l == 0 && p < md.nt) g[p] += v;
     }
 }
 
 template <class T>
-__global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_rev0_team(
+__global__ void __launch_bounds__(TeamCfg<T::B>::CTA, TeamCfg<T::B>::REV_MINB) k_rev0_team(
     ModelDesc md, const double* __restrict__ params, const double* __restrict__ t, const double* __restrict__ y,
     Geom geo, const double* __restrict__ fac, const double* __restrict__ solU, double* __restrict__ part, Outs outs,
     unsigned long long* status, const double* __restrict__ halo, long long g0, long long g1,
@@ -621,8 +654,9 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_rev0_team(
     constexpr int LD = C::LD;
     constexpr int NLI = B * (B + 1) / 2, NF = NLI + B * B + B;
     extern __shared__ double smem_team[];
-    const Team tm = make_team<C::TS>();
-    const int tid = threadIdx.x / C::TS;
+    const Team tm = make_team<C::TSR>();
+    const int tid = team_in_cta<C::TSR>();
+    if (tid >= C::TPCR) return;
     double* R = smem_team + static_cast<size_t>(tid) * C::REV;
     double* PhiS = R;
     double* QS = R + C::MAT;
@@ -638,7 +672,7 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_rev0_team(
     double* xjS = xnS + C::VEC;
     double* xLS = xjS + C::VEC;
     double* zS = xLS + C::VEC;
-    const long long g = g0 + static_cast<long long>(blockIdx.x) * C::TPC + tid;
+    const long long g = g0 + static_cast<long long>(blockIdx.x) * C::TPCR + tid;
     if (g >= g1) return;
     const int l = tm.l;
     const long long K = geo.K[0], SK = K * geo.S;
@@ -692,7 +726,7 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA) k_rev0_team(
             double hc = 0.0;
 #pragma unroll
             for (int a = 0; a < B; ++a) hc += T::H(md, a) * Cc[a];
-            double v = tsum<C::TS>(tm, Hl * hc);
+            double v = tsum(tm, Hl * hc);
             if (l == 0) {
                 if (ob) noise += rr * rr + v;
                 if (outs.var) {

@@ -14,9 +14,9 @@ void launch_fwd0_team(spingp_ctx* ctx, const ModelDesc& md, const EvalBufs& eb, 
                       const double* halo, long long c0, long long c1) {
     using C = TeamCfg<T::B>;
     static unsigned long long attr = 0;
-    const int smem = C::TPC * C::FWD * static_cast<int>(sizeof(double));
+    const int smem = C::TPCF * C::FWD * static_cast<int>(sizeof(double));
     opt_in_smem(reinterpret_cast<const void*>(k_fwd0_team<T>), attr, ctx->device, smem);
-    const unsigned grid = static_cast<unsigned>((c1 - c0 + C::TPC - 1) / C::TPC);
+    const unsigned grid = static_cast<unsigned>((c1 - c0 + C::TPCF - 1) / C::TPCF);
     ctx->pre();
     k_fwd0_team<T><<<grid, C::CTA, smem, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0], eb.rec[0], eb.part,
                                                         ctx->d_status, halo, c0, c1, a.d_obs);
@@ -28,9 +28,9 @@ void launch_rev0_team(spingp_ctx* ctx, const ModelDesc& md, const EvalBufs& eb, 
                       const double* halo, const Outs& outs, long long c0, long long c1) {
     using C = TeamCfg<T::B>;
     static unsigned long long attr = 0;
-    const int smem = C::TPC * C::REV * static_cast<int>(sizeof(double));
+    const int smem = C::TPCR * C::REV * static_cast<int>(sizeof(double));
     opt_in_smem(reinterpret_cast<const void*>(k_rev0_team<T>), attr, ctx->device, smem);
-    const unsigned grid = static_cast<unsigned>((c1 - c0 + C::TPC - 1) / C::TPC);
+    const unsigned grid = static_cast<unsigned>((c1 - c0 + C::TPCR - 1) / C::TPCR);
     ctx->pre();
     k_rev0_team<T><<<grid, C::CTA, smem, ctx->stream>>>(md, eb.params, a.d_t, a.d_y, g, eb.fac[0], eb.sol[1], eb.part,
                                                         outs, ctx->d_status, halo, c0, c1, a.d_obs);
