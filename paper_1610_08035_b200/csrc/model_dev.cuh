@@ -648,6 +648,7 @@ template <int BB>
 struct GenericTraits {
     static constexpr int B = BB;
     static constexpr int NP = kMaxTheta;  // gradient slots of the team reduction
+    static constexpr bool kDiag2 = false;
     SP_DEV static double H(const ModelDesc& md, int i) { return i < md.b ? md.H[i] : 0.0; }
     template <int LD = BB>  // row stride of Phi, Q (the team kernels use an odd one)
     SP_DEV static void step(const ModelDesc& md, const double* rec, double dt, double* Phi,
@@ -730,6 +731,8 @@ struct GenericTraits {
 template <int D>
 struct SMatern {
     static constexpr int dim = D, np = 2;
+    // Φ, Q block diagonal in aligned 2 x 2 blocks (the team kernels' fast path)
+    static constexpr bool kDiag2 = D == 2;
     template <int O, int LD>
     SP_DEV static void step(const ModelDesc&, int, const double* lr, double dt, double* Phi, double* Q) {
         matern_block<D, LD>(lr, dt, O, Phi, Q);
@@ -756,6 +759,7 @@ struct SMatern {
 template <int J>
 struct SEQ {
     static constexpr int dim = J, np = 2;
+    static constexpr bool kDiag2 = false;  // Q couples every modal pair
     template <int O, int LD>
     SP_DEV static void step(const ModelDesc& md, int l, const double* lr, double dt, double* Phi, double* Q) {
         eq_block<LD>(O, J, md.eqconst + md.eqc[l], lr, dt, Phi, Q);
@@ -781,6 +785,7 @@ struct SEQ {
 template <int J>
 struct SQP {
     static constexpr int dim = 2 * (J + 1), np = 4;
+    static constexpr bool kDiag2 = true;  // one 2 x 2 rotation block per harmonic
     template <int O, int LD>
     SP_DEV static void step(const ModelDesc&, int, const double* lr, double dt, double* Phi, double* Q) {
         qp_block<LD>(O, J, lr, dt, Phi, Q);
@@ -809,6 +814,7 @@ template <class L0, class L1 = void>
 struct StaticTraits {
     static constexpr int B = L0::dim + L1::dim;
     static constexpr int NP = L0::np + L1::np;
+    static constexpr bool kDiag2 = L0::kDiag2 && L1::kDiag2 && (L0::dim % 2 == 0);
     SP_DEV static double H(const ModelDesc& md, int i) { return md.H[i]; }
     SP_DEV static void step(const ModelDesc& md, const double* rec, double dt, double* Phi, double* Q) {
         mzero<B>(Phi);
@@ -865,6 +871,7 @@ template <class L0>
 struct StaticTraits<L0, void> {
     static constexpr int B = L0::dim;
     static constexpr int NP = L0::np;
+    static constexpr bool kDiag2 = L0::kDiag2;
     SP_DEV static double H(const ModelDesc& md, int i) { return md.H[i]; }
     SP_DEV static void step(const ModelDesc& md, const double* rec, double dt, double* Phi, double* Q) {
         mzero<B>(Phi);

@@ -182,6 +182,53 @@ TP_INL void tltsolve(double (&c)[B], const double* L) {
         c[i] = s * L[i * S + i];
     }
 }
+// Solves and products with the MODEL blocks (L_Q, Φ).  D2 = the model is block diagonal
+// in aligned 2 x 2 blocks (Matérn-3/2 + quasi-periodic sums, T::kDiag2): only the two
+// in-block terms of every sum are formed.  The dense loops would add exact zeros in the
+// same order, so both branches give identical results on such models.
+template <int B, bool D2>
+TP_INL void mlsolve(double (&c)[B], const double* L) {
+    constexpr int LD = TeamCfg<B>::LD;
+    if constexpr (D2) {
+#pragma unroll
+        for (int p = 0; p < B / 2; ++p) {
+            const int i = 2 * p;
+            c[i] = c[i] * L[i * LD + i];
+            c[i + 1] = fma(-L[(i + 1) * LD + i], c[i], c[i + 1]) * L[(i + 1) * LD + i + 1];
+        }
+    } else {
+        tlsolve<B, LD>(c, L);
+    }
+}
+template <int B, bool D2>
+TP_INL void mltsolve(double (&c)[B], const double* L) {
+    constexpr int LD = TeamCfg<B>::LD;
+    if constexpr (D2) {
+#pragma unroll
+        for (int p = 0; p < B / 2; ++p) {
+            const int i = 2 * p;
+            c[i + 1] = c[i + 1] * L[(i + 1) * LD + i + 1];
+            c[i] = fma(-L[(i + 1) * LD + i], c[i + 1], c[i]) * L[i * LD + i];
+        }
+    } else {
+        tltsolve<B, LD>(c, L);
+    }
+}
+template <int B, bool D2>
+TP_INL void mmv(double (&o)[B], const double* Phi, const double (&c)[B]) {  // o = Φ c
+    constexpr int LD = TeamCfg<B>::LD;
+    if constexpr (D2) {
+#pragma unroll
+        for (int p = 0; p < B / 2; ++p) {
+            const int i = 2 * p;
+            o[i] = fma(Phi[i * LD + i + 1], c[i + 1], Phi[i * LD + i] * c[i]);
+            o[i + 1] = fma(Phi[(i + 1) * LD + i + 1], c[i + 1], Phi[(i + 1) * LD + i] * c[i]);
+        }
+    } else {
+        tmv<B, LD>(o, Phi, c);
+    }
+}
+
 // Cholesky of the symmetric block whose column l is c (lower part read): L (inverted
 // pivots, devmat.cuh chol_nolog arithmetic) staged at Ls; team-uniform success flag.
 // The per-element fma order (k ascending from S[i][l]) equals the left-looking one.
@@ -243,8 +290,40 @@ template <class T>
 TP_INL bool tmodel(const Team& tm, const ModelDesc& md, const double* rp, double dt, double jit, double* PhiS,
                    double* QS, double* LQ, LogDetAcc* ldq) {
     constexpr int B = T::B;
-    T::template step_team<TeamCfg<B>::LD>(md, rp, dt, PhiS, QS, tm.l, tm.n, tm.mask);
+    constexpr int LD = TeamCfg<B>::LD;
+    T::template step_team<LD>(md, rp, dt, PhiS, QS, tm.l, tm.n, tm.mask);
     tsync(tm);
+    if constexpr (T::kDiag2) {
+        // 2 x 2 pivots of the block-diagonal Q̃, every lane all of them (the dense tchol's
+        // arithmetic and log-det grouping); lane 2p stores block p of L_Q
+        bool ok = true;
+        double p4 = 1.0;
+#pragma unroll
+        for (int p = 0; p < B / 2; ++p) {
+            const int i = 2 * p;
+            const double a = QS[i * LD + i] + (i < md.b ? jit : 0.0);
+            const double bq = QS[(i + 1) * LD + i];
+            const double cq = QS[(i + 1) * LD + i + 1] + (i + 1 < md.b ? jit : 0.0);
+            const double inv0 = rsqrt(a);
+            const double l10 = bq * inv0;
+            const double d = fma(-l10, l10, cq);
+            const double inv1 = rsqrt(d);
+            ok = ok && (a > 0.0) && isfinite(a) && (d > 0.0) && isfinite(d);
+            if (tm.l == i) {
+                LQ[i * LD + i] = inv0;
+                LQ[(i + 1) * LD + i] = l10;
+                LQ[(i + 1) * LD + i + 1] = inv1;
+            }
+            if (ldq) {
+                p4 *= inv0;
+                if (((i) & 3) == 3) { ldq->mul(p4); p4 = 1.0; }
+                p4 *= inv1;
+                if (((i + 1) & 3) == 3 || i + 1 == B - 1) { ldq->mul(p4); p4 = 1.0; }
+            }
+        }
+        tsync(tm);
+        return ok;
+    }
     double c[B];
     colget<B, TeamCfg<B>::LD>(c, QS, tm.l);
 #pragma unroll
@@ -256,10 +335,43 @@ TP_INL bool tmodel(const Team& tm, const ModelDesc& md, const double* rp, double
 // Assembly pieces of one step (engine.cuh step_assembly): column l of
 //   PQP = Φ^T Q̃^{-1} Φ = Z^T Z (Z = L_Q^{-1} Φ)   and   U = -Φ^T Q̃^{-1} = -(L_Q^{-T} Z)^T;
 // optionally column l of W0 = U^T = -Q̃^{-1} Φ (the first block's left coupling).
-template <int B>
+template <int B, bool D2 = false>
 TP_INL void tassembly(const Team& tm, const double* PhiS, const double* LQ, double* ZS, double* WS, double* pqp,
                       double (&U)[B], double* W0) {
     constexpr int LD = TeamCfg<B>::LD;
+    if constexpr (D2) {
+        // Z = L_Q^{-1} Φ, Z^T Z and Q̃^{-1} Φ are block diagonal: column l has entries only
+        // in its block (2p, 2p+1); the partner column comes from lane l ^ 1
+        const int l = tm.l, i0 = l & ~1;
+        double z[B];
+        colget<B, LD>(z, PhiS, l);
+        mlsolve<B, true>(z, LQ);
+        const double z0 = pick<B>(z, i0), z1 = pick<B>(z, i0 + 1);
+        const double y0 = __shfl_xor_sync(tm.mask, z0, 1), y1 = __shfl_xor_sync(tm.mask, z1, 1);
+        const double e0 = (l & 1) ? y0 : z0, e1 = (l & 1) ? y1 : z1;  // column i0 of Z
+        const double o0 = (l & 1) ? z0 : y0, o1 = (l & 1) ? z1 : y1;  // column i0 + 1 of Z
+        if (pqp) {
+#pragma unroll
+            for (int i = 0; i < B; ++i) pqp[i] = 0.0;
+            const double v0 = fma(e1, z1, e0 * z0), v1 = fma(o1, z1, o0 * z0);
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                if (i == i0) pqp[i] = v0;
+                if (i == i0 + 1) pqp[i] = v1;
+            }
+        }
+        mltsolve<B, true>(z, LQ);  // column l of Q̃^{-1} Φ
+        if (W0)
+#pragma unroll
+            for (int i = 0; i < B; ++i) W0[i] = -z[i];
+        // U = -(Q̃^{-1} Φ)^T: column l = -(row l), whose block entries are column i0's and
+        // column i0+1's element l
+        const double own = pick<B>(z, l), oth = __shfl_xor_sync(tm.mask, pick<B>(z, l ^ 1), 1);
+        const double a0 = (l & 1) ? oth : own, a1 = (l & 1) ? own : oth;
+#pragma unroll
+        for (int i = 0; i < B; ++i) U[i] = i == i0 ? -a0 : (i == i0 + 1 ? -a1 : 0.0);
+        return;
+    }
     double z[B];
     colget<B, LD>(z, PhiS, tm.l);
     tlsolve<B, LD>(z, LQ);
@@ -283,10 +395,21 @@ TP_INL void tassembly(const Team& tm, const double* PhiS, const double* LQ, doub
 }
 
 // column l of Q̃^{-1} (engine.cuh chol_inv_solve, symmetrised)
-template <int B>
+template <int B, bool D2 = false>
 TP_INL void tqinv(const Team& tm, double (&q)[B], const double* LQ, double* scratch) {
     constexpr int LD = TeamCfg<B>::LD;
     unitcol<B>(q, tm.l);
+    if constexpr (D2) {
+        mlsolve<B, true>(q, LQ);
+        mltsolve<B, true>(q, LQ);
+        // symmetrise the in-block pair with the partner column
+        const int l = tm.l;
+        const double mine = pick<B>(q, l ^ 1), theirs = __shfl_xor_sync(tm.mask, mine, 1);
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+            if (i == (l ^ 1)) q[i] = 0.5 * (q[i] + theirs);
+        return;
+    }
     tlsolve<B, LD>(q, LQ);
     tltsolve<B, LD>(q, LQ);
     tsym<B>(tm, q, scratch);
@@ -361,7 +484,7 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA, TeamCfg<T::B>::FWD_MINB) k
     }
     {
         double q[B];
-        tqinv<B>(tm, q, LQ, XS);
+        tqinv<B, T::kDiag2>(tm, q, LQ, XS);
         pput<B>(QiS, q, l);
 #pragma unroll
         for (int i = 0; i < B; ++i) q[i] = 0.0;
@@ -369,7 +492,7 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA, TeamCfg<T::B>::FWD_MINB) k
         pput<B>(AcS, q, l);
         if (hasL) {  // P_{st, st-1} = U_{st-1}^T = -Q̃_st^{-1} Φ_st
             double U[B], W[B];
-            tassembly<B>(tm, PhiS, LQ, XS, YS, nullptr, U, W);
+            tassembly<B, T::kDiag2>(tm, PhiS, LQ, XS, YS, nullptr, U, W);
             pput<B>(WS, W, l);
         } else {
             pput<B>(WS, q, l);
@@ -392,7 +515,7 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA, TeamCfg<T::B>::FWD_MINB) k
             return;
         }
         double D[B], U[B];
-        tassembly<B>(tm, PhiS, LQ, XS, YS, D, U, nullptr);
+        tassembly<B, T::kDiag2>(tm, PhiS, LQ, XS, YS, D, U, nullptr);
         const double wo = (!obs || obs[gbase + j]) ? 1.0 : 0.0;
         const double yj = wo != 0.0 ? ys[j] : 0.0;
         if (!isfinite(yj)) {
@@ -413,7 +536,7 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA, TeamCfg<T::B>::FWD_MINB) k
         }
         {
             double q[B];
-            tqinv<B>(tm, q, LQ, PhiS);  // Q̃_{j+1}^{-1}: the next block's diagonal term
+            tqinv<B, T::kDiag2>(tm, q, LQ, PhiS);  // Q̃_{j+1}^{-1}: the next block's diagonal term
             pput<B>(QiS, q, l);
         }
         double z[B];
@@ -487,7 +610,7 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA, TeamCfg<T::B>::FWD_MINB) k
             return;
         }
         double pqp[B], U[B];
-        tassembly<B>(tm, PhiS, LQ, XS, YS, pqp, U, nullptr);
+        tassembly<B, T::kDiag2>(tm, PhiS, LQ, XS, YS, pqp, U, nullptr);
 #pragma unroll
         for (int i = 0; i < B; ++i) D[i] += pqp[i];
     }
@@ -532,6 +655,7 @@ TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, d
                         bool grad, double& fe, double* g, double* S0, double* S1, double* S2, double* S3) {
     constexpr int B = T::B;
     constexpr int LD = TeamCfg<B>::LD;
+    constexpr bool D2 = T::kDiag2;
     const int l = tm.l;
     double e[B];
     if (anchor) {
@@ -541,7 +665,7 @@ TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, d
         double xp[B];
 #pragma unroll
         for (int i = 0; i < B; ++i) xp[i] = xpS[i];
-        tmv<B, LD>(e, PhiS, xp);
+        mmv<B, D2>(e, PhiS, xp);
 #pragma unroll
         for (int i = 0; i < B; ++i) e[i] = xcS[i] - e[i];
     }
@@ -549,7 +673,7 @@ TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, d
         double u[B];
 #pragma unroll
         for (int i = 0; i < B; ++i) u[i] = e[i];
-        tlsolve<B, LD>(u, LQ);
+        mlsolve<B, D2>(u, LQ);
         double q = 0.0;
 #pragma unroll
         for (int i = 0; i < B; ++i) q += u[i] * u[i];
@@ -565,8 +689,8 @@ TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, d
     } else {
         {
             double X1[B], Y1[B];
-            tmv<B, LD>(X1, PhiS, Cpc);  // Φ C_pc
-            tmv<B, LD>(Y1, PhiS, Cpp);  // Φ C_pp
+            mmv<B, D2>(X1, PhiS, Cpc);  // Φ C_pc
+            mmv<B, D2>(Y1, PhiS, Cpp);  // Φ C_pp
             tsync(tm);
             colput<B, LD>(S2, X1, l);
             colput<B, LD>(S3, Y1, l);
@@ -579,7 +703,23 @@ TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, d
         rowget<B, LD>(ph, PhiS, l);
 #pragma unroll
         for (int i = 0; i < B; ++i) E[i] -= r[i];
-        tmv<B, LD>(r, S3, ph);  // Φ C_pp Φ^T
+        if constexpr (D2) {  // row l of Φ has its two entries in block (i0, i0+1)
+            const int i0 = l & ~1;
+            const double p0 = pick<B>(ph, i0), p1 = pick<B>(ph, i0 + 1);
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+                for (int k = 0; k < B; k += 2)
+                    if (k == i0) {
+                        a0 = S3[i * LD + k];
+                        a1 = S3[i * LD + k + 1];
+                    }
+                r[i] = fma(a1, p1, a0 * p0);
+            }
+        } else {
+            tmv<B, LD>(r, S3, ph);  // Φ C_pp Φ^T
+        }
 #pragma unroll
         for (int i = 0; i < B; ++i) E[i] = (E[i] + r[i]) + e[i] * el;
     }
@@ -595,13 +735,13 @@ TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, d
     }
     tsym<B>(tm, E, S0);
     // M = Q̃^{-1}(E - Q̃)Q̃^{-1}: G = Q̃^{-1}(E - Q̃) by columns, then M = (Q̃^{-1} G^T)^T by rows
-    tlsolve<B, LD>(E, LQ);
-    tltsolve<B, LD>(E, LQ);
+    mlsolve<B, D2>(E, LQ);
+    mltsolve<B, D2>(E, LQ);
     {
         double v[B];
         ttrans<B>(tm, v, E, S1);  // column l of G^T
-        tlsolve<B, LD>(v, LQ);
-        tltsolve<B, LD>(v, LQ);   // = row l of M
+        mlsolve<B, D2>(v, LQ);
+        mltsolve<B, D2>(v, LQ);   // = row l of M
         // symmetrise M (row l in v) and hand it to T::grad at row stride B
         tsync(tm);
         rowput<B, LD>(S0, v, l);
@@ -626,8 +766,8 @@ TP_INL void tstep_terms(const Team& tm, const ModelDesc& md, const double* rp, d
 #pragma unroll
             for (int i = 0; i < B; ++i) v[i] = Cpc[i] - y1r[i] + xpS[i] * el;
             ttrans<B>(tm, v, v, S2);
-            tlsolve<B, LD>(v, LQ);
-            tltsolve<B, LD>(v, LQ);
+            mlsolve<B, D2>(v, LQ);
+            mltsolve<B, D2>(v, LQ);
         }
         rowput<B, LD>(S1, v, l);
     }
@@ -744,7 +884,7 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA, TeamCfg<T::B>::REV_MINB) k
         tsync(tm);
         tmodel<T>(tm, md, rp, dt, jit, PhiS, QS, LQ, &ldq);
         double X[B];
-        tassembly<B>(tm, PhiS, LQ, XS, S6, nullptr, X, nullptr);  // X <- U
+        tassembly<B, T::kDiag2>(tm, PhiS, LQ, XS, S6, nullptr, X, nullptr);  // X <- U
         // factor of step j
         const double* fp = fac + (g * m + (j - st)) * static_cast<long long>(NF);
         double Y[B];
@@ -766,19 +906,26 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA, TeamCfg<T::B>::REV_MINB) k
         tsync(tm);
         // back substitution: x_j = L^{-T}(z - X x_n - Y x_L)
         {
-            double a[B], tmp[B], v[B];
+            // lane l forms component l (row l of X and Y), then every lane solves
+            double r[B];
+            if (l < B) {
+                double sx = 0.0, sy = 0.0;
+                rowget<B, LD>(r, XS, l);
 #pragma unroll
-            for (int i = 0; i < B; ++i) v[i] = xnS[i];
-            tmv<B, LD>(tmp, XS, v);
+                for (int k = 0; k < B; ++k) sx = fma(r[k], xnS[k], sx);
+                double al = zS[l] - sx;
+                if (hasL) {
+                    rowget<B, LD>(r, YS, l);
 #pragma unroll
-            for (int i = 0; i < B; ++i) a[i] = zS[i] - tmp[i];
-            if (hasL) {
-#pragma unroll
-                for (int i = 0; i < B; ++i) v[i] = xLS[i];
-                tmv<B, LD>(tmp, YS, v);
-#pragma unroll
-                for (int i = 0; i < B; ++i) a[i] -= tmp[i];
+                    for (int k = 0; k < B; ++k) sy = fma(r[k], xLS[k], sy);
+                    al -= sy;
+                }
+                zS[l] = al;
             }
+            tsync(tm);
+            double a[B];
+#pragma unroll
+            for (int i = 0; i < B; ++i) a[i] = zS[i];
             tltsolve<B, LD>(a, LS);
             if (l < B) xjS[l] = pick<B>(a, l);
         }
