@@ -12,6 +12,10 @@
 // Here: L-BFGS (memory 8) on x = log(theta..., sigma_n) with an Armijo backtracking line
 // search (c1 = 1e-4, halving, <= 40 trials; trial points that fail to factorise count as
 // rejected).  sigma_n is the noise standard deviation (NoiseModel holds sigma_n^2).
+// The backtracking trials go to the GPU kProbes at a time (step a, a/2, a/4, a/8 in one
+// batched evaluation, spingp_eval_multi_theta: the series is uploaded once and the
+// probes run as independent series); the first trial, in that order, that satisfies
+// Armijo is accepted, exactly as with one trial per call.
 
 #include <algorithm>
 #include <cmath>
@@ -52,6 +56,39 @@ inline Probe mll_probe(const Dataset& data, const KernelSpec& spec, const std::v
     for (size_t i = 0; i < p; ++i) pr.g[i] = o.grad[i] * theta[i];  // chain rule to log space
     pr.g[p] = o.grad[p] * sigma;
     return pr;
+}
+
+constexpr int kProbes = 4;
+
+// kProbes (or fewer) trial points in one batched GPU evaluation.  Probes from the first
+// one that did not factorise on are left at f = -inf (the status word names only the
+// first failing probe).
+inline std::vector<Probe> mll_probes(const Dataset& data, const KernelSpec& spec,
+                                     const std::vector<std::vector<double>>& xs, Device& dev) {
+    check_data(data, NoiseModel{1.0});
+    const size_t K = xs.size(), d = xs[0].size(), p = d - 1;
+    const auto lv = leaves_of(spec);
+    std::vector<double> theta(K * p), sigma(K), ll(K), g(K * d);
+    for (size_t k = 0; k < K; ++k) {
+        for (size_t i = 0; i < p; ++i) theta[k * p + i] = std::exp(xs[k][i]);
+        sigma[k] = std::exp(xs[k][p]);
+    }
+    int64_t bad = -1;
+    const int st = spingp_eval_multi_theta(dev.get(), lv.data(), static_cast<int32_t>(lv.size()), theta.data(),
+                                           static_cast<int32_t>(p), static_cast<int64_t>(K), data.times.data(),
+                                           data.values.data(), static_cast<int64_t>(data.times.size()), sigma.data(),
+                                           SPINGP_WANT_GRAD, ll.data(), g.data(), &bad);
+    size_t valid = K;
+    if (st == SPINGP_NOT_PD || st == SPINGP_SINGULAR_Q) valid = bad >= 0 ? static_cast<size_t>(bad) : 0;
+    else Device::check(st, bad);
+    std::vector<Probe> out(K);
+    for (size_t k = 0; k < valid && k < K; ++k) {
+        out[k].f = ll[k];
+        out[k].g.resize(d);
+        for (size_t i = 0; i < p; ++i) out[k].g[i] = g[k * d + i] * theta[k * p + i];  // to log space
+        out[k].g[p] = g[k * d + p] * sigma[k];
+    }
+    return out;
 }
 
 }  // namespace detail
@@ -128,16 +165,29 @@ inline OptimizeResult optimize_hyperparameters(const Dataset& data, const Kernel
         bool accepted = false;
         std::vector<double> xn(d);
         detail::Probe nxt;
-        for (int tr = 0; tr < 40; ++tr, a *= 0.5) {
-            for (size_t i = 0; i < d; ++i) xn[i] = x[i] + a * dir[i];
-            try {
-                nxt = detail::mll_probe(data, spec, xn, dev);
-            } catch (const NotPositiveDefinite&) {
-                continue;  // a trial point that does not factorise is rejected
+        for (int tr = 0; tr < 40 && !accepted;) {
+            const int K = std::min(detail::kProbes, 40 - tr);
+            std::vector<std::vector<double>> xs(static_cast<size_t>(K), std::vector<double>(d));
+            std::vector<double> as(static_cast<size_t>(K));
+            for (int k = 0; k < K; ++k, a *= 0.5) {
+                as[static_cast<size_t>(k)] = a;
+                for (size_t i = 0; i < d; ++i) xs[static_cast<size_t>(k)][i] = x[i] + a * dir[i];
             }
-            if (std::isfinite(nxt.f) && -nxt.f <= -cur.f + 1e-4 * a * slope) {
-                accepted = true;
-                break;
+            const auto pr = detail::mll_probes(data, spec, xs, dev);
+            for (int k = 0; k < K; ++k) {
+                const auto& q = pr[static_cast<size_t>(k)];
+                if (!std::isfinite(q.f)) {  // did not factorise: rejected; later probes re-run
+                    a = as[static_cast<size_t>(k)] * 0.5;
+                    tr += k + 1;
+                    break;
+                }
+                if (-q.f <= -cur.f + 1e-4 * as[static_cast<size_t>(k)] * slope) {
+                    accepted = true;
+                    xn = xs[static_cast<size_t>(k)];
+                    nxt = q;
+                    break;
+                }
+                if (k == K - 1) tr += K;
             }
         }
         if (!accepted) {

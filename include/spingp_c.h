@@ -216,6 +216,15 @@ int spingp_seg_reverse_device(spingp_ctx* ctx, const spingp_leaf* leaves, int32_
 int spingp_seg_finalize_device(spingp_ctx* ctx, int32_t n_theta, int64_t n_total, double sigma, uint32_t flags,
                                const double* d_partials, double* d_loglik, double* d_grad);
 
+/* K hyperparameter vectors theta[K][n_theta] (noise std-devs sigma[K]) on ONE series:
+ * the optimizer's line-search probes in one batched evaluation.
+ * t, y are uploaded once.  out_loglik[K], out_grad[K][n_theta+1]; on failure
+ * fail_series = the first failing probe (its loglik is not meaningful). */
+int spingp_eval_multi_theta(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves, const double* theta,
+                            int32_t n_theta, int64_t K, const double* t, const double* y, int64_t n,
+                            const double* sigma, uint32_t flags, double* out_loglik, double* out_grad,
+                            int64_t* fail_series);
+
 /* ---- multi-GPU inside the library -----------------------
  * A multi-device context: one spingp_ctx per device plus an NCCL communicator
  * (ncclCommInitAll; NCCL is dlopen'ed on first use — SPINGP_NCCL_ERR without it).

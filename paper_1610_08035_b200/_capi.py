@@ -107,6 +107,8 @@ SIGNATURES = {
     "spingp_btd_selinv": (ctypes.c_int, [_vp, _i64, _i32, _d, _d, _d, _d, _d, _i64p]),
     "spingp_btd_selinv_device": (ctypes.c_int, [_vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
     "spingp_btd_matvec": (ctypes.c_int, [_vp, _i64, _i32, _d, _d, _d, _d]),
+    "spingp_eval_multi_theta": (ctypes.c_int, [_vp, _vp, _i32, _d, _i32, _i64, _d, _d, _i64, _d, _u32, _d, _d,
+                                               _i64p]),
     "spingp_mctx_create": (ctypes.c_int, [_i32, _i32p, _P(_vp)]),
     "spingp_mctx_destroy": (ctypes.c_int, [_vp]),
     "spingp_mctx_size": (_i32, [_vp]),

@@ -502,6 +502,41 @@ int spingp_eval_batched(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_le
     });
 }
 
+// K hyperparameter vectors on ONE series (line-search probes of the optimizer):
+// t, y go up once and are replicated on the device, then one batched evaluation.
+int spingp_eval_multi_theta(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves, const double* theta,
+                            int32_t n_theta, int64_t K, const double* t, const double* y, int64_t n,
+                            const double* sigma, uint32_t flags, double* out_loglik, double* out_grad,
+                            int64_t* fail_series) {
+    return guarded(fail_series, [&] {
+        checked(ctx);
+        if (!theta || !sigma || !t || !y || !out_loglik || K < 1 || n < 1) throw std::invalid_argument("bad argument");
+        if ((flags & SPINGP_WANT_GRAD) && !out_grad) throw std::invalid_argument("gradient output is null");
+        flags &= SPINGP_WANT_GRAD;  // per-point outputs are not returned here
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        const size_t N = static_cast<size_t>(K) * n;
+        const size_t ng = (flags & SPINGP_WANT_GRAD) ? K * (static_cast<size_t>(n_theta) + 1) : 0;
+        double* d_t = ctx->host_io.get(2 * N + K + ng);
+        double* d_y = d_t + N;
+        double* d_ll = d_y + N;
+        double* d_g = d_ll + K;
+        CUDA_OK(cudaMemcpyAsync(d_t, t, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_OK(cudaMemcpyAsync(d_y, y, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        for (int64_t k = 1; k < K; ++k) {
+            CUDA_OK(cudaMemcpyAsync(d_t + k * n, d_t, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+            CUDA_OK(cudaMemcpyAsync(d_y + k * n, d_y, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        eval_batched_locked(ctx, leaves, n_leaves, theta, n_theta, K, n, d_t, d_y, sigma, flags, d_ll,
+                            ng ? d_g : nullptr, nullptr, nullptr);
+        CUDA_OK(cudaMemcpyAsync(out_loglik, d_ll, K * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        if (ng) CUDA_OK(cudaMemcpyAsync(out_grad, d_g, ng * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        int64_t fb = -1;
+        const int st = take_status(ctx, &fb);
+        if (fail_series) *fail_series = fb >= 0 ? fb / n : -1;  // the (first) failing probe
+        return st;
+    });
+}
+
 int spingp_predict(spingp_ctx* ctx, const spingp_leaf* leaves, int32_t n_leaves, const double* theta,
                    int32_t n_theta, const double* t, const double* y, int64_t n, const double* test_t, int64_t m,
                    double sigma, uint32_t flags, double* out_loglik, double* out_grad, double* out_mean,
