@@ -1,3 +1,5 @@
-python tools/team_check.py 1000000 50000 > gpurun_out/team_check3.log 2>&1
-python bench.py --config cfg4 --steps 3 --warmup 3 --no-cpu-baseline --no-per-config 2>&1 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('cfg4', d['ms_per_step'], d['kernels_ms_per_step'])" >> gpurun_out/team_check3.log
-python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "cfg4 or eval_matches" >> gpurun_out/team_check3.log 2>&1
+python tools/team_check.py 1000000 50000 > gpurun_out/team_check4.log 2>&1
+for c in cfg4 cfg5; do
+python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline --no-per-config 2>&1 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$c', d['ms_per_step'], d['kernels_ms_per_step'])" >> gpurun_out/team_check4.log
+done
+python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "cfg4 or cfg5 or eval_matches or segment" >> gpurun_out/team_check4.log 2>&1
