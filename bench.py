@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--no-per-config", action="store_true")
     ap.add_argument("--no-scaling-ref", action="store_true")
     ap.add_argument("--dry-run", action="store_true")
+    ap.add_argument("--force-segments", action="store_true",
+                    help="testing: run the N>1 segment protocol (NCCL collectives) even at one rank")
     return ap.parse_args()
 
 
@@ -98,10 +100,10 @@ def load(name, points):
     return datasets.make(name, **({"n": points} if points else {}))
 
 
-def shard(wl, rank, ws):
+def shard(wl, rank, ws, force_segments=False):
     """This rank's part of the workload: batched configs shard whole series, single
     series are cut into contiguous time segments (strong scaling)."""
-    if ws == 1:
+    if ws == 1 and not (force_segments and not wl.batched):
         return dict(kind="single" if not wl.batched else "batched", t=wl.t, y=wl.y, theta=wl.theta, sigma=wl.sigma,
                     a=0, b=len(wl.t), n_total=wl.points)
     if wl.batched:
@@ -533,12 +535,12 @@ def run_ours(args, ws, rank, local):
     torch.cuda.set_device(local)
     dist = None
     dev = torch.device("cuda", local)
-    if ws > 1:
+    if ws > 1 or args.force_segments:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     name = config_name(args, ws)
     wl = load(name, args.points)
-    sh = shard(wl, rank, ws)
+    sh = shard(wl, rank, ws, args.force_segments)
     ctx = P.Context(local)
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
@@ -561,7 +563,7 @@ def run_ours(args, ws, rank, local):
         "e2e": m["e2e"], "gpu_launches": m["launches"], "clocks": clocks,
     }
     del run
-    if ws > 1 and not args.no_scaling_ref:
+    if (ws > 1 or args.force_segments) and not args.no_scaling_ref:
         # the same workload on rank 0's GPU alone (the other ranks wait): the 1-GPU point of
         # this job's scaling curve, measured in the same process and on the same box
         if rank == 0:
@@ -588,7 +590,7 @@ def run_ours(args, ws, rank, local):
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
-    if ws > 1:
+    if dist is not None:
         dist.destroy_process_group()
 
 

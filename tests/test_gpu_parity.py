@@ -292,7 +292,8 @@ def test_device_pointer_api_on_external_stream(ctx):
 
 
 @pytest.mark.parametrize("leaves,theta", [([P.MATERN52], [2.0, 1.5]), ([P.MATERN32, P.MATERN12], [1.0, 0.7, 0.5, 2.0]),
-                                          ([P.MATERN32, (P.QP, 6)], [1.0, 10.0, 1.0, 1.0, 1.0, 20.0])])
+                                          ([P.MATERN32, (P.QP, 6)], [1.0, 10.0, 1.0, 1.0, 1.0, 20.0]),
+                                          ([(P.EQ, 6)], [1.1, 1.4])])
 @pytest.mark.parametrize("nranks", [1, 2, 3, 8])
 def test_segment_protocol_on_gpu(ctx, leaves, theta, nranks):
     """The multi-GPU partition's device half (seg_forward / seg_reverse / seg_finalize)
