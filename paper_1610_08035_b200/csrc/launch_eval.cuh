@@ -200,6 +200,9 @@ void launch_fwd0_team(spingp_ctx* ctx, const ModelDesc& md, const EvalBufs& eb, 
 template <class T>
 void launch_rev0_team(spingp_ctx* ctx, const ModelDesc& md, const EvalBufs& eb, const EvalArgs& a, const Geom& g,
                       const double* halo, const Outs& outs, long long c0, long long c1);
+template <int B>
+void launch_upper_team(spingp_ctx* ctx, const Geom& g, const EvalBufs& eb, bool do_fwd, bool do_top, bool do_rev,
+                       bool needC);
 
 template <class T>
 void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
@@ -278,6 +281,8 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
                     launch_tree<B>(ctx, TREE_FWD, ta);
                 }
                     }
+        } else if (B >= 6 && team_enabled()) {
+            if constexpr (B >= 6) launch_upper_team<B>(ctx, g, eb, true, false, false, needC);
         } else if (!fused || a.mode == 2) {
             for (int l = 1; l < g.nlev; ++l) {
                 RecSource<B> src{eb.rec[l - 1], g.K[l - 1] * g.S, g.n[l]};
@@ -314,6 +319,8 @@ void launch_eval(spingp_ctx* ctx, const EvalArgs& a) {
                 launch_tree<B>(ctx, TREE_REV, ta);
             }
             }
+    } else if (B >= 6 && team_enabled()) {
+        if constexpr (B >= 6) launch_upper_team<B>(ctx, g, eb, false, a.mode == 0, true, needC);
     } else if (fused && (a.mode == 0 || g.nlev > 1)) {
         UpperArgs ua{};
         for (int l = 0; l < g.nlev; ++l) {

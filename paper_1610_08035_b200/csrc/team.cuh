@@ -1028,4 +1028,341 @@ __global__ void __launch_bounds__(TeamCfg<T::B>::CTA, TeamCfg<T::B>::REV_MINB) k
     }
 }
 
+// ================================================== upper levels (b >= 6) ====
+// Levels >= 1 with a team per chunk of m_l records (engine.cuh fwdL_item / revL_item,
+// the same arithmetic): the blocks come from the level-(l-1) records (RecSource
+// semantics) instead of the model.  Per-thread chains kept every b x b block of these
+// levels in local memory (k_upper<16>: 18 GB of DRAM traffic per cfg5 evaluation).
+// Factor layout of level l: fac[(chunk * m_l + step) * NF + comp], NF = b(b+1)/2 + b^2 + b.
+template <int B>
+struct TeamUpper {
+    static constexpr int TS = TeamCfg<B>::TSF;
+    static constexpr int CTA = TeamCfg<B>::CTA;
+    static constexpr int TPC = (CTA / 32) * (32 / TS);
+    static constexpr int LD = TeamCfg<B>::LD;
+    static constexpr int SMF = TeamCfg<B>::pad_to(3 * TeamCfg<B>::MAT + TeamCfg<B>::VEC, TS);      // per team, fwd
+    static constexpr int SMR = TeamCfg<B>::pad_to(5 * TeamCfg<B>::MAT + 2 * TeamCfg<B>::VEC, TS);  // per team, rev
+};
+
+template <int B>
+__global__ void __launch_bounds__(TeamUpper<B>::CTA) k_fwdL_team(RecSource<B> src, Geom geo, int lev,
+                                                               double* __restrict__ fac, double* __restrict__ rec,
+                                                               unsigned long long* status) {
+    using U_ = TeamUpper<B>;
+    constexpr int LD = U_::LD;
+    constexpr int NLI = B * (B + 1) / 2, NF = NLI + B * B + B;
+    extern __shared__ double smem_team[];
+    const Team tm = make_team<U_::TS>();
+    const int tid = team_in_cta<U_::TS>();
+    if (tid >= U_::TPC) return;
+    double* R = smem_team + static_cast<size_t>(tid) * U_::SMF;
+    double* LS = R;
+    double* XS = R + TeamCfg<B>::MAT;
+    double* YS = R + 2 * TeamCfg<B>::MAT;
+    double* vS = R + 3 * TeamCfg<B>::MAT;  // rc gather
+    const long long g = static_cast<long long>(blockIdx.x) * U_::TPC + tid;
+    const long long K = geo.K[lev], SK = K * geo.S;
+    if (g >= SK) return;
+    const int l = tm.l;
+    const int s = static_cast<int>(g / K);
+    const long long c = g - s * K;
+    const long long n = geo.n[lev];
+    const int m = geo.m[lev];
+    const long long st = c * m, en = min(n, st + m);
+    const bool hasL = c > 0 || geo.segL;
+    const long long gbase = static_cast<long long>(s) * geo.n[0];
+    const long long base = static_cast<long long>(s) * n;  // this series' first record
+    const double* rr = src.rec;
+    const long long SKp = src.SKp;
+    auto dcol = [&](long long k, double (&D)[B]) {  // column l of D_k = R-part of k + L-part of k+1
+        const bool nx = k + 1 < n;
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+            D[i] = l < B ? rr[(Rec<B>::RDIAG + i * B + l) * SKp + base + k] +
+                               (nx ? rr[(Rec<B>::LDIAG + i * B + l) * SKp + base + k + 1] : 0.0)
+                         : 0.0;
+    };
+    auto rvec = [&](long long k, double (&r)[B]) {
+        const bool nx = k + 1 < n;
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+            r[i] = rr[(Rec<B>::RRHS + i) * SKp + base + k] + (nx ? rr[(Rec<B>::LRHS + i) * SKp + base + k + 1] : 0.0);
+    };
+    auto ucol = [&](long long k, double (&U)[B]) {  // column l of the (k, k+1) block
+#pragma unroll
+        for (int i = 0; i < B; ++i) U[i] = l < B ? rr[(Rec<B>::LR + i * B + l) * SKp + base + k + 1] : 0.0;
+    };
+    double Tc[B], acc[B], W[B], rc[B];
+    double accrL = 0.0, cld = 0.0;
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+        Tc[i] = 0.0;
+        acc[i] = 0.0;
+        W[i] = 0.0;
+        rc[i] = 0.0;
+    }
+    if (c == 0 && geo.segL) {  // carried to the segment's L
+#pragma unroll
+        for (int i = 0; i < B; ++i) acc[i] = l < B ? rr[(Rec<B>::LDIAG + i * B + l) * SKp + base] : 0.0;
+        accrL = l < B ? rr[(Rec<B>::LRHS + l) * SKp + base] : 0.0;
+    }
+    if (hasL)  // P_{st, st-1} = upper(st-1)^T: column l = row l of upper(st-1)
+#pragma unroll
+        for (int i = 0; i < B; ++i) W[i] = l < B ? rr[(Rec<B>::LR + l * B + i) * SKp + base + st] : 0.0;
+    LogDetAcc piv;
+    piv.init();
+    for (long long j = st; j < en - 1; ++j) {
+        double D[B], U[B], r[B];
+        dcol(j, D);
+        ucol(j, U);
+        rvec(j, r);
+#pragma unroll
+        for (int i = 0; i < B; ++i) D[i] -= Tc[i];
+        tsync(tm);
+        if (!tchol<B>(tm, D, LS, &piv)) {
+            if (l == 0) report(status, gbase + to_global(geo, lev, j), ST_NOT_PD);
+            return;
+        }
+        double z[B];
+#pragma unroll
+        for (int i = 0; i < B; ++i) z[i] = r[i] - rc[i];
+        tlsolve<B, LD>(z, LS);
+        tlsolve<B, LD>(U, LS);
+        if (hasL) tlsolve<B, LD>(W, LS);
+        colput<B, LD>(XS, U, l);
+        if (hasL) colput<B, LD>(YS, W, l);
+        tsync(tm);
+        tmtv<B, LD>(Tc, XS, U);
+        double rcl = 0.0;
+#pragma unroll
+        for (int i = 0; i < B; ++i) rcl = fma(U[i], z[i], rcl);
+        double* fp = fac + (g * m + (j - st)) * static_cast<long long>(NF);
+        if (l < B) {
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+                if (i >= l) fp[i * (i + 1) / 2 + l] = LS[i * LD + l];
+            if (hasL)
+#pragma unroll
+                for (int i = 0; i < B; ++i) fp[NLI + i * B + l] = W[i];
+            fp[NLI + B * B + l] = pick<B>(z, l);
+        }
+        if (hasL) {
+            double G[B];
+            tmtv<B, LD>(G, YS, W);
+#pragma unroll
+            for (int i = 0; i < B; ++i) acc[i] -= G[i];
+            double yz = 0.0;
+#pragma unroll
+            for (int i = 0; i < B; ++i) yz = fma(W[i], z[i], yz);
+            accrL -= yz;
+            tmtv<B, LD>(G, XS, W);
+#pragma unroll
+            for (int i = 0; i < B; ++i) W[i] = -G[i];
+        }
+        tsync(tm);
+        if (l < B) vS[l] = rcl;
+        tsync(tm);
+#pragma unroll
+        for (int i = 0; i < B; ++i) rc[i] = vS[i];
+    }
+    double D[B], r[B];
+    dcol(en - 1, D);
+    rvec(en - 1, r);
+    for (long long j = st; j < en; ++j) cld += rr[Rec<B>::LOGDET * SKp + base + j];
+    double* ro = rec + g;
+    if (l < B) {
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            ro[(Rec<B>::RDIAG + i * B + l) * SK] = D[i] - Tc[i];
+            ro[(Rec<B>::LDIAG + i * B + l) * SK] = acc[i];
+            ro[(Rec<B>::LR + l * B + i) * SK] = hasL ? W[i] : 0.0;
+        }
+        ro[(Rec<B>::RRHS + l) * SK] = pick<B>(r, l) - pick<B>(rc, l);
+        ro[(Rec<B>::LRHS + l) * SK] = accrL;
+    }
+    if (l == 0) ro[Rec<B>::LOGDET * SK] = cld + piv.logdet();
+}
+
+template <int B>
+__global__ void __launch_bounds__(TeamUpper<B>::CTA) k_revL_team(RecSource<B> src, SolSink<B> sink, Geom geo, int lev,
+                                                               const double* __restrict__ fac,
+                                                               const double* __restrict__ solU, int needC) {
+    using U_ = TeamUpper<B>;
+    constexpr int LD = U_::LD;
+    constexpr int NLI = B * (B + 1) / 2, NF = NLI + B * B + B;
+    extern __shared__ double smem_team[];
+    const Team tm = make_team<U_::TS>();
+    const int tid = team_in_cta<U_::TS>();
+    if (tid >= U_::TPC) return;
+    double* R = smem_team + static_cast<size_t>(tid) * U_::SMR;
+    double* LS = R;
+    double* XS = R + TeamCfg<B>::MAT;
+    double* YS = R + 2 * TeamCfg<B>::MAT;
+    double* vS = R + 3 * TeamCfg<B>::MAT;  // z / x_L
+    double* wS = vS + TeamCfg<B>::VEC;      // a -> x_j
+    const long long g = static_cast<long long>(blockIdx.x) * U_::TPC + tid;
+    const long long K = geo.K[lev], SK = K * geo.S;
+    if (g >= SK) return;
+    const int l = tm.l;
+    const int s = static_cast<int>(g / K);
+    const long long c = g - s * K;
+    const long long n = geo.n[lev];
+    const int m = geo.m[lev];
+    const long long st = c * m, en = min(n, st + m);
+    const bool hasL = c > 0 || geo.segL;
+    const bool nC = needC != 0;
+    const long long base = static_cast<long long>(s) * n;
+    const double* rr = src.rec;
+    const long long SKp = src.SKp;
+    const long long SnU = static_cast<long long>(geo.S) * (geo.n[lev + 1] + geo.segL), iR = g + geo.segL * (s + 1);
+    // separators: x vectors every lane, C blocks by columns
+    double xn[B], xL[B], Cnn[B], CnL[B], CLL[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+        xn[i] = solU[(Sol<B>::X + i) * SnU + iR];
+        xL[i] = hasL ? solU[(Sol<B>::X + i) * SnU + iR - 1] : 0.0;
+        Cnn[i] = (nC && l < B) ? solU[(Sol<B>::CD + i * B + l) * SnU + iR] : 0.0;
+        CLL[i] = (nC && hasL && l < B) ? solU[(Sol<B>::CD + i * B + l) * SnU + iR - 1] : 0.0;
+        CnL[i] = (nC && hasL && l < B) ? solU[(Sol<B>::CU + l * B + i) * SnU + iR - 1] : 0.0;
+    }
+    auto put = [&](long long i, const double (&x)[B], const double (&Cc)[B]) {  // SolSink::put, column l
+        const long long k = static_cast<long long>(s) * (sink.n + sink.segL) + sink.segL + i;
+        if (l < B) {
+            sink.sol[(Sol<B>::X + l) * sink.Sn + k] = pick<B>(x, l);
+            if (nC)
+#pragma unroll
+                for (int q = 0; q < B; ++q) sink.sol[(Sol<B>::CD + q * B + l) * sink.Sn + k] = Cc[q];
+        }
+    };
+    auto put_upper = [&](long long i, const double (&Cu)[B]) {  // column l of C_{i,i+1}
+        const long long k = static_cast<long long>(s) * (sink.n + sink.segL) + sink.segL + i;
+        if (l < B)
+#pragma unroll
+            for (int q = 0; q < B; ++q) sink.sol[(Sol<B>::CU + q * B + l) * sink.Sn + k] = Cu[q];
+    };
+    put(en - 1, xn, Cnn);
+    if (c == 0 && geo.segL) put(-1, xL, CLL);
+    for (long long j = en - 2; j >= st; --j) {
+        const double* fp = fac + (g * m + (j - st)) * static_cast<long long>(NF);
+        double Y[B], X[B];
+        tsync(tm);
+        if (l < B) {
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                if (i >= l) LS[i * LD + l] = fp[i * (i + 1) / 2 + l];
+                Y[i] = hasL ? fp[NLI + i * B + l] : 0.0;
+                X[i] = rr[(Rec<B>::LR + i * B + l) * SKp + base + j + 1];  // column l of upper(j)
+            }
+            vS[l] = fp[NLI + B * B + l];
+        } else {
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                Y[i] = 0.0;
+                X[i] = 0.0;
+            }
+        }
+        tsync(tm);
+        tlsolve<B, LD>(X, LS);
+        colput<B, LD>(XS, X, l);
+        if (hasL) colput<B, LD>(YS, Y, l);
+        tsync(tm);
+        {  // x_j = L^{-T}(z - X x_n - Y x_L), component l per lane
+            double r[B];
+            if (l < B) {
+                double sx = 0.0, sy = 0.0;
+                rowget<B, LD>(r, XS, l);
+#pragma unroll
+                for (int k = 0; k < B; ++k) sx = fma(r[k], xn[k], sx);
+                double al = vS[l] - sx;
+                if (hasL) {
+                    rowget<B, LD>(r, YS, l);
+#pragma unroll
+                    for (int k = 0; k < B; ++k) sy = fma(r[k], xL[k], sy);
+                    al -= sy;
+                }
+                wS[l] = al;
+            }
+            tsync(tm);
+        }
+        double xj[B];
+#pragma unroll
+        for (int i = 0; i < B; ++i) xj[i] = wS[i];
+        tltsolve<B, LD>(xj, LS);
+        double Cjj[B], CjL[B], Cjn[B];
+        if (nC) {
+            double P[B], tmp[B], q[B];
+            tmv<B, LD>(P, XS, CnL);
+            if (hasL) {
+                tmv<B, LD>(tmp, YS, CLL);
+#pragma unroll
+                for (int i = 0; i < B; ++i) P[i] += tmp[i];
+            }
+            tmv<B, LD>(Cjn, XS, Cnn);
+            if (hasL) {
+                ttrans<B>(tm, q, CnL, vS + 2 * TeamCfg<B>::VEC);  // column l of C_{L,n}
+                tmv<B, LD>(tmp, YS, q);
+#pragma unroll
+                for (int i = 0; i < B; ++i) Cjn[i] += tmp[i];
+            }
+            (void)tmp;
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                CjL[i] = P[i];
+                Cjj[i] = Cjn[i];
+            }
+            tltsolve<B, LD>(CjL, LS);
+            tltsolve<B, LD>(Cjn, LS);
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                CjL[i] = -CjL[i];
+                Cjn[i] = -Cjn[i];
+            }
+            // M = I + P2 X^T + P1 Y^T with P2 = (pre-solve Cjn) in Cjj, P1 in P
+            double* S6 = vS + 2 * TeamCfg<B>::VEC;
+            double* S7 = S6 + TeamCfg<B>::MAT;
+            tsync(tm);
+            colput<B, LD>(S6, Cjj, l);
+            colput<B, LD>(S7, P, l);
+            tsync(tm);
+            double M[B], rw[B];
+            rowget<B, LD>(rw, XS, l);
+            tmv<B, LD>(M, S6, rw);
+            if (hasL) {
+                rowget<B, LD>(rw, YS, l);
+                tmv<B, LD>(tmp, S7, rw);
+#pragma unroll
+                for (int i = 0; i < B; ++i) M[i] += tmp[i];
+            }
+#pragma unroll
+            for (int i = 0; i < B; ++i)
+                if (i == l) M[i] += 1.0;
+            tsym<B>(tm, M, S6);
+            tltsolve<B, LD>(M, LS);
+            ttrans<B>(tm, Cjj, M, S7);
+            tltsolve<B, LD>(Cjj, LS);
+            tsym<B>(tm, Cjj, S6);
+        } else {
+#pragma unroll
+            for (int i = 0; i < B; ++i) {
+                Cjj[i] = 0.0;
+                CjL[i] = 0.0;
+                Cjn[i] = 0.0;
+            }
+        }
+        put(j, xj, Cjj);
+        if (nC) put_upper(j, Cjn);
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+            xn[i] = xj[i];
+            Cnn[i] = Cjj[i];
+            CnL[i] = CjL[i];
+        }
+    }
+    if (hasL && nC) {  // C_{st-1, st} = C_{st, L}^T: column l = row l of C_{st, L}
+        double q[B];
+        ttrans<B>(tm, q, CnL, vS + 2 * TeamCfg<B>::VEC);
+        put_upper(st - 1, q);
+    }
+}
+
 }  // namespace spingp_dev

@@ -5,3 +5,4 @@ using namespace spingp_dev;
 using spingp_host::EvalBufs;
 using spingp_host::EvalArgs;
 SPINGP_TEAM_INST(GenericTraits<12>)
+SPINGP_TEAM_UPPER_INST(12)

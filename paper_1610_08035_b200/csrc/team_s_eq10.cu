@@ -5,3 +5,4 @@ using namespace spingp_dev;
 using spingp_host::EvalBufs;
 using spingp_host::EvalArgs;
 SPINGP_TEAM_INST(StaticTraits<SEQ<10>>)
+SPINGP_TEAM_UPPER_INST(10)

@@ -73,3 +73,12 @@ def _has_gpu():
 def test_no_cpu_fallback_without_gpu():
     with pytest.raises(P.DeviceError):
         P.Context(0)
+
+
+def test_library_has_no_undefined_own_symbols():
+    """Every template the launch code references is instantiated in some translation unit
+    (a missing one only shows up when the library is loaded on the GPU box)."""
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--undefined-only", P.lib_path], capture_output=True, text=True, check=True).stdout
+    own = [ln for ln in out.splitlines() if "spingp" in ln]
+    assert not own, own[:5]
