@@ -418,3 +418,20 @@ def test_multi_theta_probes_equal_single_evaluations(ctx):
     for k in range(K):
         one = ctx.eval([P.MATERN52], theta[k], t, y, sig[k], grad=True)
         assert rel(ll[k], one["loglik"]) < 1e-12 and rel(g[k], one["grad"]) < 1e-10
+
+
+@pytest.mark.parametrize("leaves,theta", [([(P.EQ, 6)], [1.1, 1.4]), ([P.MATERN32, (P.QP, 6)], [1.0, 10.0, 1.0, 1.0, 1.0, 20.0])])
+def test_batched_team_path_equals_single_series(ctx, leaves, theta):
+    """b >= 6 batches: the team kernels (level 0 and upper levels) index several series."""
+    rng = np.random.default_rng(23)
+    S, n = 3, 2500
+    t = np.cumsum(rng.uniform(0.05, 0.15, (S, n)), axis=1)
+    y = rng.standard_normal((S, n))
+    th = np.tile(np.asarray(theta, float), (S, 1))
+    th[:, 1] *= np.array([1.0, 1.3, 0.8])
+    b = ctx.eval_batched(leaves, th, t, y, 0.3, grad=True, var=True)
+    for s in range(S):
+        one = ctx.eval(leaves, th[s], t[s], y[s], 0.3, grad=True, var=True)
+        assert rel(b["loglik"][s], one["loglik"]) < 1e-9
+        assert rel(b["grad"][s], one["grad"]) < 1e-6
+        assert rel(b["var"][s], one["var"]) < 1e-6
