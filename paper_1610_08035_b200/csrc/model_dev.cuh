@@ -533,14 +533,13 @@ SP_DEV void eq_grad_team(int o, int J, const double* ac, const double* lr, doubl
     const double ilen = lr[2], ivar = lr[3];
     gvar += 0.5 * s * ivar;
     if (dt < 0.0) return;
-    const double tau = dt * ilen;
+    // z = e^{Aτ} g: pair p -> e^{a τ} [cos(cτ), -sin(cτ)] = (Φ_kk, -Φ_{k,k+1}) of the
+    // rotation block eq_block_team wrote (same expressions: no second exp / sincos)
     double z0[kMaxB / 2], z1[kMaxB / 2];
     for (int p = 0; p < J / 2; ++p) {
-        const double rho = exp(ac[2 * p] * tau);
-        double sn, cs;
-        sincos(ac[2 * p + 1] * tau, &sn, &cs);
-        z0[p] = rho * cs;
-        z1[p] = -rho * sn;
+        const int k = o + 2 * p;
+        z0[p] = Phi[k * LD + k];
+        z1[p] = -Phi[k * LD + k + 1];
     }
     double tq = 0.0, tb = 0.0;
     const double cdt = -dt * ilen;

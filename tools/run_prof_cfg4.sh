@@ -12,7 +12,9 @@ with P.Context(0) as ctx:
 PY
 for cfg in cfg4 cfg5; do
   n=0; [ $cfg = cfg5 ] && n=2000000
-  ncu --set full --import-source on --clock-control none -k regex:"k_(rev0|fwd0)_team|k_(fwd|rev)L_team" -s 4 -c 4 -o /tmp/p_$cfg python /tmp/prof_team.py $cfg $n > gpurun_out/p_$cfg.log 2>&1
-  ncu -i /tmp/p_$cfg.ncu-rep --page details --csv > gpurun_out/r02b_ncu_${cfg}_details.csv 2>/dev/null
-  ncu -i /tmp/p_$cfg.ncu-rep --page raw --csv > gpurun_out/r02b_ncu_${cfg}_raw.csv 2>/dev/null
+  for k in k_rev0_team k_fwd0_team; do
+    ncu --set full --import-source on --clock-control none -k regex:"$k" -s 1 -c 1 -o /tmp/p_${cfg}_$k python /tmp/prof_team.py $cfg $n > gpurun_out/p_${cfg}_$k.log 2>&1
+    ncu -i /tmp/p_${cfg}_$k.ncu-rep --page details --csv > gpurun_out/r02b_ncu_${cfg}_${k}_details.csv 2>/dev/null
+    ncu -i /tmp/p_${cfg}_$k.ncu-rep --page raw --csv > gpurun_out/r02b_ncu_${cfg}_${k}_raw.csv 2>/dev/null
+  done
 done
