@@ -228,6 +228,7 @@ int spingp_ctx_destroy(spingp_ctx* ctx) {
     ctx->host_io.release();
     if (ctx->d_status) cudaFree(ctx->d_status);
     if (ctx->d_arrive) cudaFree(ctx->d_arrive);
+    if (ctx->d_ss_sync) cudaFree(ctx->d_ss_sync);
     for (int k = 0; k < 2; ++k) {
         if (ctx->h_stage[k]) cudaFreeHost(ctx->h_stage[k]);
         if (ctx->stage_ev[k]) cudaEventDestroy(ctx->stage_ev[k]);
@@ -660,6 +661,8 @@ static void cr_solve_locked(spingp_ctx* ctx, int64_t n, int32_t b, const double*
                             const double* d_rhs, int32_t k, double* d_x, double* d_logdet) {
     if (!d_diag || (n > 1 && !d_upper) || k < 0 || (k > 0 && (!d_rhs || !d_x)))
         throw std::invalid_argument("bad argument");
+    // b <= 4, at most one right-hand side: the tile-streaming kernel (stream_solve.cuh)
+    if (k <= 1 && stream_solve(ctx, n, b, d_diag, d_upper, k ? d_rhs : nullptr, k ? d_x : nullptr, d_logdet)) return;
     if (k == 0) {
         btd_dispatch(ctx, n, b, d_diag, d_upper, nullptr, 1, 0, nullptr, nullptr, nullptr, d_logdet, false);
         return;

@@ -138,6 +138,9 @@ struct spingp_ctx {
     // self-resetting per-series arrival counters of k_reduce (kept out of the arena so
     // their zero state survives between calls; grown on demand, zeroed when allocated)
     unsigned int* d_arrive = nullptr;
+    // grid barrier words of the tile-streaming solve (stream_solve.cu): monotonic counters
+    unsigned long long* d_ss_sync = nullptr;
+    unsigned long long ss_arrivals = 0, ss_releases = 0;
     unsigned long long* upper_stamps = nullptr;  // diagnostics (spingp_ctx_upper_stamps)
     long long arrive_cap = 0;
     unsigned int* counters(long long S) {
@@ -268,6 +271,8 @@ void eval_s_m32eq10(spingp_ctx* ctx, const EvalArgs& a);   // inst_s_m32eq10.cu
     void btd_run_##B(spingp_ctx* ctx, int64_t n, int b, const double* diag, const double* upper, \
                      const double* rhs, int k, int col, double* x, double* cdiag, double* cupper, \
                      double* logdet, bool needC);
+bool stream_solve(spingp_ctx* ctx, int64_t n, int b, const double* diag, const double* upper, const double* rhs,
+                  double* x, double* logdet);  // stream_solve.cu
 SPINGP_BTD_DECL(1)
 SPINGP_BTD_DECL(2)
 SPINGP_BTD_DECL(3)

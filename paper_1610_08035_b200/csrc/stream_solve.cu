@@ -1,0 +1,143 @@
+// stream_solve.cu — host side of the tile-streaming cr_solve (stream_solve.cuh): one
+// cooperative launch of G co-resident CTAs per solve.  Used by spingp_btd_cr_solve[_device]
+// for b <= 4 with at most one right-hand side; everything else keeps the partitioned
+// kernels of btd_ops.cuh.  SPINGP_SOLVE_STREAM=0 disables it (A/B knob).
+#include <cstdlib>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "ctx.hpp"
+#include "stream_solve.cuh"
+
+// b = 3 tile shape (threads = chunks per tile, blocks per chunk): two CTAs per SM
+#ifndef SP_SS3_NT
+#define SP_SS3_NT 96
+#endif
+#ifndef SP_SS3_M
+#define SP_SS3_M 5
+#endif
+
+namespace spingp_host {
+
+using namespace spingp_dev;
+
+namespace {
+
+// read on every call (cheap): tests and A/B runs toggle them inside one process
+bool stream_enabled() {
+    const char* e = std::getenv("SPINGP_SOLVE_STREAM");
+    return !(e && std::strcmp(e, "0") == 0);
+}
+int stream_l2mode() {
+    const char* e = std::getenv("SPINGP_SS_L2");
+    return e ? std::atoi(e) : 0;
+}
+
+// diagnostics (SPINGP_SS_STAMPS=1): per-phase %globaltimer of every CTA, summarised on stderr
+void ss_print_stamps(spingp_ctx* ctx, unsigned long long* d, int G) {
+    std::vector<unsigned long long> h(static_cast<size_t>(G) * 16);
+    CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    CUDA_OK(cudaMemcpy(h.data(), d, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaFree(d));
+    unsigned long long t0 = ~0ULL;
+    for (int g = 0; g < G; ++g) t0 = std::min(t0, h[g * 16]);
+    static const char* names[16] = {"start", "s1.t1 loaded", "s1.t1 eliminated", "s1.t1 tree", "s1.t1 chained",
+                                    "sweep1 end", "released", "end", "s2.t1 loaded", "s2.t1 eliminated",
+                                    "s2.t1 tree up", "s2.t1 tree down", "s2.t1 stored", "", "", ""};
+    for (int k = 0; k < 13; ++k) {
+        std::vector<double> v;
+        for (int g = 0; g < G; ++g)
+            if (h[g * 16 + k]) v.push_back((h[g * 16 + k] - t0) * 1e-3);
+        if (v.empty()) continue;
+        std::sort(v.begin(), v.end());
+        std::fprintf(stderr, "[ss] %-18s min %8.2f  med %8.2f  max %8.2f us  (cta0 %8.2f)\n", names[k], v.front(),
+                     v[v.size() / 2], v.back(), h[k] ? (h[k] - t0) * 1e-3 : -1.0);
+    }
+}
+
+template <int B, int NT, int M>
+bool ss_launch(spingp_ctx* ctx, int64_t n, const double* diag, const double* upper, const double* rhs, double* x,
+               double* logdet) {
+    using C = SSCfg<B, NT, M>;
+    constexpr int NR = C::NR, NF = C::NF;
+    const long long ntiles = (n + C::TB - 1) / C::TB;
+    if (ntiles < 2) return false;
+    auto kern = k_solve_stream<C, B>;
+    static unsigned long long attr = 0;
+    opt_in_smem(reinterpret_cast<const void*>(kern), attr, ctx->device, static_cast<int>(C::SMEM_BYTES));
+    static int resident_dev[64] = {};
+    int& resident = resident_dev[ctx->device & 63];
+    if (!resident) {
+        int per = 0, sms = 0;
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, NT, C::SMEM_BYTES));
+        CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+        resident = std::max(1, per) * sms;
+    }
+    // CTA 0 stages all G records ([NR][G rounded to even]) over its tile area
+    long long G = std::min<long long>(resident, ntiles);
+    const long long gcap = (C::TILE_DOUBLES / NR) & ~1LL;
+    G = std::min(G, gcap);
+    if (const char* e = std::getenv("SPINGP_SS_CTAS")) G = std::max<long long>(1, std::min<long long>(G, std::atoll(e)));
+    const int Tmax = static_cast<int>((ntiles + G - 1) / G);
+    ctx->ensure_ws(arena_bytes(NR * G) + arena_bytes(G * B) + arena_bytes(G * Tmax * NF) + 4096);
+    ctx->ws.reset();
+    SSArgs a{};
+    a.diag = diag;
+    a.up = upper;
+    a.rhs = rhs;
+    a.x = x;
+    a.logdet = logdet;
+    a.n = n;
+    a.ntiles = ntiles;
+    a.G = static_cast<int>(G);
+    a.Tmax = Tmax;
+    auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    a.bulk = (rhs && aligned(diag) && aligned(upper) && aligned(rhs)) ? 1 : 0;
+    a.l2mode = stream_l2mode();
+    a.crec = ctx->ws.take<double>(NR * G);
+    a.xsep = ctx->ws.take<double>(G * B);
+    a.cfac = ctx->ws.take<double>(G * Tmax * NF);
+    if (!ctx->d_ss_sync) {
+        CUDA_OK(cudaMalloc(&ctx->d_ss_sync, 2 * sizeof(unsigned long long)));
+        CUDA_OK(cudaMemsetAsync(ctx->d_ss_sync, 0, 2 * sizeof(unsigned long long), ctx->stream));
+        ctx->ss_arrivals = ctx->ss_releases = 0;
+    }
+    a.sync = ctx->d_ss_sync;
+    a.arrive_target = ctx->ss_arrivals + static_cast<unsigned long long>(G);
+    a.release_target = ctx->ss_releases + 1;
+    a.status = ctx->d_status;
+    const bool stamps = std::getenv("SPINGP_SS_STAMPS") != nullptr;
+    a.stamps = nullptr;
+    if (stamps) {
+        CUDA_OK(cudaMalloc(&a.stamps, G * 16 * sizeof(unsigned long long)));
+        CUDA_OK(cudaMemsetAsync(a.stamps, 0, G * 16 * sizeof(unsigned long long), ctx->stream));
+    }
+    void* args[] = {&a};
+    ctx->pre();
+    CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(static_cast<unsigned>(G)), dim3(NT), args,
+                                        C::SMEM_BYTES, ctx->stream));
+    ctx->launched("k_solve_stream");
+    ctx->ss_arrivals = a.arrive_target;
+    if (x) ctx->ss_releases = a.release_target;
+    if (stamps) ss_print_stamps(ctx, a.stamps, static_cast<int>(G));
+    return true;
+}
+
+}  // namespace
+
+// x = M^{-1} rhs (one right-hand side, or none: log det only) by the tile-streaming kernel;
+// false when the case is not covered (b > 4, too few blocks, disabled).
+bool stream_solve(spingp_ctx* ctx, int64_t n, int b, const double* diag, const double* upper, const double* rhs,
+                  double* x, double* logdet) {
+    if (!stream_enabled() || n < 2 || !upper) return false;
+    switch (b) {
+        case 1: return ss_launch<1, 128, 7>(ctx, n, diag, upper, rhs, x, logdet);
+        case 2: return ss_launch<2, 128, 5>(ctx, n, diag, upper, rhs, x, logdet);
+        case 3: return ss_launch<3, SP_SS3_NT, SP_SS3_M>(ctx, n, diag, upper, rhs, x, logdet);
+        case 4: return ss_launch<4, 64, 3>(ctx, n, diag, upper, rhs, x, logdet);
+        default: return false;
+    }
+}
+
+}  // namespace spingp_host

@@ -143,11 +143,54 @@ struct TreeFwdScratch {
     bool active, merged, ok;
 };
 
+// Merge of two adjacent records held in registers: A = (L, M), Bv = (M, R) -> C = (L, R)
+// and the merge factor F = (L_S, Y_L, Y_R, z) of the eliminated separator M.
+template <int B>
+SP_DEV bool tree_merge(const double* A, const double* Bv, double* C, double* F) {
+    using TR = Tree<B>;
+    using RC = Rec<B>;
+    double S[B * B], r[B], T1[B * B], v[B];
+    double* Ls = F + TR::FL;
+    double* YL = F + TR::FYL;
+    double* YR = F + TR::FYR;
+    double* z = F + TR::FZ;
+TR_UNROLL
+    for (int i = 0; i < B * B; ++i) S[i] = A[RC::RDIAG + i] + Bv[RC::LDIAG + i];
+    msym<B>(S);
+TR_UNROLL
+    for (int i = 0; i < B; ++i) r[i] = A[RC::RRHS + i] + Bv[RC::LRHS + i];
+    double ld;
+    const bool ok = chol<B>(Ls, S, ld);
+    lsolve_v<B>(z, Ls, r);
+TR_UNROLL
+    for (int i = 0; i < B; ++i)
+TR_UNROLL
+        for (int j = 0; j < B; ++j) T1[i * B + j] = A[RC::LR + j * B + i];  // P_{M,L} = A.LR^T
+    lsolve<B>(YL, Ls, T1);
+    lsolve<B>(YR, Ls, Bv + RC::LR);  // P_{M,R} = B.LR
+    mtm_sym<B>(T1, YL, YL);
+TR_UNROLL
+    for (int i = 0; i < B * B; ++i) C[RC::LDIAG + i] = A[RC::LDIAG + i] - T1[i];
+    mtm<B>(T1, YL, YR);
+TR_UNROLL
+    for (int i = 0; i < B * B; ++i) C[RC::LR + i] = -T1[i];
+    mtm_sym<B>(T1, YR, YR);
+TR_UNROLL
+    for (int i = 0; i < B * B; ++i) C[RC::RDIAG + i] = Bv[RC::RDIAG + i] - T1[i];
+    mtv<B>(v, YL, z);
+TR_UNROLL
+    for (int i = 0; i < B; ++i) C[RC::LRHS + i] = A[RC::LRHS + i] - v[i];
+    mtv<B>(v, YR, z);
+TR_UNROLL
+    for (int i = 0; i < B; ++i) C[RC::RRHS + i] = Bv[RC::RRHS + i] - v[i];
+    C[RC::LOGDET] = A[RC::LOGDET] + Bv[RC::LOGDET] + ld;
+    return ok;
+}
+
 // round j -> j+1, compute part: node k (< n_{j+1}) merges slots 2k and 2k+1 of level j
 template <int B>
 SP_DEV void tree_fwd_compute(const double* R, int RS, int n, int k, TreeFwdScratch<B>& sc) {
     using TR = Tree<B>;
-    using RC = Rec<B>;
     const int nn = (n + 1) >> 1;
     sc.active = k < nn;
     sc.merged = sc.active && 2 * k + 1 < n;
@@ -170,41 +213,7 @@ TR_UNROLL
         Bv[c] = v.y;
 #endif
     }
-    double S[B * B], r[B], T1[B * B], v[B];
-    double* Ls = sc.F + TR::FL;
-    double* YL = sc.F + TR::FYL;
-    double* YR = sc.F + TR::FYR;
-    double* z = sc.F + TR::FZ;
-TR_UNROLL
-    for (int i = 0; i < B * B; ++i) S[i] = A[RC::RDIAG + i] + Bv[RC::LDIAG + i];
-    msym<B>(S);
-TR_UNROLL
-    for (int i = 0; i < B; ++i) r[i] = A[RC::RRHS + i] + Bv[RC::LRHS + i];
-    double ld;
-    sc.ok = chol<B>(Ls, S, ld);
-    lsolve_v<B>(z, Ls, r);
-TR_UNROLL
-    for (int i = 0; i < B; ++i)
-TR_UNROLL
-        for (int j = 0; j < B; ++j) T1[i * B + j] = A[RC::LR + j * B + i];  // P_{M,L} = A.LR^T
-    lsolve<B>(YL, Ls, T1);
-    lsolve<B>(YR, Ls, Bv + RC::LR);  // P_{M,R} = B.LR
-    mtm_sym<B>(T1, YL, YL);
-TR_UNROLL
-    for (int i = 0; i < B * B; ++i) sc.C[RC::LDIAG + i] = A[RC::LDIAG + i] - T1[i];
-    mtm<B>(T1, YL, YR);
-TR_UNROLL
-    for (int i = 0; i < B * B; ++i) sc.C[RC::LR + i] = -T1[i];
-    mtm_sym<B>(T1, YR, YR);
-TR_UNROLL
-    for (int i = 0; i < B * B; ++i) sc.C[RC::RDIAG + i] = Bv[RC::RDIAG + i] - T1[i];
-    mtv<B>(v, YL, z);
-TR_UNROLL
-    for (int i = 0; i < B; ++i) sc.C[RC::LRHS + i] = A[RC::LRHS + i] - v[i];
-    mtv<B>(v, YR, z);
-TR_UNROLL
-    for (int i = 0; i < B; ++i) sc.C[RC::RRHS + i] = Bv[RC::RRHS + i] - v[i];
-    sc.C[RC::LOGDET] = A[RC::LOGDET] + Bv[RC::LOGDET] + ld;
+    sc.ok = tree_merge<B>(A, Bv, sc.C, sc.F);
 }
 // store part (after the barrier): record -> slot k, factor -> slot n_{j+1} + k
 template <int B>
