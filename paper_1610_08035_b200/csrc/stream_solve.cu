@@ -10,9 +10,9 @@
 #include "ctx.hpp"
 #include "stream_solve.cuh"
 
-// b = 3 tile shape (threads = chunks per tile, blocks per chunk): two CTAs per SM
-#ifndef SP_SS3_NT
-#define SP_SS3_NT 96
+// b = 3 shape: warps per CTA (one CTA per SM), blocks per lane
+#ifndef SP_SS3_NW
+#define SP_SS3_NW 8
 #endif
 #ifndef SP_SS3_M
 #define SP_SS3_M 5
@@ -42,10 +42,9 @@ void ss_print_stamps(spingp_ctx* ctx, unsigned long long* d, int G) {
     CUDA_OK(cudaFree(d));
     unsigned long long t0 = ~0ULL;
     for (int g = 0; g < G; ++g) t0 = std::min(t0, h[g * 16]);
-    static const char* names[16] = {"start", "s1.t1 loaded", "s1.t1 eliminated", "s1.t1 tree", "s1.t1 chained",
-                                    "sweep1 end", "released", "end", "s2.t1 loaded", "s2.t1 eliminated",
-                                    "s2.t1 tree up", "s2.t1 tree down", "s2.t1 stored", "", "", ""};
-    for (int k = 0; k < 13; ++k) {
+    static const char* names[16] = {"start", "sweep 1 (warp 0)", "CTA record out", "top: all arrived", "top: released",
+                                    "release seen", "end (warp 0)", "", "", "", "", "", "", "", "", ""};
+    for (int k = 0; k < 7; ++k) {
         std::vector<double> v;
         for (int g = 0; g < G; ++g)
             if (h[g * 16 + k]) v.push_back((h[g * 16 + k] - t0) * 1e-3);
@@ -56,13 +55,13 @@ void ss_print_stamps(spingp_ctx* ctx, unsigned long long* d, int G) {
     }
 }
 
-template <int B, int NT, int M>
+template <int B, int NW, int M>
 bool ss_launch(spingp_ctx* ctx, int64_t n, const double* diag, const double* upper, const double* rhs, double* x,
                double* logdet) {
-    using C = SSCfg<B, NT, M>;
-    constexpr int NR = C::NR, NF = C::NF;
-    const long long ntiles = (n + C::TB - 1) / C::TB;
-    if (ntiles < 2) return false;
+    using C = SSCfg<B, NW, M>;
+    constexpr int NR = C::NR, NK = C::NK;
+    const long long ntiles = (n + C::WT - 1) / C::WT;
+    if (ntiles < NW) return false;  // every warp of a CTA needs a tile
     auto kern = k_solve_stream<C, B>;
     static unsigned long long attr = 0;
     opt_in_smem(reinterpret_cast<const void*>(kern), attr, ctx->device, static_cast<int>(C::SMEM_BYTES));
@@ -70,17 +69,18 @@ bool ss_launch(spingp_ctx* ctx, int64_t n, const double* diag, const double* upp
     int& resident = resident_dev[ctx->device & 63];
     if (!resident) {
         int per = 0, sms = 0;
-        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, NT, C::SMEM_BYTES));
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, C::NT, C::SMEM_BYTES));
         CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
         resident = std::max(1, per) * sms;
     }
-    // CTA 0 stages all G records ([NR][G rounded to even]) over its tile area
-    long long G = std::min<long long>(resident, ntiles);
-    const long long gcap = (C::TILE_DOUBLES / NR) & ~1LL;
+    long long G = std::min<long long>(resident, ntiles / NW);
+    // CTA 0 stages all G records ([NR][G rounded to even]) next to the top tree, over its tile buffers
+    const long long gcap = ((C::OFF_WR - C::TOP_FIXED) / NR) & ~1LL;
     G = std::min(G, gcap);
     if (const char* e = std::getenv("SPINGP_SS_CTAS")) G = std::max<long long>(1, std::min<long long>(G, std::atoll(e)));
-    const int Tmax = static_cast<int>((ntiles + G - 1) / G);
-    ctx->ensure_ws(arena_bytes(NR * G) + arena_bytes(G * B) + arena_bytes(G * Tmax * NF) + 4096);
+    const long long GW = G * NW;
+    const int Tmax = static_cast<int>((ntiles + GW - 1) / GW);
+    ctx->ensure_ws(arena_bytes(NR * G) + arena_bytes(G * B) + arena_bytes(GW * Tmax * NK) + 4096);
     ctx->ws.reset();
     SSArgs a{};
     a.diag = diag;
@@ -97,7 +97,7 @@ bool ss_launch(spingp_ctx* ctx, int64_t n, const double* diag, const double* upp
     a.l2mode = stream_l2mode();
     a.crec = ctx->ws.take<double>(NR * G);
     a.xsep = ctx->ws.take<double>(G * B);
-    a.cfac = ctx->ws.take<double>(G * Tmax * NF);
+    a.ckpt = ctx->ws.take<double>(GW * Tmax * NK);
     if (!ctx->d_ss_sync) {
         CUDA_OK(cudaMalloc(&ctx->d_ss_sync, 2 * sizeof(unsigned long long)));
         CUDA_OK(cudaMemsetAsync(ctx->d_ss_sync, 0, 2 * sizeof(unsigned long long), ctx->stream));
@@ -115,8 +115,8 @@ bool ss_launch(spingp_ctx* ctx, int64_t n, const double* diag, const double* upp
     }
     void* args[] = {&a};
     ctx->pre();
-    CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(static_cast<unsigned>(G)), dim3(NT), args,
-                                        C::SMEM_BYTES, ctx->stream));
+    CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(static_cast<unsigned>(G)), dim3(C::NT),
+                                        args, C::SMEM_BYTES, ctx->stream));
     ctx->launched("k_solve_stream");
     ctx->ss_arrivals = a.arrive_target;
     if (x) ctx->ss_releases = a.release_target;
@@ -132,10 +132,10 @@ bool stream_solve(spingp_ctx* ctx, int64_t n, int b, const double* diag, const d
                   double* x, double* logdet) {
     if (!stream_enabled() || n < 2 || !upper) return false;
     switch (b) {
-        case 1: return ss_launch<1, 128, 7>(ctx, n, diag, upper, rhs, x, logdet);
-        case 2: return ss_launch<2, 128, 5>(ctx, n, diag, upper, rhs, x, logdet);
-        case 3: return ss_launch<3, SP_SS3_NT, SP_SS3_M>(ctx, n, diag, upper, rhs, x, logdet);
-        case 4: return ss_launch<4, 64, 3>(ctx, n, diag, upper, rhs, x, logdet);
+        case 1: return ss_launch<1, 8, 7>(ctx, n, diag, upper, rhs, x, logdet);
+        case 2: return ss_launch<2, 8, 5>(ctx, n, diag, upper, rhs, x, logdet);
+        case 3: return ss_launch<3, SP_SS3_NW, SP_SS3_M>(ctx, n, diag, upper, rhs, x, logdet);
+        case 4: return ss_launch<4, 8, 3>(ctx, n, diag, upper, rhs, x, logdet);
         default: return false;
     }
 }

@@ -16,7 +16,8 @@ def system(n, b, dev, seed=7, off=0):
     g = torch.Generator(device=dev).manual_seed(seed)
     A = torch.randn(n, b, b, device=dev, dtype=torch.float64, generator=g)
     diag = A @ A.transpose(1, 2) + 4 * b * torch.eye(b, device=dev, dtype=torch.float64)
-    upper = torch.randn(max(n - 1, 1), b, b, device=dev, dtype=torch.float64, generator=g)
+    # off-diagonal blocks scaled so that the matrix stays positive definite at b = 1
+    upper = torch.randn(max(n - 1, 1), b, b, device=dev, dtype=torch.float64, generator=g) * (0.5 if b == 1 else 1.0)
     rhs = torch.randn(n * b, device=dev, dtype=torch.float64, generator=g)
 
     def place(v):  # optionally 8 bytes off a 16-byte boundary
@@ -54,7 +55,7 @@ def main():
     ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
     quick = len(sys.argv) > 1 and sys.argv[1] == "quick"
     worst = 0.0
-    sizes = [961, 962, 1500, 4801, 20000, 100003] + ([] if quick else [1_000_000, 3_000_001])
+    sizes = [1281, 1282, 1500, 1793, 4801, 20000, 100003] + ([] if quick else [1_000_000, 3_000_001])
     for b in (3, 1, 2, 4):
         for n in sizes:
             for off in (0, 1):
