@@ -17,6 +17,9 @@
 #ifndef SP_SS3_M
 #define SP_SS3_M 5
 #endif
+#ifndef SP_SS3_LPT
+#define SP_SS3_LPT 32
+#endif
 
 namespace spingp_host {
 
@@ -55,11 +58,11 @@ void ss_print_stamps(spingp_ctx* ctx, unsigned long long* d, int G) {
     }
 }
 
-template <int B, int NW, int M>
+template <int B, int NWARP, int M, int LPT>
 bool ss_launch(spingp_ctx* ctx, int64_t n, const double* diag, const double* upper, const double* rhs, double* x,
                double* logdet) {
-    using C = SSCfg<B, NW, M>;
-    constexpr int NR = C::NR, NK = C::NK;
+    using C = SSCfg<B, NWARP, M, LPT>;
+    constexpr int NR = C::NR, NK = C::NK, NF = C::NF, NW = C::NW;
     const long long ntiles = (n + C::WT - 1) / C::WT;
     if (ntiles < NW) return false;  // every warp of a CTA needs a tile
     auto kern = k_solve_stream<C, B>;
@@ -74,13 +77,12 @@ bool ss_launch(spingp_ctx* ctx, int64_t n, const double* diag, const double* upp
         resident = std::max(1, per) * sms;
     }
     long long G = std::min<long long>(resident, ntiles / NW);
-    // CTA 0 stages all G records ([NR][G rounded to even]) next to the top tree, over its tile buffers
-    const long long gcap = ((C::OFF_WR - C::TOP_FIXED) / NR) & ~1LL;
-    G = std::min(G, gcap);
+    G = std::min<long long>(G, C::NT);  // the top system: one CTA record per thread of CTA 0
     if (const char* e = std::getenv("SPINGP_SS_CTAS")) G = std::max<long long>(1, std::min<long long>(G, std::atoll(e)));
     const long long GW = G * NW;
     const int Tmax = static_cast<int>((ntiles + GW - 1) / GW);
-    ctx->ensure_ws(arena_bytes(NR * G) + arena_bytes(G * B) + arena_bytes(GW * Tmax * NK) + 4096);
+    ctx->ensure_ws(arena_bytes(NR * G) + arena_bytes(G * B) + arena_bytes(GW * Tmax * NK) +
+                   arena_bytes(GW * Tmax * NF * LPT) + 4096);
     ctx->ws.reset();
     SSArgs a{};
     a.diag = diag;
@@ -98,6 +100,7 @@ bool ss_launch(spingp_ctx* ctx, int64_t n, const double* diag, const double* upp
     a.crec = ctx->ws.take<double>(NR * G);
     a.xsep = ctx->ws.take<double>(G * B);
     a.ckpt = ctx->ws.take<double>(GW * Tmax * NK);
+    a.tfac = ctx->ws.take<double>(GW * Tmax * NF * LPT);
     if (!ctx->d_ss_sync) {
         CUDA_OK(cudaMalloc(&ctx->d_ss_sync, 2 * sizeof(unsigned long long)));
         CUDA_OK(cudaMemsetAsync(ctx->d_ss_sync, 0, 2 * sizeof(unsigned long long), ctx->stream));
@@ -132,10 +135,10 @@ bool stream_solve(spingp_ctx* ctx, int64_t n, int b, const double* diag, const d
                   double* x, double* logdet) {
     if (!stream_enabled() || n < 2 || !upper) return false;
     switch (b) {
-        case 1: return ss_launch<1, 8, 7>(ctx, n, diag, upper, rhs, x, logdet);
-        case 2: return ss_launch<2, 8, 5>(ctx, n, diag, upper, rhs, x, logdet);
-        case 3: return ss_launch<3, SP_SS3_NW, SP_SS3_M>(ctx, n, diag, upper, rhs, x, logdet);
-        case 4: return ss_launch<4, 8, 3>(ctx, n, diag, upper, rhs, x, logdet);
+        case 1: return ss_launch<1, 8, 7, 32>(ctx, n, diag, upper, rhs, x, logdet);
+        case 2: return ss_launch<2, 8, 5, 32>(ctx, n, diag, upper, rhs, x, logdet);
+        case 3: return ss_launch<3, SP_SS3_NW, SP_SS3_M, SP_SS3_LPT>(ctx, n, diag, upper, rhs, x, logdet);
+        case 4: return ss_launch<4, 8, 3, 32>(ctx, n, diag, upper, rhs, x, logdet);
         default: return false;
     }
 }

@@ -31,12 +31,17 @@
 //              memory (tree.cuh) and the CTA record is published.
 //   top        one grid-wide barrier; CTA 0 solves the G-record reduced system in shared
 //              memory and publishes the solution at every CTA boundary and log det.
-//   sweep 2    every warp walks its tiles in DESCENDING order: reload and re-eliminate
-//              from the checkpoint (the last tile of sweep 1 is still in shared memory
-//              and registers and is not re-read), un-merge the warp tree, back-substitute
-//              x_j = h_j - G_j x_{j+1} - V_j x_L per lane, store x coalesced.
+//   sweep 2    every group walks its tiles in DESCENDING order: un-merge the tile's tree from
+//              the merge factors sweep 1 stored (30 doubles per lane and tile), which gives
+//              every lane the solution at both ends of its chunk; reload the tile (the last
+//              tile of sweep 1 is still in shared memory and is not re-read) and solve each
+//              chunk as a Dirichlet problem: plain block Thomas, no spike, no tree.
 //
-// HBM traffic: sweep 1 reads every block once; sweep 2 re-reads what L2 lost and writes x.
+// HBM traffic: sweep 1 reads every block once and writes the tree factors (48 B per block
+// at b = 3, M = 5, mostly L2-resident until sweep 2 reads them back in reverse order);
+// sweep 2 re-reads what L2 lost and writes x.
+// A "group" is LPT = 32, 16 or 8 lanes of a warp with their own tile buffer and run: fewer
+// lanes per tile means a shallower tree for the same blocks per lane.
 #pragma once
 
 #include "tree.cuh"
@@ -45,12 +50,13 @@ namespace spingp_dev {
 
 constexpr int ss_even(int v) { return (v + 1) & ~1; }
 
-template <int B, int NW_, int M_>
+template <int B, int NW_, int M_, int LPT_ = 32>
 struct SSCfg {
-    static constexpr int NW = NW_;            // warps per CTA (independent pipelines)
+    static constexpr int LPT = LPT_;          // lanes per tile (a group of lanes of one warp)
+    static constexpr int NW = NW_ * (32 / LPT_);  // groups per CTA (independent pipelines)
     static constexpr int NT = 32 * NW_;
     static constexpr int M = M_;              // blocks per lane (M - 1 interior + 1 separator)
-    static constexpr int WT = 32 * M_;        // blocks per warp tile
+    static constexpr int WT = LPT_ * M_;      // blocks per tile
     static constexpr int BB = B * B;
     static constexpr int NR = Rec<B>::N;      // record components
     static constexpr int NF = Tree<B>::NF;    // merge factor components
@@ -64,18 +70,19 @@ struct SSCfg {
     static constexpr int W_BAR = ss_even(W_UH + BB);
     static constexpr int W_SIZE = W_BAR + 2;
     // CTA level: warp records, their separators
-    static constexpr int RSW = ss_even(NW_);
-    static constexpr int ESW = ss_even(NW_ + 1);
-    static constexpr int OFF_WR = NW_ * W_SIZE;
+    static constexpr int RSW = ss_even(NW);
+    static constexpr int ESW = ss_even(NW + 1);
+    static constexpr int OFF_WR = NW * W_SIZE;
     static constexpr int OFF_WE = OFF_WR + NR * RSW;
     static constexpr int SMEM_DOUBLES = ss_even(OFF_WE + B * ESW);
     static constexpr size_t SMEM_BYTES = static_cast<size_t>(SMEM_DOUBLES) * 8;
-    // top system (CTA 0, over its tile buffers): records [NR][GS], tree [NR][RS], separators [B][ES]
-    static constexpr int RS = ss_even(NT);
-    static constexpr int ES = ss_even(NT + 1);
-    static constexpr int TOP_FIXED = NR * RS + B * ES;   // + NR * GS must fit OFF_WR doubles
+    // top system (CTA 0, over its tile buffers): one record per thread, the NT / 32 warp
+    // records [NR][RST] and their separators [B][EST]
+    static constexpr int RST = ss_even(NT / 32);
+    static constexpr int EST = ss_even(NT / 32 + 1);
     static_assert(WT % 2 == 0, "tile pieces must be multiples of 16 bytes");
-    static_assert(TOP_FIXED + 2 * NR < OFF_WR, "top system does not fit");
+    static_assert(NR * RST + B * EST < OFF_WR, "top system does not fit");
+    static_assert((M_ & 1) == 1 || B % 2 == 0, "odd M keeps the lane strips off the same banks");
 };
 
 struct SSArgs {
@@ -93,6 +100,7 @@ struct SSArgs {
     double* crec;     // [NR][G] CTA records, component-major
     double* xsep;     // [G][B] solution at every CTA's last block
     double* ckpt;     // [G * NW][Tmax][NK] carry checkpoints (S_P, W_P, r_P) per tile
+    double* tfac;     // [G * NW][Tmax][NF][LPT] merge factors of every tile's tree
     unsigned long long* sync;  // [0] arrivals (monotonic), [1] release word (monotonic)
     unsigned long long arrive_target, release_target;
     unsigned long long* status;
@@ -160,19 +168,16 @@ SP_DEV void ss_st_release(unsigned long long* p, unsigned long long v) {
 }
 constexpr unsigned kFullWarp = 0xffffffffu;
 
-// ---- one lane's chunk: forward elimination (in place when KEEP) ----------------
+// ---- one lane's chunk: forward elimination against the left spike ----------------
 template <int B>
 struct SSElim {
     double T[B * B], rc[B], W[B * B], accLL[B * B], accrL[B];
     LogDetAcc piv;
     bool ok;
 };
-// One interior block with diagonal D, coupling U (to the next block) and rhs r; with KEEP
-// V = S^{-1}W -> Vo, G = S^{-1}U -> Go, h = S^{-1}r -> ho (they may be D, U, r's own
-// storage: everything is read before anything is written).
-template <int B, bool KEEP>
-SP_DEV void ss_elim_step(SSElim<B>& es, const double* Dp, const double* Up, const double* rp, double* Vo, double* Go,
-                         double* ho) {
+// One interior block with diagonal D, coupling U (to the next block) and rhs r.
+template <int B>
+SP_DEV void ss_elim_step(SSElim<B>& es, const double* Dp, const double* Up, const double* rp) {
     constexpr int BB = B * B;
     double S[BB], L[BB], U[BB], r[B], z[B], X[BB], Y[BB], Gm[BB];
 TR_UNROLL
@@ -198,27 +203,15 @@ TR_UNROLL
     for (int i = 0; i < BB; ++i) es.W[i] = -Gm[i];
     mtm_sym<B>(es.T, X, X);
     mtv<B>(es.rc, X, z);
-    if (KEEP) {
-        double h[B];
-        ltsolve<B>(Gm, L, X);
-TR_UNROLL
-        for (int i = 0; i < BB; ++i) Go[i] = Gm[i];
-        ltsolve<B>(Gm, L, Y);
-TR_UNROLL
-        for (int i = 0; i < BB; ++i) Vo[i] = Gm[i];
-        ltsolve_v<B>(h, L, z);
-TR_UNROLL
-        for (int i = 0; i < B; ++i) ho[i] = h[i];
-    }
 }
 
-// Lane chunk lo .. lo+M-1 of the warp tile at (sD, sU, sR).  Uprev = the upper block that
-// couples block lo-1 to lo.  carry (lane 0, tiles after the warp's first): the checkpoint
-// (S_P, W_P = P_{P,Z}, r_P) of the carried block P, eliminated first (kept factor -> sP),
-// with the run's accumulated left-separator terms and log det in rec (LDIAG, LRHS, LOGDET).
-template <class C, int B, bool KEEP>
-SP_DEV bool ss_eliminate(double* sD, double* sU, double* sR, const double* Uprev, int lo, const double* carry,
-                         double* sP, double* rec) {
+// Lane chunk lo .. lo+M-1 of the tile at (sD, sU, sR), read only.  Uprev = the upper block
+// that couples block lo-1 to lo.  carry (group leader, tiles after the run's first): the
+// checkpoint (S_P, W_P = P_{P,Z}, r_P) of the carried block P, eliminated first, with the
+// run's accumulated left-separator terms and log det in rec (LDIAG, LRHS, LOGDET).
+template <class C, int B>
+SP_DEV bool ss_eliminate(const double* sD, const double* sU, const double* sR, const double* Uprev, int lo,
+                         const double* carry, double* rec) {
     constexpr int BB = B * B;
     constexpr int M = C::M;
     using RC = Rec<B>;
@@ -236,7 +229,7 @@ TR_UNROLL
 TR_UNROLL
         for (int i = 0; i < B; ++i) es.accrL[i] = rec[RC::LRHS + i];
         ld0 = rec[RC::LOGDET];
-        ss_elim_step<B, KEEP>(es, carry, Uprev, carry + 2 * BB, sP, sP + BB, sP + 2 * BB);
+        ss_elim_step<B>(es, carry, Uprev, carry + 2 * BB);
     } else {
 TR_UNROLL
         for (int i = 0; i < B; ++i)
@@ -246,12 +239,8 @@ TR_UNROLL
         vzero<B>(es.accrL);
     }
 #pragma unroll 1
-    for (int j = 0; j < M - 1; ++j) {
-        double* Dp = sD + (lo + j) * BB;
-        double* Up = sU + (lo + j) * BB;
-        double* rp = sR + (lo + j) * B;
-        ss_elim_step<B, KEEP>(es, Dp, Up, rp, Dp, Up, rp);
-    }
+    for (int j = 0; j < M - 1; ++j)
+        ss_elim_step<B>(es, sD + (lo + j) * BB, sU + (lo + j) * BB, sR + (lo + j) * B);
     const double* Dp = sD + (lo + M - 1) * BB;
     const double* rp = sR + (lo + M - 1) * B;
 TR_UNROLL
@@ -270,6 +259,93 @@ TR_UNROLL
     return es.ok;
 }
 
+// ---- one lane's chunk as a Dirichlet problem (sweep 2) ----------------------------
+// Both ends known (xl at the chunk's left separator, xr at its own last block): plain
+// block Thomas over the M - 1 interior blocks, L -> diag slot, X = L^{-1}U -> upper slot,
+// z -> rhs slot, then x_j = L^{-T}(z_j - X_j x_{j+1}) written over the rhs slots.
+// Leader with a carried block P: P is eliminated first from its checkpoint, and x_P (the
+// solution at the previous tile's last block) is returned in xP.
+template <class C, int B>
+SP_DEV void ss_dirichlet(double* sD, double* sU, double* sR, const double* Uprev, int lo, const double* carry,
+                         const double* xl, const double* xr, double* xP) {
+    constexpr int BB = B * B;
+    constexpr int M = C::M;
+    double T[BB], rc[B], Lp[BB], Xp[BB], zp[B];
+    if (carry) {  // S_P, W_P (coupling to the run's left separator Z, x_Z = xl), r_P
+        double S[BB], r[B], t1[B];
+TR_UNROLL
+        for (int i = 0; i < BB; ++i) S[i] = carry[i];
+        mv<B>(t1, carry + BB, xl);
+TR_UNROLL
+        for (int i = 0; i < B; ++i) r[i] = carry[2 * BB + i] - t1[i];
+        msym<B>(S);
+        chol_nolog<B>(Lp, S);
+        lsolve_v<B>(zp, Lp, r);
+        lsolve<B>(Xp, Lp, Uprev);
+        mtm_sym<B>(T, Xp, Xp);
+        mtv<B>(rc, Xp, zp);
+    } else {  // the left separator's x moves to the first block's right-hand side
+        mzero<B>(T);
+        mtv<B>(rc, Uprev, xl);  // P_{lo,lo-1} x_{lo-1} = Uprev^T xl
+    }
+#pragma unroll 1
+    for (int j = 0; j < M - 1; ++j) {
+        double* Dp = sD + (lo + j) * BB;
+        double* Up = sU + (lo + j) * BB;
+        double* rp = sR + (lo + j) * B;
+        double S[BB], L[BB], U[BB], r[B], z[B], X[BB];
+TR_UNROLL
+        for (int i = 0; i < BB; ++i) S[i] = Dp[i] - T[i];
+TR_UNROLL
+        for (int i = 0; i < BB; ++i) U[i] = Up[i];
+TR_UNROLL
+        for (int i = 0; i < B; ++i) r[i] = rp[i] - rc[i];
+        msym<B>(S);
+        chol_nolog<B>(L, S);
+        lsolve_v<B>(z, L, r);
+        lsolve<B>(X, L, U);
+        mtm_sym<B>(T, X, X);
+        mtv<B>(rc, X, z);
+TR_UNROLL
+        for (int i = 0; i < BB; ++i) Dp[i] = L[i];
+TR_UNROLL
+        for (int i = 0; i < BB; ++i) Up[i] = X[i];
+TR_UNROLL
+        for (int i = 0; i < B; ++i) rp[i] = z[i];
+    }
+    double xn[B];
+TR_UNROLL
+    for (int i = 0; i < B; ++i) {
+        xn[i] = xr[i];
+        sR[(lo + M - 1) * B + i] = xr[i];
+    }
+#pragma unroll 1
+    for (int j = M - 2; j >= 0; --j) {
+        const double* Lq = sD + (lo + j) * BB;
+        const double* Xq = sU + (lo + j) * BB;
+        double* zq = sR + (lo + j) * B;
+        double L[BB], a[B], t1[B], xj[B];
+TR_UNROLL
+        for (int i = 0; i < BB; ++i) L[i] = Lq[i];
+        mv<B>(t1, Xq, xn);
+TR_UNROLL
+        for (int i = 0; i < B; ++i) a[i] = zq[i] - t1[i];
+        ltsolve_v<B>(xj, L, a);
+TR_UNROLL
+        for (int i = 0; i < B; ++i) {
+            zq[i] = xj[i];
+            xn[i] = xj[i];
+        }
+    }
+    if (carry) {
+        double a[B], t1[B];
+        mv<B>(t1, Xp, xn);
+TR_UNROLL
+        for (int i = 0; i < B; ++i) a[i] = zp[i] - t1[i];
+        ltsolve_v<B>(xP, Lp, a);
+    }
+}
+
 // x of the separator eliminated by a merge with factor F (L_S, Y_L, Y_R, z):
 //   x_M = L_S^{-T} (z - Y_L x_L - Y_R x_R)
 template <int B>
@@ -283,19 +359,22 @@ TR_UNROLL
     ltsolve_v<B>(xM, F + TR::FL, a);
 }
 
-// ---- warp tree (shuffles) -------------------------------------------------------
-// In: every lane's record rec.  Out: lane 0's rec = the merged record of the 32 chunks;
-// lane l > 0 holds in F the factor of the merge that consumed its record (round ctz(l)).
-template <int B>
-SP_DEV bool ss_warp_tree_up(double* rec, double* F) {
+// ---- group tree (shuffles over W = 32, 16 or 8 lanes) ------------------------------
+// In: every lane's record rec.  Out: the group leader's rec = the merged record of the W
+// chunks; every other lane holds in F the factor of the merge that consumed its record.
+// Fo + c * fs receives component c of the factor (registers: fs = 1; global: fs = lanes).
+// mask: the lanes of this group (groups of one warp run independently: their runs may
+// differ by a tile, so every warp-level primitive names only the group's own lanes).
+template <int B, int W>
+SP_DEV bool ss_warp_tree_up(double* rec, double* Fo, int fs, unsigned mask) {
     constexpr int NR = Rec<B>::N, NF = Tree<B>::NF;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & (W - 1);
     bool ok = true;
 #pragma unroll 1
-    for (int s = 1; s < 32; s <<= 1) {
+    for (int s = 1; s < W; s <<= 1) {
         double Bv[NR], Fm[NF];
 TR_UNROLL
-        for (int c = 0; c < NR; ++c) Bv[c] = __shfl_down_sync(kFullWarp, rec[c], s);
+        for (int c = 0; c < NR; ++c) Bv[c] = __shfl_down_sync(mask, rec[c], s, W);
 TR_UNROLL
         for (int c = 0; c < NF; ++c) Fm[c] = 0.0;
         if ((lane & (2 * s - 1)) == 0) {
@@ -306,24 +385,24 @@ TR_UNROLL
         }
 TR_UNROLL
         for (int c = 0; c < NF; ++c) {
-            const double f = __shfl_up_sync(kFullWarp, Fm[c], s);
-            if ((lane & (2 * s - 1)) == s) F[c] = f;
+            const double f = __shfl_up_sync(mask, Fm[c], s, W);
+            if ((lane & (2 * s - 1)) == s) Fo[c * fs] = f;
         }
     }
     return ok;
 }
-// In: lane 0's (xL, xR) = the solution at the tile's outer separators.  Out: every lane's
-// (xL, xR) = the solution at its chunk's left separator and at its own last block.
-template <int B>
-SP_DEV void ss_warp_tree_down(const double* F, double* xL, double* xR) {
-    const int lane = threadIdx.x & 31;
+// In: the leader's (xL, xR) = the solution at the tile's outer separators.  Out: every
+// lane's (xL, xR) = the solution at its chunk's left separator and at its own last block.
+template <int B, int W>
+SP_DEV void ss_warp_tree_down(const double* F, double* xL, double* xR, unsigned mask) {
+    const int lane = threadIdx.x & (W - 1);
 #pragma unroll 1
-    for (int s = 16; s >= 1; s >>= 1) {
+    for (int s = W / 2; s >= 1; s >>= 1) {
         double pL[B], pR[B], xM[B];
 TR_UNROLL
         for (int i = 0; i < B; ++i) {
-            pL[i] = __shfl_up_sync(kFullWarp, xL[i], s);
-            pR[i] = __shfl_up_sync(kFullWarp, xR[i], s);
+            pL[i] = __shfl_up_sync(mask, xL[i], s, W);
+            pR[i] = __shfl_up_sync(mask, xR[i], s, W);
             xM[i] = 0.0;
         }
         const bool consumed = (lane & (2 * s - 1)) == s;
@@ -337,13 +416,13 @@ TR_UNROLL
         }
 TR_UNROLL
         for (int i = 0; i < B; ++i) {
-            const double m = __shfl_down_sync(kFullWarp, xM[i], s);
+            const double m = __shfl_down_sync(mask, xM[i], s, W);
             if ((lane & (2 * s - 1)) == 0) xR[i] = m;
         }
     }
 }
 
-// ---- CTA-level trees in shared memory (warp records; the top system) -------------
+// ---- CTA-level trees in shared memory (group records; the top's warp records) -------
 // Forward tree over cnt records at slots [0, cnt) of R (component-major, row RS): leaves
 // the merged record at slot 0 and the merge factors parked (tree.cuh layout).
 template <int B>
@@ -397,87 +476,52 @@ TR_UNROLL
         __syncthreads();
     }
 }
-// Merge of records read with strides -> record at Cp, merge factor at Fp.  A real call:
-// it runs on a few threads of CTA 0 only, and its ~130 live doubles must not set the
-// register count of the whole kernel.
-template <int B>
-__device__ __noinline__ bool ss_merge_at(const double* Ap, int As, const double* Bp, int Bs, double* Cp, int Cs,
-                                         double* Fp, int Fs) {
-    constexpr int NR = Rec<B>::N, NF = Tree<B>::NF;
-    double A[NR], Bv[NR], Cm[NR], F[NF];
-TR_UNROLL
-    for (int c = 0; c < NR; ++c) {
-        A[c] = Ap[c * As];
-        Bv[c] = Bp[c * Bs];
-    }
-    const bool ok = tree_merge<B>(A, Bv, Cm, F);
-TR_UNROLL
-    for (int c = 0; c < NR; ++c) Cp[c * Cs] = Cm[c];
-TR_UNROLL
-    for (int c = 0; c < NF; ++c) Fp[c * Fs] = F[c];
-    return ok;
-}
 
-// ---- warp tile staging -----------------------------------------------------------
-// Full tiles with every upper block present go through three bulk copies (lane 0); the
-// last tile(s) and misaligned arrays are staged with plain loads, padded with identity
-// blocks past the end (D = I, U = 0, r = 0: x = 0, log det 0).
+// ---- tile staging ------------------------------------------------------------------
+// Three bulk copies per tile (the group leader): diag, upper, rhs, each clipped to the
+// blocks that exist and to an even block count (16-byte multiples); the odd block, the
+// last upper block's absence and the identity padding past the end (D = I, U = 0, r = 0:
+// x = 0, log det 0) are plain accesses.  Misaligned arrays are staged with plain loads.
 template <class C, int B>
 SP_DEV bool ss_tile_is_bulk(const SSArgs& a, long long tile) {
-    return a.bulk && (tile + 1) * C::WT <= a.n - 1;
+    return a.bulk && a.n - tile * C::WT >= 2;
 }
 template <class C, int B>
-SP_DEV void ss_tile_issue(const SSArgs& a, double* wm, long long tile, unsigned long long policy) {
+SP_DEV void ss_tile_issue(const SSArgs& a, double* wm, long long tile, unsigned long long policy, unsigned mask) {
     constexpr int BB = B * B;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & (C::LPT - 1);
     const long long t0 = tile * C::WT;
     void* bar = wm + C::W_BAR;
-    __syncwarp();
-    if (ss_tile_is_bulk<C, B>(a, tile)) {
-        if (lane == 0) {
-            ss_fence_async();
-            constexpr unsigned nbD = C::WT * BB * 8, nbR = C::WT * B * 8;
-            ss_bar_expect(bar, 2 * nbD + nbR);
-            ss_bulk_load(wm + C::W_D, a.diag + t0 * BB, nbD, bar, policy);
-            ss_bulk_load(wm + C::W_U, a.up + t0 * BB, nbD, bar, policy);
-            ss_bulk_load(wm + C::W_R, a.rhs + t0 * B, nbR, bar, policy);
-        }
-    } else {
-        const long long nd = a.n * BB, nu = (a.n - 1) * BB, nr = a.n * B;
-        for (int i = lane; i < C::WT * BB; i += 32) {
-            const long long gi = t0 * BB + i;
-            const int e = i % BB;
-            wm[C::W_D + i] = gi < nd ? a.diag[gi] : ((e / B == e % B) ? 1.0 : 0.0);
-            wm[C::W_U + i] = gi < nu ? a.up[gi] : 0.0;
-        }
-        for (int i = lane; i < C::WT * B; i += 32) {
-            const long long gi = t0 * B + i;
-            wm[C::W_R + i] = (gi < nr && a.rhs) ? a.rhs[gi] : 0.0;
-        }
+    const int cD = static_cast<int>(min(static_cast<long long>(C::WT), a.n - t0));
+    const int cU = static_cast<int>(max(0LL, min(static_cast<long long>(C::WT), a.n - 1 - t0)));
+    const int bD = a.bulk ? (cD & ~1) : 0, bU = a.bulk ? (cU & ~1) : 0;
+    __syncwarp(mask);
+    if (lane == 0 && bD > 0) {
+        ss_fence_async();
+        ss_bar_expect(bar, static_cast<unsigned>((bD * BB + bU * BB + bD * B) * 8));
+        ss_bulk_load(wm + C::W_D, a.diag + t0 * BB, static_cast<unsigned>(bD * BB * 8), bar, policy);
+        if (bU > 0) ss_bulk_load(wm + C::W_U, a.up + t0 * BB, static_cast<unsigned>(bU * BB * 8), bar, policy);
+        ss_bulk_load(wm + C::W_R, a.rhs + t0 * B, static_cast<unsigned>(bD * B * 8), bar, policy);
     }
-    if (lane < BB) wm[C::W_UH + lane] = t0 > 0 ? a.up[(t0 - 1) * BB + lane] : 0.0;
+    if (bD < C::WT || bU < C::WT) {  // ragged end or no bulk copies
+        for (int i = bD * BB + lane; i < C::WT * BB; i += C::LPT) {
+            const int e = i % BB;
+            wm[C::W_D + i] = i < cD * BB ? a.diag[t0 * BB + i] : ((e / B == e % B) ? 1.0 : 0.0);
+        }
+        for (int i = bU * BB + lane; i < C::WT * BB; i += C::LPT)
+            wm[C::W_U + i] = i < cU * BB ? a.up[t0 * BB + i] : 0.0;
+        for (int i = bD * B + lane; i < C::WT * B; i += C::LPT)
+            wm[C::W_R + i] = (i < cD * B && a.rhs) ? a.rhs[t0 * B + i] : 0.0;
+    }
+    for (int i = lane; i < BB; i += C::LPT) wm[C::W_UH + i] = t0 > 0 ? a.up[(t0 - 1) * BB + i] : 0.0;
 }
 template <class C, int B>
-SP_DEV void ss_tile_wait(const SSArgs& a, double* wm, long long tile, unsigned& phase) {
+SP_DEV void ss_tile_wait(const SSArgs& a, double* wm, long long tile, unsigned& phase, unsigned mask) {
     if (ss_tile_is_bulk<C, B>(a, tile)) {
         ss_bar_wait(wm + C::W_BAR, phase);
         phase ^= 1u;
     }
-    __syncwarp();  // halo / plain loads visible
-}
-
-// eliminate the staged tile -> lane records.  ck: lane 0's checkpoint of the carried block
-// (has_carry: every tile but the warp's first); lane 0's rec holds the run's record.
-template <class C, int B, bool KEEP>
-SP_DEV void ss_tile_reduce(const SSArgs& a, double* wm, long long tile, bool has_carry, const double* ck,
-                           double* rec) {
-    constexpr int BB = B * B;
-    const int lane = threadIdx.x & 31;
-    const double* Uprev = lane == 0 ? wm + C::W_UH : wm + C::W_U + (lane * C::M - 1) * BB;
-    const bool carry = has_carry && lane == 0;
-    const bool ok = ss_eliminate<C, B, KEEP>(wm + C::W_D, wm + C::W_U, wm + C::W_R, Uprev, lane * C::M,
-                                             carry ? ck : nullptr, wm + C::W_P, rec);
-    if (!ok) report(a.status, min(a.n - 1, tile * C::WT + lane * C::M), ST_NOT_PD);
+    __syncwarp(mask);  // halo / plain loads visible
 }
 
 template <class C, int B>
@@ -485,9 +529,11 @@ __global__ void __launch_bounds__(C::NT, 1) k_solve_stream(SSArgs a) {
     extern __shared__ double2 ss_sm2[];
     double* sm = reinterpret_cast<double*>(ss_sm2);
     constexpr int BB = B * B;
-    constexpr int NR = C::NR, NF = C::NF, NK = C::NK;
+    constexpr int NR = C::NR, NF = C::NF, NK = C::NK, LPT = C::LPT;
     using RC = Rec<B>;
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int t = threadIdx.x, lane = t & (LPT - 1), w = t / LPT;  // w: group within the CTA
+    const bool lead = lane == 0;
+    const unsigned gmask = LPT == 32 ? kFullWarp : (((1u << (LPT & 31)) - 1u) << ((t & 31) / LPT * LPT));
     const int cta = blockIdx.x;
     const long long GW = static_cast<long long>(a.G) * C::NW, gw = static_cast<long long>(cta) * C::NW + w;
     const long long tlo = a.ntiles * gw / GW, thi = a.ntiles * (gw + 1) / GW;
@@ -496,28 +542,27 @@ __global__ void __launch_bounds__(C::NT, 1) k_solve_stream(SSArgs a) {
     double* WR = sm + C::OFF_WR;
     double* WE = sm + C::OFF_WE;
     double* ckw = a.ckpt + gw * a.Tmax * NK;
+    double* tfw = a.tfac + gw * a.Tmax * (NF * LPT);
     unsigned phase = 0;
-    if (lane == 0) ss_bar_init(wm + C::W_BAR, 1);
+    if (lead) ss_bar_init(wm + C::W_BAR, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     const bool want_x = a.x != nullptr;
     const bool retain = want_x && cta != 0;  // the last tile of sweep 1 stays on the SM
     const unsigned long long pol_keep = a.l2mode == 1 ? ss_policy_last() : ss_policy_normal();
     const unsigned long long pol_once = ss_policy_first();
-    double rec[NR], F[NF], ck[NK];
-TR_UNROLL
-    for (int c = 0; c < NF; ++c) F[c] = 0.0;
-TR_UNROLL
-    for (int c = 0; c < NK; ++c) ck[c] = 0.0;
+    double rec[NR];
+    double* ck = wm + C::W_P;  // the carried block's checkpoint (written and read by the leader)
+    const double* Uprev = lead ? wm + C::W_UH : wm + C::W_U + (lane * C::M - 1) * BB;
 
     ss_stamp(a, 0);
-    // ---- sweep 1: tiles ascending -> warp record -----------------------------------
-    ss_tile_issue<C, B>(a, wm, tlo, T == 1 && retain ? pol_once : pol_keep);
+    // ---- sweep 1: tiles ascending -> run record --------------------------------------
+    ss_tile_issue<C, B>(a, wm, tlo, T == 1 && retain ? pol_once : pol_keep, gmask);
 #pragma unroll 1
     for (int k = 0; k < T; ++k) {
         const long long tile = tlo + k;
         const bool keep = retain && k == T - 1;
-        if (k > 0 && lane == 0) {  // checkpoint of the carried block: S_P, W_P = LR^T, r_P
+        if (k > 0 && lead) {  // checkpoint of the carried block: S_P, W_P = LR^T, r_P
 TR_UNROLL
             for (int i = 0; i < BB; ++i) ck[i] = rec[RC::RDIAG + i];
 TR_UNROLL
@@ -526,19 +571,22 @@ TR_UNROLL
                 for (int j = 0; j < B; ++j) ck[BB + i * B + j] = rec[RC::LR + j * B + i];
 TR_UNROLL
             for (int i = 0; i < B; ++i) ck[2 * BB + i] = rec[RC::RRHS + i];
-            if (want_x)
-TR_UNROLL
+            if (want_x && !keep)
                 for (int i = 0; i < NK; ++i) ckw[k * NK + i] = ck[i];
         }
-        ss_tile_wait<C, B>(a, wm, tile, phase);
-        if (keep) ss_tile_reduce<C, B, true>(a, wm, tile, k > 0, ck, rec);
-        else ss_tile_reduce<C, B, false>(a, wm, tile, k > 0, ck, rec);
+        __syncwarp(gmask);
+        ss_tile_wait<C, B>(a, wm, tile, phase, gmask);
+        if (!ss_eliminate<C, B>(wm + C::W_D, wm + C::W_U, wm + C::W_R, Uprev, lane * C::M,
+                                (k > 0 && lead) ? ck : nullptr, rec))
+            report(a.status, min(a.n - 1, tile * C::WT + lane * C::M), ST_NOT_PD);
         // the tile buffer is free again: stage the next tile behind the tree rounds
-        if (k + 1 < T) ss_tile_issue<C, B>(a, wm, tile + 1, (retain && k + 2 == T) ? pol_once : pol_keep);
-        if (!ss_warp_tree_up<B>(rec, F)) report(a.status, min(a.n - 1, tile * C::WT), ST_NOT_PD);
+        if (k + 1 < T) ss_tile_issue<C, B>(a, wm, tile + 1, (retain && k + 2 == T) ? pol_once : pol_keep, gmask);
+        // the tree's merge factors go to tfac (L2) for sweep 2
+        if (!ss_warp_tree_up<B, LPT>(rec, tfw + static_cast<long long>(k) * (NF * LPT) + lane, LPT, gmask))
+            report(a.status, min(a.n - 1, tile * C::WT), ST_NOT_PD);
     }
     ss_stamp(a, 1);
-    if (lane == 0)
+    if (lead)
 TR_UNROLL
         for (int c = 0; c < NR; ++c) WR[c * C::RSW + w] = rec[c];
     __syncthreads();
@@ -550,68 +598,60 @@ TR_UNROLL
     ss_stamp(a, 2);
 
     // ---- top: CTA 0 solves the G-record reduced system ---------------------------
+    // One record per thread (G <= NT, padded with identity records), a shuffle tree per
+    // warp, the NT / 32 warp records through the shared-memory tree, and back down.
     if (cta == 0) {
         if (t == 0)
             while (ss_ld_acquire(a.sync) < a.arrive_target) __nanosleep(40);
         __syncthreads();
         ss_stamp(a, 3);
-        const int G = a.G, GS = (G + 1) & ~1;
-        double* GR = sm;                 // [NR][GS] over the tile buffers
-        double* R = GR + NR * GS;        // [NR][RS]
-        double* E = R + NR * C::RS;      // [B][ES]
-        for (int c = 0; c < NR; ++c)
-            for (int i = t; i < G; i += C::NT) GR[c * GS + i] = __ldcg(a.crec + static_cast<long long>(c) * G + i);
-        __syncthreads();
-        const int q = (G + C::NT - 1) / C::NT;       // records per thread
-        const int NG = (G + q - 1) / q;              // active threads
-        const int g0 = t * q, gc = t < NG ? min(q, G - g0) : 0;
-        if (gc > 0) {  // chain in place at slot g0; factors parked over the consumed records
-            for (int i = 1; i < gc; ++i)
-                if (!ss_merge_at<B>(GR + g0, GS, GR + g0 + i, GS, GR + g0, GS, GR + g0 + i, GS))
-                    report(a.status, a.n - 1, ST_NOT_PD);
-            for (int c = 0; c < NR; ++c) R[c * C::RS + t] = GR[c * GS + g0];
+        const int G = a.G;
+        double* TR_ = sm;                      // [NR][RST] over the tile buffers
+        double* TE = TR_ + NR * C::RST;        // [B][EST]
+        double grec[NR], gF[NF];
+TR_UNROLL
+        for (int c = 0; c < NR; ++c) {
+            const bool diag1 = c >= RC::RDIAG && c < RC::RDIAG + BB && ((c - RC::RDIAG) % (B + 1) == 0);
+            grec[c] = t < G ? __ldcg(a.crec + static_cast<long long>(c) * G + t) : (diag1 ? 1.0 : 0.0);
         }
+TR_UNROLL
+        for (int c = 0; c < NF; ++c) gF[c] = 0.0;
+        if (!ss_warp_tree_up<B, 32>(grec, gF, 1, kFullWarp)) report(a.status, a.n - 1, ST_NOT_PD);
+        if ((t & 31) == 0)
+TR_UNROLL
+            for (int c = 0; c < NR; ++c) TR_[c * C::RST + (t >> 5)] = grec[c];
         __syncthreads();
-        if (!ss_tree_up<B>(R, C::RS, NG)) report(a.status, a.n - 1, ST_NOT_PD);
+        if (!ss_tree_up<B>(TR_, C::RST, C::NT / 32)) report(a.status, a.n - 1, ST_NOT_PD);
         if (t == 0) {  // top block
             double D[BB], r[B], Lc[BB], z[B], xx[B], ld;
 TR_UNROLL
-            for (int i = 0; i < BB; ++i) D[i] = R[(RC::RDIAG + i) * C::RS];
+            for (int i = 0; i < BB; ++i) D[i] = TR_[(RC::RDIAG + i) * C::RST];
 TR_UNROLL
-            for (int i = 0; i < B; ++i) r[i] = R[(RC::RRHS + i) * C::RS];
+            for (int i = 0; i < B; ++i) r[i] = TR_[(RC::RRHS + i) * C::RST];
             msym<B>(D);
             if (!chol<B>(Lc, D, ld)) report(a.status, a.n - 1, ST_NOT_PD);
             lsolve_v<B>(z, Lc, r);
             ltsolve_v<B>(xx, Lc, z);
 TR_UNROLL
             for (int i = 0; i < B; ++i) {
-                E[i * C::ES] = 0.0;
-                E[i * C::ES + 1] = xx[i];
+                TE[i * C::EST] = 0.0;
+                TE[i * C::EST + 1] = xx[i];
             }
-            if (a.logdet) *a.logdet = ld + R[RC::LOGDET * C::RS];
+            if (a.logdet) *a.logdet = ld + TR_[RC::LOGDET * C::RST];
         }
         __syncthreads();
         if (want_x) {
-            ss_tree_down<B>(R, C::RS, E, C::ES, NG);
-            if (gc > 0) {  // un-chain: x at the right separator of every record of the group
-                double xL[B], xR[B], xM[B];
+            ss_tree_down<B>(TR_, C::RST, TE, C::EST, C::NT / 32);
+            double xl[B], xr[B];
 TR_UNROLL
-                for (int i = 0; i < B; ++i) {
-                    xL[i] = E[i * C::ES + t];
-                    xR[i] = E[i * C::ES + t + 1];
-                }
-                for (int i = gc - 1; i >= 0; --i) {
-TR_UNROLL
-                    for (int p = 0; p < B; ++p) a.xsep[static_cast<long long>(g0 + i) * B + p] = xR[p];
-                    if (i == 0) break;
-                    double Fg[NF];
-TR_UNROLL
-                    for (int c = 0; c < NF; ++c) Fg[c] = GR[c * GS + g0 + i];
-                    ss_unmerge<B>(Fg, xL, xR, xM);
-TR_UNROLL
-                    for (int p = 0; p < B; ++p) xR[p] = xM[p];
-                }
+            for (int i = 0; i < B; ++i) {
+                xl[i] = (t & 31) == 0 ? TE[i * C::EST + (t >> 5)] : 0.0;
+                xr[i] = (t & 31) == 0 ? TE[i * C::EST + (t >> 5) + 1] : 0.0;
             }
+            ss_warp_tree_down<B, 32>(gF, xl, xr, kFullWarp);
+            if (t < G)
+TR_UNROLL
+                for (int p = 0; p < B; ++p) a.xsep[static_cast<long long>(t) * B + p] = xr[p];
             __threadfence();
             __syncthreads();
             if (t == 0) ss_st_release(a.sync + 1, a.release_target);
@@ -626,7 +666,7 @@ TR_UNROLL
     __syncthreads();
     ss_stamp(a, 5);
 
-    // ---- CTA tree down: the solution at every warp run's boundaries ---------------
+    // ---- CTA tree down: the solution at every run's boundaries ----------------------
     if (t < B) {
         WE[t * C::ESW] = cta > 0 ? __ldcg(a.xsep + static_cast<long long>(cta - 1) * B + t) : 0.0;
         WE[t * C::ESW + 1] = __ldcg(a.xsep + static_cast<long long>(cta) * B + t);
@@ -645,84 +685,35 @@ TR_UNROLL
     for (int k = T - 1; k >= 0; --k) {
         const long long tile = tlo + k;
         const bool staged = retain && k == T - 1;
-        if (!staged) {
-            ss_tile_issue<C, B>(a, wm, tile, pol_once);
-            if (k > 0 && lane == 0)
+        if (!staged) ss_tile_issue<C, B>(a, wm, tile, pol_once, gmask);
+        double F[NF];
+        {
+            const double* tf = tfw + static_cast<long long>(k) * (NF * LPT) + lane;
 TR_UNROLL
-                for (int i = 0; i < NK; ++i) ck[i] = ckw[k * NK + i];
-            rec[RC::LOGDET] = 0.0;
-TR_UNROLL
-            for (int i = 0; i < BB; ++i) rec[RC::LDIAG + i] = 0.0;
-TR_UNROLL
-            for (int i = 0; i < B; ++i) rec[RC::LRHS + i] = 0.0;
-            ss_tile_wait<C, B>(a, wm, tile, phase);
-            ss_tile_reduce<C, B, true>(a, wm, tile, k > 0, ck, rec);
-            ss_warp_tree_up<B>(rec, F);
+            for (int c = 0; c < NF; ++c) F[c] = lead ? 0.0 : tf[c * LPT];
         }
-        double xl[B], xr[B];
+        double xl[B], xr[B], xP[B];
 TR_UNROLL
         for (int i = 0; i < B; ++i) {
-            xl[i] = lane == 0 ? xZ[i] : 0.0;
-            xr[i] = lane == 0 ? xRt[i] : 0.0;
+            xl[i] = lead ? xZ[i] : 0.0;
+            xr[i] = lead ? xRt[i] : 0.0;
+            xP[i] = 0.0;
         }
-        ss_warp_tree_down<B>(F, xl, xr);
-        {  // back-substitution of this lane's chunk, x over the rhs slots
-            const int lo = lane * C::M;
-            double* sR = wm + C::W_R;
-            double xn[B];
+        ss_warp_tree_down<B, LPT>(F, xl, xr, gmask);
+        if (!staged) ss_tile_wait<C, B>(a, wm, tile, phase, gmask);
+        ss_dirichlet<C, B>(wm + C::W_D, wm + C::W_U, wm + C::W_R, Uprev, lane * C::M,
+                           (k > 0 && lead) ? (staged ? ck : ckw + k * NK) : nullptr, xl, xr, xP);
 TR_UNROLL
-            for (int i = 0; i < B; ++i) {
-                xn[i] = xr[i];
-                sR[(lo + C::M - 1) * B + i] = xr[i];
-            }
-#pragma unroll 1
-            for (int j = C::M - 2; j >= 0; --j) {
-                const double* Gp = wm + C::W_U + (lo + j) * BB;
-                const double* Vp = wm + C::W_D + (lo + j) * BB;
-                double* hp = sR + (lo + j) * B;
-                double xj[B];
-TR_UNROLL
-                for (int i = 0; i < B; ++i) {
-                    double s = hp[i];
-TR_UNROLL
-                    for (int c = 0; c < B; ++c) s = fma(-Gp[i * B + c], xn[c], s);
-TR_UNROLL
-                    for (int c = 0; c < B; ++c) s = fma(-Vp[i * B + c], xl[c], s);
-                    xj[i] = s;
-                }
-TR_UNROLL
-                for (int i = 0; i < B; ++i) {
-                    hp[i] = xj[i];
-                    xn[i] = xj[i];
-                }
-            }
-            // the carried block P (the previous tile's last block): the next right boundary
-            double xP[B];
-            const double* sP = wm + C::W_P;
-TR_UNROLL
-            for (int i = 0; i < B; ++i) {
-                double s = 0.0;
-                if (lane == 0 && k > 0) {
-                    s = sP[2 * BB + i];
-TR_UNROLL
-                    for (int c = 0; c < B; ++c) s = fma(-sP[BB + i * B + c], xn[c], s);
-TR_UNROLL
-                    for (int c = 0; c < B; ++c) s = fma(-sP[i * B + c], xl[c], s);
-                }
-                xP[i] = s;
-            }
-TR_UNROLL
-            for (int i = 0; i < B; ++i) xRt[i] = __shfl_sync(kFullWarp, xP[i], 0);
-        }
-        __syncwarp();
+        for (int i = 0; i < B; ++i) xRt[i] = __shfl_sync(gmask, xP[i], 0, LPT);
+        __syncwarp(gmask);
         {
             const long long t0 = tile * C::WT;
             const long long lim = min(static_cast<long long>(C::WT), a.n - t0) * B;
             const double* sR = wm + C::W_R;
             double* xo = a.x + t0 * B;
-            for (int i = lane; i < lim; i += 32) __stcs(xo + i, sR[i]);
+            for (int i = lane; i < lim; i += LPT) __stcs(xo + i, sR[i]);
         }
-        __syncwarp();
+        __syncwarp(gmask);
     }
     ss_stamp(a, 6);
 }
