@@ -693,11 +693,13 @@ int spingp_btd_cr_solve(spingp_ctx* ctx, int64_t n, int32_t b, const double* dia
         std::lock_guard<std::mutex> lk(ctx->mu);
         const size_t nd = static_cast<size_t>(n) * b * b, nu = static_cast<size_t>(n - 1) * b * b;
         const size_t nr = static_cast<size_t>(n) * b * k;
-        double* d_d = ctx->host_io.get(nd + nu + 2 * nr + 1);
-        double* d_u = d_d + nd;
-        double* d_r = d_u + nu;
-        double* d_x = d_r + nr;
-        double* d_ld = d_x + nr;
+        // every array on a 16-byte boundary (even offsets): the streaming solve's bulk copies
+        auto even = [](size_t c) { return (c + 1) & ~size_t(1); };
+        double* d_d = ctx->host_io.get(even(nd) + even(nu) + 2 * even(nr) + 2);
+        double* d_u = d_d + even(nd);
+        double* d_r = d_u + even(nu);
+        double* d_x = d_r + even(nr);
+        double* d_ld = d_x + even(nr);
         CUDA_OK(cudaMemcpyAsync(d_d, diag, nd * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
         if (nu) CUDA_OK(cudaMemcpyAsync(d_u, upper, nu * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
         if (nr) CUDA_OK(cudaMemcpyAsync(d_r, rhs, nr * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));

@@ -67,6 +67,12 @@ SP_DEV void report(unsigned long long* st, long long idx, int code) {
                       static_cast<unsigned long long>(code));
 }
 
+// A failure that may only be the echo of an earlier one (a pivot that is NaN because its
+// inputs already were): priority 2, reported only if nothing else was.
+SP_DEV void report_echo(unsigned long long* st, long long idx, int code) {
+    atomicMin(st, (2ULL << 60) | (static_cast<unsigned long long>(idx) << 4) | static_cast<unsigned long long>(code));
+}
+
 // level-l block k -> level-0 block index (the separator chain)
 SP_DEV long long to_global(const Geom& g, int lev, long long k) {
     for (int l = lev; l > 0; --l) {

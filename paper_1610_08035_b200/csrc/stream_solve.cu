@@ -46,8 +46,10 @@ void ss_print_stamps(spingp_ctx* ctx, unsigned long long* d, int G) {
     unsigned long long t0 = ~0ULL;
     for (int g = 0; g < G; ++g) t0 = std::min(t0, h[g * 16]);
     static const char* names[16] = {"start", "sweep 1 (warp 0)", "CTA record out", "top: all arrived", "top: released",
-                                    "release seen", "end (warp 0)", "", "", "", "", "", "", "", "", ""};
-    for (int k = 0; k < 7; ++k) {
+                                    "release seen", "end (warp 0)", "s1 t2: start", "s1 t2: tile in", "s1 t2: eliminated",
+                                    "s1 t2: tree up", "s2 t2: F loaded", "s2 t2: tree down", "s2 t2: tile in",
+                                    "s2 t2: solved", "s2 t2: stored"};
+    for (int k = 0; k < 16; ++k) {
         std::vector<double> v;
         for (int g = 0; g < G; ++g)
             if (h[g * 16 + k]) v.push_back((h[g * 16 + k] - t0) * 1e-3);

@@ -173,8 +173,21 @@ template <int B>
 struct SSElim {
     double T[B * B], rc[B], W[B * B], accLL[B * B], accrL[B];
     LogDetAcc piv;
-    bool ok;
+    unsigned long long* status;
+    long long idx, nmax;  // global index of the block being eliminated, n - 1
 };
+// A pivot failed.  If its inputs were finite it is the origin (priority 1); a NaN pivot
+// is most likely the echo of an earlier failure or of a NaN in the caller's arrays
+// (priority 2: reported only when nothing else was), so that the smallest index that
+// reaches the caller is the block that really is not positive definite.
+template <int N>
+SP_DEV void ss_report_pivot(unsigned long long* status, long long idx, const double* S) {
+    double acc = 0.0;
+TR_UNROLL
+    for (int i = 0; i < N; ++i) acc += S[i];
+    if (isfinite(acc)) report(status, idx, ST_NOT_PD);
+    else report_echo(status, idx, ST_NOT_PD);
+}
 // One interior block with diagonal D, coupling U (to the next block) and rhs r.
 template <int B>
 SP_DEV void ss_elim_step(SSElim<B>& es, const double* Dp, const double* Up, const double* rp) {
@@ -187,7 +200,8 @@ TR_UNROLL
 TR_UNROLL
     for (int i = 0; i < B; ++i) r[i] = rp[i] - es.rc[i];
     msym<B>(S);
-    es.ok = chol<B>(L, S, es.piv) && es.ok;
+    if (!chol<B>(L, S, es.piv)) ss_report_pivot<BB>(es.status, min(es.idx, es.nmax), S);
+    ++es.idx;
     lsolve_v<B>(z, L, r);
     lsolve<B>(X, L, U);
     lsolve<B>(Y, L, es.W);
@@ -209,15 +223,18 @@ TR_UNROLL
 // that couples block lo-1 to lo.  carry (group leader, tiles after the run's first): the
 // checkpoint (S_P, W_P = P_{P,Z}, r_P) of the carried block P, eliminated first, with the
 // run's accumulated left-separator terms and log det in rec (LDIAG, LRHS, LOGDET).
+// base = the global index of block lo (failed pivots are reported from here).
 template <class C, int B>
-SP_DEV bool ss_eliminate(const double* sD, const double* sU, const double* sR, const double* Uprev, int lo,
-                         const double* carry, double* rec) {
+SP_DEV void ss_eliminate(const double* sD, const double* sU, const double* sR, const double* Uprev, int lo,
+                         const double* carry, double* rec, unsigned long long* status, long long base, long long nmax) {
     constexpr int BB = B * B;
     constexpr int M = C::M;
     using RC = Rec<B>;
     SSElim<B> es;
     es.piv.init();
-    es.ok = true;
+    es.status = status;
+    es.idx = base - (carry ? 1 : 0);
+    es.nmax = nmax;
     mzero<B>(es.T);
     vzero<B>(es.rc);
     double ld0 = 0.0;
@@ -256,7 +273,6 @@ TR_UNROLL
 TR_UNROLL
     for (int i = 0; i < B; ++i) rec[RC::LRHS + i] = es.accrL[i];
     rec[RC::LOGDET] = ld0 + es.piv.logdet();
-    return es.ok;
 }
 
 // ---- one lane's chunk as a Dirichlet problem (sweep 2) ----------------------------
@@ -365,11 +381,14 @@ TR_UNROLL
 // Fo + c * fs receives component c of the factor (registers: fs = 1; global: fs = lanes).
 // mask: the lanes of this group (groups of one warp run independently: their runs may
 // differ by a tile, so every warp-level primitive names only the group's own lanes).
-template <int B, int W>
-SP_DEV bool ss_warp_tree_up(double* rec, double* Fo, int fs, unsigned mask) {
+// A failed merge pivot is reported at last(lane + stride - 1): the separator it eliminates
+// is the last block of that lane's record.
+template <int B, int W, class LastFn>
+SP_DEV void ss_warp_tree_up(double* rec, double* Fo, int fs, unsigned mask, unsigned long long* status,
+                            LastFn last) {
     constexpr int NR = Rec<B>::N, NF = Tree<B>::NF;
+    using RC = Rec<B>;
     const int lane = threadIdx.x & (W - 1);
-    bool ok = true;
 #pragma unroll 1
     for (int s = 1; s < W; s <<= 1) {
         double Bv[NR], Fm[NF];
@@ -379,7 +398,12 @@ TR_UNROLL
         for (int c = 0; c < NF; ++c) Fm[c] = 0.0;
         if ((lane & (2 * s - 1)) == 0) {
             double Cm[NR];
-            ok = tree_merge<B>(rec, Bv, Cm, Fm) && ok;
+            if (!tree_merge<B>(rec, Bv, Cm, Fm)) {  // rare: the pivot block, for origin vs echo
+                double Sm[B * B];
+TR_UNROLL
+                for (int i = 0; i < B * B; ++i) Sm[i] = rec[RC::RDIAG + i] + Bv[RC::LDIAG + i];
+                ss_report_pivot<B * B>(status, last(lane + s - 1), Sm);
+            }
 TR_UNROLL
             for (int c = 0; c < NR; ++c) rec[c] = Cm[c];
         }
@@ -389,7 +413,6 @@ TR_UNROLL
             if ((lane & (2 * s - 1)) == s) Fo[c * fs] = f;
         }
     }
-    return ok;
 }
 // In: the leader's (xL, xR) = the solution at the tile's outer separators.  Out: every
 // lane's (xL, xR) = the solution at its chunk's left separator and at its own last block.
@@ -425,20 +448,25 @@ TR_UNROLL
 // ---- CTA-level trees in shared memory (group records; the top's warp records) -------
 // Forward tree over cnt records at slots [0, cnt) of R (component-major, row RS): leaves
 // the merged record at slot 0 and the merge factors parked (tree.cuh layout).
-template <int B>
-SP_DEV bool ss_tree_up(double* R, int RS, int cnt) {
-    bool ok = true;
+// A failed merge pivot of node k in round j is reported at last(((2k + 1) << j) - 1).
+template <int B, class LastFn>
+SP_DEV void ss_tree_up(double* R, int RS, int cnt, unsigned long long* status, LastFn last) {
     const int J = tree_levels(cnt);
     for (int j = 0; j < J; ++j) {
         const int n = tree_width(cnt, j);
         TreeFwdScratch<B> sc;
         tree_fwd_compute<B>(R, RS, n, threadIdx.x, sc);
-        ok = ok && sc.ok;
+        if (!sc.ok) {  // origin or echo: the eliminated pivot block is finite or not
+            double Sm[B * B];
+TR_UNROLL
+            for (int i = 0; i < B * B; ++i)
+                Sm[i] = R[(Rec<B>::RDIAG + i) * RS + 2 * threadIdx.x] + R[(Rec<B>::LDIAG + i) * RS + 2 * threadIdx.x + 1];
+            ss_report_pivot<B * B>(status, last(((2 * static_cast<int>(threadIdx.x) + 1) << j) - 1), Sm);
+        }
         __syncthreads();
         tree_fwd_store<B>(R, RS, n, threadIdx.x, sc);
         __syncthreads();
     }
-    return ok;
 }
 // Reverse tree, solution only: E[q * ES + i], slots 0 (left) and 1 (right) set by the
 // caller; on return E holds x at the cnt + 1 record boundaries.
@@ -575,22 +603,32 @@ TR_UNROLL
                 for (int i = 0; i < NK; ++i) ckw[k * NK + i] = ck[i];
         }
         __syncwarp(gmask);
+        if (k == 2) ss_stamp(a, 7);
         ss_tile_wait<C, B>(a, wm, tile, phase, gmask);
-        if (!ss_eliminate<C, B>(wm + C::W_D, wm + C::W_U, wm + C::W_R, Uprev, lane * C::M,
-                                (k > 0 && lead) ? ck : nullptr, rec))
-            report(a.status, min(a.n - 1, tile * C::WT + lane * C::M), ST_NOT_PD);
+        if (k == 2) ss_stamp(a, 8);
+        ss_eliminate<C, B>(wm + C::W_D, wm + C::W_U, wm + C::W_R, Uprev, lane * C::M, (k > 0 && lead) ? ck : nullptr,
+                           rec, a.status, tile * C::WT + lane * C::M, a.n - 1);
+        if (k == 2) ss_stamp(a, 9);
         // the tile buffer is free again: stage the next tile behind the tree rounds
         if (k + 1 < T) ss_tile_issue<C, B>(a, wm, tile + 1, (retain && k + 2 == T) ? pol_once : pol_keep, gmask);
         // the tree's merge factors go to tfac (L2) for sweep 2
-        if (!ss_warp_tree_up<B, LPT>(rec, tfw + static_cast<long long>(k) * (NF * LPT) + lane, LPT, gmask))
-            report(a.status, min(a.n - 1, tile * C::WT), ST_NOT_PD);
+        ss_warp_tree_up<B, LPT>(rec, tfw + static_cast<long long>(k) * (NF * LPT) + lane, LPT, gmask, a.status,
+                                [&](int l) { return min(a.n - 1, tile * C::WT + (l + 1) * C::M - 1); });
+        if (k == 2) ss_stamp(a, 10);
     }
     ss_stamp(a, 1);
     if (lead)
 TR_UNROLL
         for (int c = 0; c < NR; ++c) WR[c * C::RSW + w] = rec[c];
     __syncthreads();
-    if (!ss_tree_up<B>(WR, C::RSW, C::NW)) report(a.status, a.n - 1, ST_NOT_PD);
+    // last block of the run of group g of this CTA / of CTA c
+    auto run_last = [&](int g) {
+        return min(a.n - 1, a.ntiles * (static_cast<long long>(cta) * C::NW + g + 1) / GW * C::WT - 1);
+    };
+    auto cta_last = [&](int c) {
+        return min(a.n - 1, a.ntiles * (static_cast<long long>(min(c, a.G - 1) + 1) * C::NW) / GW * C::WT - 1);
+    };
+    ss_tree_up<B>(WR, C::RSW, C::NW, a.status, run_last);
     for (int c = t; c < NR; c += C::NT) a.crec[static_cast<long long>(c) * a.G + cta] = WR[c * C::RSW];
     __threadfence();
     __syncthreads();
@@ -616,12 +654,12 @@ TR_UNROLL
         }
 TR_UNROLL
         for (int c = 0; c < NF; ++c) gF[c] = 0.0;
-        if (!ss_warp_tree_up<B, 32>(grec, gF, 1, kFullWarp)) report(a.status, a.n - 1, ST_NOT_PD);
+        ss_warp_tree_up<B, 32>(grec, gF, 1, kFullWarp, a.status, [&](int l) { return cta_last((t & ~31) + l); });
         if ((t & 31) == 0)
 TR_UNROLL
             for (int c = 0; c < NR; ++c) TR_[c * C::RST + (t >> 5)] = grec[c];
         __syncthreads();
-        if (!ss_tree_up<B>(TR_, C::RST, C::NT / 32)) report(a.status, a.n - 1, ST_NOT_PD);
+        ss_tree_up<B>(TR_, C::RST, C::NT / 32, a.status, [&](int wv) { return cta_last(32 * wv + 31); });
         if (t == 0) {  // top block
             double D[BB], r[B], Lc[BB], z[B], xx[B], ld;
 TR_UNROLL
@@ -629,7 +667,7 @@ TR_UNROLL
 TR_UNROLL
             for (int i = 0; i < B; ++i) r[i] = TR_[(RC::RRHS + i) * C::RST];
             msym<B>(D);
-            if (!chol<B>(Lc, D, ld)) report(a.status, a.n - 1, ST_NOT_PD);
+            if (!chol<B>(Lc, D, ld)) ss_report_pivot<BB>(a.status, a.n - 1, D);
             lsolve_v<B>(z, Lc, r);
             ltsolve_v<B>(xx, Lc, z);
 TR_UNROLL
@@ -699,13 +737,17 @@ TR_UNROLL
             xr[i] = lead ? xRt[i] : 0.0;
             xP[i] = 0.0;
         }
+        if (k == 2) ss_stamp(a, 11);
         ss_warp_tree_down<B, LPT>(F, xl, xr, gmask);
+        if (k == 2) ss_stamp(a, 12);
         if (!staged) ss_tile_wait<C, B>(a, wm, tile, phase, gmask);
+        if (k == 2) ss_stamp(a, 13);
         ss_dirichlet<C, B>(wm + C::W_D, wm + C::W_U, wm + C::W_R, Uprev, lane * C::M,
                            (k > 0 && lead) ? (staged ? ck : ckw + k * NK) : nullptr, xl, xr, xP);
 TR_UNROLL
         for (int i = 0; i < B; ++i) xRt[i] = __shfl_sync(gmask, xP[i], 0, LPT);
         __syncwarp(gmask);
+        if (k == 2) ss_stamp(a, 14);
         {
             const long long t0 = tile * C::WT;
             const long long lim = min(static_cast<long long>(C::WT), a.n - t0) * B;
@@ -714,6 +756,7 @@ TR_UNROLL
             for (int i = lane; i < lim; i += LPT) __stcs(xo + i, sR[i]);
         }
         __syncwarp(gmask);
+        if (k == 2) ss_stamp(a, 15);
     }
     ss_stamp(a, 6);
 }
