@@ -541,7 +541,13 @@ SP_DEV void ss_tile_issue(const SSArgs& a, double* wm, long long tile, unsigned 
         for (int i = bD * B + lane; i < C::WT * B; i += C::LPT)
             wm[C::W_R + i] = (i < cD * B && a.rhs) ? a.rhs[t0 * B + i] : 0.0;
     }
-    for (int i = lane; i < BB; i += C::LPT) wm[C::W_UH + i] = t0 > 0 ? a.up[(t0 - 1) * BB + i] : 0.0;
+    // halo: the upper block that couples the previous tile's last block to this tile (8 bytes
+    // off a 16-byte boundary, so not a bulk copy): asynchronous 8-byte copies, waited for with
+    // the tile, so that the issuing lanes do not sit on an L2 / HBM round trip here
+    for (int i = lane; i < BB; i += C::LPT) {
+        if (t0 > 0) tree_copy(wm + C::W_UH + i, a.up + (t0 - 1) * BB + i);
+        else wm[C::W_UH + i] = 0.0;
+    }
 }
 template <class C, int B>
 SP_DEV void ss_tile_wait(const SSArgs& a, double* wm, long long tile, unsigned& phase, unsigned mask) {
@@ -549,6 +555,7 @@ SP_DEV void ss_tile_wait(const SSArgs& a, double* wm, long long tile, unsigned& 
         ss_bar_wait(wm + C::W_BAR, phase);
         phase ^= 1u;
     }
+    tree_copy_wait();  // the halo's cp.async
     __syncwarp(mask);  // halo / plain loads visible
 }
 

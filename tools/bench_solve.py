@@ -36,19 +36,34 @@ def measure(n=1_000_000, b=3, steps=20, device=0, check=True):
         if st != 0:
             raise RuntimeError(f"status {st}")
 
-    for _ in range(3):
-        run()
-    torch.cuda.synchronize()
-    ms = []
-    for _ in range(steps):
-        flush.zero_()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        run()
-        e1.record(stream)
-        e1.synchronize()
-        ms.append(e0.elapsed_time(e1))
+    def timed():
+        for _ in range(3):
+            run()
+        torch.cuda.synchronize()
+        out = []
+        for _ in range(steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            run()
+            e1.record(stream)
+            e1.synchronize()
+            out.append(e0.elapsed_time(e1))
+        return out
+
+    # the partitioned thread-per-chunk kernels (round 1) for comparison, then the default path
+    # (b <= 4, one rhs: the tile-streaming kernel, csrc/stream_solve.cuh)
+    prev = os.environ.get("SPINGP_SOLVE_STREAM")
+    os.environ["SPINGP_SOLVE_STREAM"] = "0"
+    t_part = float(np.median(timed()))
+    if prev is None:
+        del os.environ["SPINGP_SOLVE_STREAM"]
+    else:
+        os.environ["SPINGP_SOLVE_STREAM"] = prev
+    k0 = ctx.launch_count()
+    ms = timed()
+    launches = (ctx.launch_count() - k0) // (steps + 3)
     t = float(np.median(ms))
     res = None
     if check:  # residual || M x - rhs || / || rhs || (block matvec on the device, fp64)
@@ -67,7 +82,10 @@ def measure(n=1_000_000, b=3, steps=20, device=0, check=True):
     gbs = bytes_ / (t * 1e-3) / 1e9
     out = {"op": "spingp_btd_cr_solve_device", "n": n, "b": b, "k": 1, "ms": t, "blocks_per_s": n / (t * 1e-3),
            "compulsory_bytes": bytes_, "achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak,
-           "residual": res, "data": "random SPD blocks (seeded), L2 flushed before each call"}
+           "residual": res, "launches_per_solve": launches,
+           "kernel": "k_solve_stream" if launches == 1 else "k_fwdL / k_tree_* / k_revL",
+           "partitioned_ms": t_part, "partitioned_frac": bytes_ / (t_part * 1e-3) / 1e9 / peak,
+           "data": "random SPD blocks (seeded), L2 flushed before each call"}
     ctx.close()
     return out
 
