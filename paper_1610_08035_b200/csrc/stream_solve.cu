@@ -9,6 +9,7 @@
 
 #include "ctx.hpp"
 #include "stream_solve.cuh"
+#include "strip_solve.cuh"
 
 // b = 3 shape: warps per CTA (one CTA per SM), blocks per lane
 #ifndef SP_SS3_NW
@@ -19,6 +20,10 @@
 #endif
 #ifndef SP_SS3_LPT
 #define SP_SS3_LPT 32
+#endif
+// strip kernel, b = 3: blocks per lane and sub-tile
+#ifndef SP_ST3_MB
+#define SP_ST3_MB 4
 #endif
 
 namespace spingp_host {
@@ -129,6 +134,80 @@ bool ss_launch(spingp_ctx* ctx, int64_t n, const double* diag, const double* upp
     return true;
 }
 
+// The strip kernel (strip_solve.cuh): one lane per long chunk, cooperative cp.async staging.
+template <int B, int NWARP, int MB>
+bool st_launch(spingp_ctx* ctx, int64_t n, const double* diag, const double* upper, const double* rhs, double* x,
+               double* logdet) {
+    using C = STCfg<B, NWARP, MB>;
+    constexpr int NR = C::NR, NCK = C::NCK, NF = C::NF, NW = C::NW, NT = C::NT;
+    if (n < static_cast<int64_t>(NT) * 2 * MB) return false;  // at least two sub-tiles per lane of one CTA
+    auto kern = k_solve_strip<C, B>;
+    static unsigned long long attr = 0;
+    opt_in_smem(reinterpret_cast<const void*>(kern), attr, ctx->device, static_cast<int>(C::SMEM_BYTES));
+    static int resident_dev[64] = {};
+    int& resident = resident_dev[ctx->device & 63];
+    if (!resident) {
+        int per = 0, sms = 0;
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, NT, C::SMEM_BYTES));
+        CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+        resident = std::max(1, per) * sms;
+    }
+    long long G = std::min<long long>(resident, n / (static_cast<long long>(NT) * 2 * MB));
+    G = std::min<long long>(G, NT);  // the top system: one CTA record per thread of CTA 0
+    if (const char* e = std::getenv("SPINGP_SS_CTAS")) G = std::max<long long>(1, std::min<long long>(G, std::atoll(e)));
+    const long long GL = G * NT, GW = G * NW;
+    const int nsub = static_cast<int>((n + MB * GL - 1) / (MB * GL));  // sub-tiles per lane, all full
+    const long long Lc = static_cast<long long>(nsub) * MB;
+    ctx->ensure_ws(arena_bytes(NR * G) + arena_bytes(G * B) + arena_bytes(GW * nsub * NCK * 32) +
+                   arena_bytes(GW * NF * 32) + 4096);
+    ctx->ws.reset();
+    SSArgs a{};
+    a.diag = diag;
+    a.up = upper;
+    a.rhs = rhs;
+    a.x = x;
+    a.logdet = logdet;
+    a.n = n;
+    a.G = static_cast<int>(G);
+    a.Lc = Lc;
+    a.nsub = nsub;
+    auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    a.bulk = (rhs && aligned(diag) && aligned(upper) && aligned(rhs)) ? 1 : 0;
+    a.crec = ctx->ws.take<double>(NR * G);
+    a.xsep = ctx->ws.take<double>(G * B);
+    a.ckpt = ctx->ws.take<double>(GW * nsub * NCK * 32);
+    a.tfac = ctx->ws.take<double>(GW * NF * 32);
+    if (!ctx->d_ss_sync) {
+        CUDA_OK(cudaMalloc(&ctx->d_ss_sync, 2 * sizeof(unsigned long long)));
+        CUDA_OK(cudaMemsetAsync(ctx->d_ss_sync, 0, 2 * sizeof(unsigned long long), ctx->stream));
+        ctx->ss_arrivals = ctx->ss_releases = 0;
+    }
+    a.sync = ctx->d_ss_sync;
+    a.arrive_target = ctx->ss_arrivals + static_cast<unsigned long long>(G);
+    a.release_target = ctx->ss_releases + 1;
+    a.status = ctx->d_status;
+    const bool stamps = std::getenv("SPINGP_SS_STAMPS") != nullptr;
+    a.stamps = nullptr;
+    if (stamps) {
+        CUDA_OK(cudaMalloc(&a.stamps, G * 16 * sizeof(unsigned long long)));
+        CUDA_OK(cudaMemsetAsync(a.stamps, 0, G * 16 * sizeof(unsigned long long), ctx->stream));
+    }
+    void* args[] = {&a};
+    ctx->pre();
+    CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(static_cast<unsigned>(G)), dim3(NT), args,
+                                        C::SMEM_BYTES, ctx->stream));
+    ctx->launched("k_solve_strip");
+    ctx->ss_arrivals = a.arrive_target;
+    if (x) ctx->ss_releases = a.release_target;
+    if (stamps) ss_print_stamps(ctx, a.stamps, static_cast<int>(G));
+    return true;
+}
+
+bool strip_enabled() {
+    const char* e = std::getenv("SPINGP_SOLVE_STRIP");
+    return !(e && std::strcmp(e, "0") == 0);
+}
+
 }  // namespace
 
 // x = M^{-1} rhs (one right-hand side, or none: log det only) by the tile-streaming kernel;
@@ -136,6 +215,17 @@ bool ss_launch(spingp_ctx* ctx, int64_t n, const double* diag, const double* upp
 bool stream_solve(spingp_ctx* ctx, int64_t n, int b, const double* diag, const double* upper, const double* rhs,
                   double* x, double* logdet) {
     if (!stream_enabled() || n < 2 || !upper) return false;
+    if (strip_enabled()) {  // one lane per long chunk (strip_solve.cuh); else contiguous tiles
+        bool done = false;
+        switch (b) {
+            case 1: done = st_launch<1, 8, 8>(ctx, n, diag, upper, rhs, x, logdet); break;
+            case 2: done = st_launch<2, 8, 4>(ctx, n, diag, upper, rhs, x, logdet); break;
+            case 3: done = st_launch<3, 8, SP_ST3_MB>(ctx, n, diag, upper, rhs, x, logdet); break;
+            case 4: done = st_launch<4, 4, 4>(ctx, n, diag, upper, rhs, x, logdet); break;
+            default: break;
+        }
+        if (done) return true;
+    }
     switch (b) {
         case 1: return ss_launch<1, 8, 7, 32>(ctx, n, diag, upper, rhs, x, logdet);
         case 2: return ss_launch<2, 8, 5, 32>(ctx, n, diag, upper, rhs, x, logdet);

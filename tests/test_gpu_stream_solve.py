@@ -1,6 +1,8 @@
-"""The tile-streaming cr_solve (csrc/stream_solve.cuh: b <= 4, at most one right-hand side,
-n >= 8 warp tiles) against the CPU oracle's block Thomas and
-against the partitioned kernels it replaces on that path."""
+"""The streaming cr_solve kernels (b <= 4, at most one right-hand side): the strip kernel
+(csrc/strip_solve.cuh, one lane per long chunk; n >= 2 sub-tiles per lane of one CTA) and the
+tile kernel (csrc/stream_solve.cuh, contiguous warp tiles; SPINGP_SOLVE_STRIP=0 or smaller n)
+against the CPU oracle's block Thomas and against the partitioned
+kernels they replace on that path."""
 import os
 
 import numpy as np
@@ -33,18 +35,30 @@ def system(n, b, seed):
     return diag, upper, rhs
 
 
+@pytest.fixture(params=["strip", "tile"])
+def kernel(request):
+    """Selects the streaming kernel: the strip kernel is tried first unless disabled."""
+    if request.param == "tile":
+        os.environ["SPINGP_SOLVE_STRIP"] = "0"
+    yield request.param
+    os.environ.pop("SPINGP_SOLVE_STRIP", None)
+
+
 def launches(ctx, fn):
     k0 = ctx.launch_count()
     out = fn()
     return out, ctx.launch_count() - k0
 
 
-# tile = 32 lanes x M blocks (b = 1: 224, b = 2, 3: 160, b = 4: 96), 8 warps per CTA: the
-# sizes cover one CTA, ragged last tiles (odd and even remainders), several CTAs and tiles
-@pytest.mark.parametrize("n,b", [(1792, 1), (1793, 1), (30001, 1), (1280, 2), (1283, 2), (25000, 2), (1280, 3),
-                                 (1281, 3), (1282, 3), (1439, 3), (1441, 3), (4801, 3), (60000, 3), (200001, 3),
-                                 (768, 4), (769, 4), (20001, 4)])
-def test_stream_solve_matches_oracle(ctx, n, b):
+# tile kernel: tile = 32 lanes x M blocks (b = 1: 224, b = 2, 3: 160, b = 4: 96), 8 warps per
+# CTA; strip kernel: 256 lanes per CTA, sub-tiles of 8 / 4 / 4 / 2 blocks per lane, from
+# 4096 / 2048 / 2048 / 1024 blocks (smaller n falls through to the tile kernel).  The sizes
+# cover one CTA, ragged ends (odd and even remainders), several CTAs and sub-tiles.
+@pytest.mark.parametrize("n,b", [(1792, 1), (1793, 1), (4096, 1), (30001, 1), (1280, 2), (1283, 2), (2049, 2),
+                                 (25000, 2), (1280, 3), (1281, 3), (1282, 3), (1439, 3), (1441, 3), (2048, 3),
+                                 (2049, 3), (2051, 3), (4801, 3), (60000, 3), (200001, 3), (768, 4), (769, 4),
+                                 (1025, 4), (20001, 4)])
+def test_stream_solve_matches_oracle(ctx, kernel, n, b):
     diag, upper, rhs = system(n, b, n + 7 * b)
     (x, ld), nl = launches(ctx, lambda: ctx.btd_cr_solve(diag, upper, rhs))
     assert nl == 1, "the streaming solve is one kernel launch"
@@ -54,7 +68,7 @@ def test_stream_solve_matches_oracle(ctx, n, b):
     assert nl == 1 and abs(ld0 - ldo) <= 1e-12 * abs(ldo)
 
 
-def test_stream_solve_equals_partitioned_path(ctx):
+def test_stream_solve_equals_partitioned_path(ctx, kernel):
     n, b = 50000, 3
     diag, upper, rhs = system(n, b, 5)
     x, ld = ctx.btd_cr_solve(diag, upper, rhs)
@@ -77,9 +91,11 @@ def test_stream_solve_below_threshold_and_multi_rhs_use_partitioned_kernels(ctx)
     assert nl > 1 and rel(x, O.btd_solve(diag, upper, rhs)[0]) < 1e-12
 
 
-# a non-positive-definite block inside a lane chunk, at a lane, tile, run and CTA boundary
-@pytest.mark.parametrize("bad", [0, 7, 159, 164, 319, 1599, 3333, 4800])
-def test_stream_solve_reports_the_failing_block(ctx, bad):
+# a non-positive-definite block inside a lane chunk and at the lane, tile / warp, run and CTA
+# boundaries of both kernels (n = 4801: tile kernel 160-block tiles, 3 CTAs of 10 tiles; strip
+# kernel 10 blocks per lane, 2 CTAs of 2560 blocks)
+@pytest.mark.parametrize("bad", [0, 7, 9, 159, 164, 319, 1599, 2559, 3333, 4800])
+def test_stream_solve_reports_the_failing_block(ctx, kernel, bad):
     n, b = 4801, 3
     diag, upper, rhs = system(n, b, 11)
     diag[bad] = -np.eye(b)
@@ -92,7 +108,7 @@ def test_stream_solve_reports_the_failing_block(ctx, bad):
     assert rel(x, O.btd_solve(diag, upper, rhs)[0]) < 1e-12
 
 
-def test_stream_solve_device_pointers_any_alignment(ctx):
+def test_stream_solve_device_pointers_any_alignment(ctx, kernel):
     torch = pytest.importorskip("torch")
     n, b = 3201, 3
     diag, upper, rhs = system(n, b, 21)
