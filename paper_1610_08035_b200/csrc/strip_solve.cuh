@@ -43,7 +43,8 @@ struct STCfg {
     static constexpr int W_D = 0;
     static constexpr int W_U = 32 * SD;
     static constexpr int W_R = 64 * SD;
-    static constexpr int W_SIZE = ss_even(64 * SD + 32 * SR);
+    static constexpr int W_BAR = ss_even(64 * SD + 32 * SR);   // two mbarriers (bulk-copy staging)
+    static constexpr int W_SIZE = W_BAR + 2;
     static constexpr int RSW = ss_even(NW);
     static constexpr int ESW = ss_even(NW + 1);
     static constexpr int OFF_WR = NW * W_SIZE;
@@ -119,6 +120,45 @@ TR_UNROLL
     }
 }
 
+#ifdef SP_ST_BULK
+// Staging by bulk copies: lane q copies its own strip (three cp.async.bulk: diag, upper, rhs)
+// onto the warp's mbarrier `bar`; the strips across / past the end element by element.
+template <class C, int B, int NB>
+SP_DEV void st_stage_bulk(const SSArgs& a, double* wm, long long wfl, int qin, int s, int j0, void* bar,
+                          unsigned long long policy) {
+    constexpr int BB = B * B, MB = C::MB;
+    const int lane = threadIdx.x & 31;
+    const long long gb0 = wfl * a.Lc + static_cast<long long>(s) * MB + j0;
+    double* wD = wm + C::W_D + j0 * BB;
+    double* wU = wm + C::W_U + j0 * BB;
+    double* wR = wm + C::W_R + j0 * B;
+    constexpr unsigned nbD = NB * BB * 8, nbR = NB * B * 8;
+    if (lane == 0) ss_bar_expect(bar, static_cast<unsigned>(qin) * (2 * nbD + nbR));
+    __syncwarp();
+    if (lane < qin) {
+        const long long gb = gb0 + lane * a.Lc;
+        ss_fence_async();
+        ss_bulk_load(wD + lane * C::SD, a.diag + gb * BB, nbD, bar, policy);
+        ss_bulk_load(wU + lane * C::SD, a.up + gb * BB, nbD, bar, policy);
+        ss_bulk_load(wR + lane * C::SR, a.rhs + gb * B, nbR, bar, policy);
+    }
+    if (qin == 32) return;
+    const long long nd = a.n * BB, nu = (a.n - 1) * BB, nr = a.n * B;
+    const int nq = 32 - qin;
+    for (int p = lane; p < nq * NB * BB; p += 32) {
+        const int q = qin + p / (NB * BB), e = p % (NB * BB);
+        const long long gi = (gb0 + q * a.Lc) * BB + e;
+        wD[q * C::SD + e] = gi < nd ? a.diag[gi] : (((e % BB) % (B + 1) == 0) ? 1.0 : 0.0);
+        wU[q * C::SD + e] = gi < nu ? a.up[gi] : 0.0;
+    }
+    for (int p = lane; p < nq * NB * B; p += 32) {
+        const int q = qin + p / (NB * B), e = p % (NB * B);
+        const long long gi = (gb0 + q * a.Lc) * B + e;
+        wR[q * C::SR + e] = (gi < nr && a.rhs) ? a.rhs[gi] : 0.0;
+    }
+}
+#endif
+
 // Store the sub-tile's solution (the rhs slots of the 32 strips) to x.
 template <class C, int B>
 SP_DEV void st_store_x(const SSArgs& a, const double* wm, long long wfl, int s) {
@@ -169,6 +209,18 @@ __global__ void __launch_bounds__(C::NT, 1) k_solve_strip(SSArgs a) {
     double* ckw = a.ckpt + gwarp * nsub * (NCK * 32) + lane;
     double* tfw = a.tfac + gwarp * (NF * 32) + lane;
     const bool want_x = a.x != nullptr;
+#ifdef SP_ST_BULK
+    void* bar0 = wm + C::W_BAR;
+    void* bar1 = wm + C::W_BAR + 1;
+    unsigned ph0 = 0, ph1 = 0;
+    if (lane == 0) {
+        ss_bar_init(bar0, 1);
+        ss_bar_init(bar1, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    const unsigned long long pol = ss_policy_normal();
+#endif
     const bool empty = wfl * a.Lc >= a.n;  // a warp past the end of the matrix: neutral records
     // lanes of this warp whose whole chunk (and its last upper block) lies inside the matrix
     const int qin = a.bulk ? static_cast<int>(max(0LL, min(32LL, (a.n - 1) / a.Lc - wfl))) : 0;
@@ -198,14 +250,24 @@ TR_UNROLL
         // sub-tiles are staged in halves of MB / 2 blocks, one half ahead of the elimination
         // (the half being filled was eliminated one step earlier)
         constexpr int HB = MB / 2;
+#ifdef SP_ST_BULK
+        if (!empty) st_stage_bulk<C, B, HB>(a, wm, wfl, qin, 0, 0, bar0, pol);
+#else
         if (!empty) st_stage<C, B, HB>(a, wm, wfl, qin, 0, 0);
         st_cp_commit();
+#endif
 #pragma unroll 1
         for (int sh = 0; sh < 2 * nsub && !empty; ++sh) {
             const int s = sh >> 1, h = sh & 1;
             __syncwarp();
+#ifdef SP_ST_BULK
+            if (sh + 1 < 2 * nsub)
+                st_stage_bulk<C, B, HB>(a, wm, wfl, qin, (sh + 1) >> 1, ((sh + 1) & 1) * HB, ((sh + 1) & 1) ? bar1 : bar0,
+                                        pol);
+#else
             if (sh + 1 < 2 * nsub) st_stage<C, B, HB>(a, wm, wfl, qin, (sh + 1) >> 1, ((sh + 1) & 1) * HB);
             st_cp_commit();
+#endif
             if (want_x && s > 0 && h == 0) {  // the state at the sub-tile's start, for sweep 2
                 double* ck = ckw + static_cast<long long>(s) * (NCK * 32);
 TR_UNROLL
@@ -216,7 +278,17 @@ TR_UNROLL
                 for (int i = 0; i < B; ++i) ck[(2 * BB + i) * 32] = es.rc[i];
             }
             if (sh == 6) ss_stamp(a, 7);
+#ifdef SP_ST_BULK
+            if (h == 0) {
+                ss_bar_wait(bar0, ph0);
+                ph0 ^= 1u;
+            } else {
+                ss_bar_wait(bar1, ph1);
+                ph1 ^= 1u;
+            }
+#else
             st_cp_wait_but_one();
+#endif
             __syncwarp();
             if (sh == 6) ss_stamp(a, 8);
             const int nel = sh == 2 * nsub - 1 ? HB - 1 : HB;
@@ -357,7 +429,11 @@ TR_UNROLL
         double T[BB], rc[B];
         if (s < nsub - 1) {  // (the last sub-tile of sweep 1 is still staged)
             __syncwarp();
+#ifdef SP_ST_BULK
+            st_stage_bulk<C, B, MB>(a, wm, wfl, qin, s, 0, bar0, ss_policy_first());
+#else
             st_stage<C, B, MB>(a, wm, wfl, qin, s, 0);
+#endif
         }
         if (s > 0) {
             const double* ck = ckw + static_cast<long long>(s) * (NCK * 32);
@@ -376,7 +452,14 @@ TR_UNROLL
             mtv<B>(rc, Up0, xl);
         }
         if (s == 2) ss_stamp(a, 11);
+#ifdef SP_ST_BULK
+        if (s < nsub - 1) {
+            ss_bar_wait(bar0, ph0);
+            ph0 ^= 1u;
+        }
+#else
         st_cp_wait();
+#endif
         __syncwarp();
         if (s == 2) ss_stamp(a, 12);
         const int nel = s == nsub - 1 ? MB - 1 : MB;

@@ -53,7 +53,7 @@ def measure(n=1_000_000, b=3, steps=20, device=0, check=True):
         return out
 
     # the partitioned thread-per-chunk kernels (round 1) for comparison, then the default path
-    # (b <= 4, one rhs: the tile-streaming kernel, csrc/stream_solve.cuh)
+    # (b <= 4, one rhs: the strip-streaming kernel, csrc/strip_solve.cuh)
     prev = os.environ.get("SPINGP_SOLVE_STREAM")
     os.environ["SPINGP_SOLVE_STREAM"] = "0"
     t_part = float(np.median(timed()))
@@ -83,7 +83,7 @@ def measure(n=1_000_000, b=3, steps=20, device=0, check=True):
     out = {"op": "spingp_btd_cr_solve_device", "n": n, "b": b, "k": 1, "ms": t, "blocks_per_s": n / (t * 1e-3),
            "compulsory_bytes": bytes_, "achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak,
            "residual": res, "launches_per_solve": launches,
-           "kernel": "k_solve_stream" if launches == 1 else "k_fwdL / k_tree_* / k_revL",
+           "kernel": "k_solve_strip" if launches == 1 else "k_fwdL / k_tree_* / k_revL",
            "partitioned_ms": t_part, "partitioned_frac": bytes_ / (t_part * 1e-3) / 1e9 / peak,
            "data": "random SPD blocks (seeded), L2 flushed before each call"}
     ctx.close()

@@ -33,7 +33,8 @@ PY
 cap final_ncu_cfg2 "k_(rev0|fwd0|tree_coop|reduce)" 0 4 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-per-config
 cap final_ncu_cfg4 "k_(rev0|fwd0)_team|k_upper" 3 3 python /tmp/prof_team.py cfg4 0
 cap final_ncu_cfg5 "k_(rev0|fwd0)_team|k_upper" 3 3 python /tmp/prof_team.py cfg5 2000000
-cap final_ncu_solve "k_solve_stream" 3 1 python /tmp/prof_solve.py
+cap final_ncu_solve "k_solve_strip" 3 1 python /tmp/prof_solve.py
+SPINGP_SOLVE_STRIP=0 python tools/stream_time.py tile-kernel > gpurun_out/final_stream_tile_time.log 2>&1
 cap final_ncu_solve_partitioned "k_(fwdL|revL|tree)" 6 3 python /tmp/prof_solve.py
 SPINGP_SS_STAMPS=1 python tools/stream_stamps.py > gpurun_out/final_stream_stamps.log 2>&1
 ls -la gpurun_out
