@@ -134,40 +134,7 @@ bool ss_launch(spingp_ctx* ctx, int64_t n, const double* diag, const double* upp
     return true;
 }
 
-// 2-D tensor map of a strip-major view: `rows` chunks of `inner` doubles (row pitch = inner),
-// box = 32 rows x `box_inner` doubles.  The encoder comes from the driver (no libcuda link).
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-EncodeTiledFn tensor_map_encoder() {
-    static EncodeTiledFn fn = [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            p = nullptr;
-        return reinterpret_cast<EncodeTiledFn>(p);
-    }();
-    return fn;
-}
-bool strip_tensor_map(CUtensorMap* m, const double* base, long long inner, long long rows, int box_inner) {
-    EncodeTiledFn enc = tensor_map_encoder();
-    if (!enc || rows < 1) return false;
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(inner) * sizeof(double)};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), 32u};
-    const cuuint32_t estr[2] = {1u, 1u};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-bool strip_tma_enabled() {
-    const char* e = std::getenv("SPINGP_STRIP_TMA");
-    return !(e && std::strcmp(e, "0") == 0);
-}
-
-// The strip kernel (strip_solve.cuh): one lane per long chunk; the strips staged by 2-D tensor
-// copies (TMA) or, for misaligned arrays / SPINGP_STRIP_TMA=0, cooperative cp.async.
+// The strip kernel (strip_solve.cuh): one lane per long chunk, cooperative cp.async staging.
 template <int B, int NWARP, int MB>
 bool st_launch(spingp_ctx* ctx, int64_t n, const double* diag, const double* upper, const double* rhs, double* x,
                double* logdet) {
@@ -210,13 +177,6 @@ bool st_launch(spingp_ctx* ctx, int64_t n, const double* diag, const double* upp
     a.xsep = ctx->ws.take<double>(G * B);
     a.ckpt = ctx->ws.take<double>(GW * nsub * NCK * 32);
     a.tfac = ctx->ws.take<double>(GW * NF * 32);
-    // chunks that lie inside the matrix with their last upper block: the rows of the tensor maps
-    CUtensorMap mD{}, mU{}, mR{};
-    const long long rows = (n - 1) / Lc;
-    a.tma = (a.bulk && strip_tma_enabled() && strip_tensor_map(&mD, diag, Lc * B * B, rows, C::HD) &&
-             strip_tensor_map(&mU, upper, Lc * B * B, rows, C::HD) && strip_tensor_map(&mR, rhs, Lc * B, rows, C::HR))
-                ? 1
-                : 0;
     if (!ctx->d_ss_sync) {
         CUDA_OK(cudaMalloc(&ctx->d_ss_sync, 2 * sizeof(unsigned long long)));
         CUDA_OK(cudaMemsetAsync(ctx->d_ss_sync, 0, 2 * sizeof(unsigned long long), ctx->stream));
@@ -232,7 +192,7 @@ bool st_launch(spingp_ctx* ctx, int64_t n, const double* diag, const double* upp
         CUDA_OK(cudaMalloc(&a.stamps, G * 16 * sizeof(unsigned long long)));
         CUDA_OK(cudaMemsetAsync(a.stamps, 0, G * 16 * sizeof(unsigned long long), ctx->stream));
     }
-    void* args[] = {&a, &mD, &mU, &mR};
+    void* args[] = {&a};
     ctx->pre();
     CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(static_cast<unsigned>(G)), dim3(NT), args,
                                         C::SMEM_BYTES, ctx->stream));

@@ -101,7 +101,6 @@ struct SSArgs {
     double* xsep;     // [G][B] solution at every CTA's last block
     double* ckpt;     // [G * NW][Tmax][NK] carry checkpoints (S_P, W_P, r_P) per tile
     double* tfac;     // [G * NW][Tmax][NF][LPT] merge factors of every tile's tree
-    int tma;          // strip kernel: 1 = stage with 2-D tensor copies (the kernel's tensor maps are valid)
     long long Lc;     // strip kernel: blocks per lane (even)
     int nsub;         // strip kernel: sub-tiles per lane
     unsigned long long* sync;  // [0] arrivals (monotonic), [1] release word (monotonic)

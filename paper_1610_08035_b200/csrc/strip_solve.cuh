@@ -21,11 +21,13 @@
 //            The last sub-tile of sweep 1 is still in shared memory and is not re-read.
 #pragma once
 
-#include <cuda.h>  // CUtensorMap
-
 #include "stream_solve.cuh"
 
 namespace spingp_dev {
+
+// strip stride in shared memory: even (16-byte pieces) with an odd half, so that the 32
+// strips of a warp fall on distinct bank pairs within every group of 8 lanes
+constexpr int st_pad(int x) { return ((x / 2) & 1) ? x : x + 2; }
 
 template <int B, int NWARP, int MB_>
 struct STCfg {
@@ -36,17 +38,12 @@ struct STCfg {
     static constexpr int NR = Rec<B>::N;
     static constexpr int NF = Tree<B>::NF;
     static constexpr int NCK = 2 * BB + B;    // checkpoint: T, W, rc
-    // per-warp shared memory (doubles): the sub-tile in two halves of HB = MB / 2 blocks, each
-    // half strip-major and dense (the layout a 2-D TMA box of 32 rows lands in):
-    //   D half 0 | D half 1 | U half 0 | U half 1 | r half 0 | r half 1 | two mbarriers
-    static constexpr int HB = MB_ / 2;
-    static constexpr int HD = HB * BB;        // doubles per strip and half (diag, upper)
-    static constexpr int HR = HB * B;         // (rhs)
+    static constexpr int SD = st_pad(MB_ * BB);   // strip strides (doubles)
+    static constexpr int SR = st_pad(MB_ * B);
     static constexpr int W_D = 0;
-    static constexpr int W_U = 64 * HD;
-    static constexpr int W_R = 128 * HD;
-    static constexpr int W_BAR = 128 * HD + 64 * HR;
-    static constexpr int W_SIZE = W_BAR + 16;  // keeps every warp's buffers 128-byte aligned
+    static constexpr int W_U = 32 * SD;
+    static constexpr int W_R = 64 * SD;
+    static constexpr int W_SIZE = ss_even(64 * SD + 32 * SR);
     static constexpr int RSW = ss_even(NW);
     static constexpr int ESW = ss_even(NW + 1);
     static constexpr int OFF_WR = NW * W_SIZE;
@@ -56,11 +53,7 @@ struct STCfg {
     static constexpr int EST = ss_even(NT / 32 + 1);
     static constexpr int SMEM_DOUBLES = ss_even(OFF_TOP + NR * RST + B * EST);
     static constexpr size_t SMEM_BYTES = static_cast<size_t>(SMEM_DOUBLES) * 8;
-    static_assert(MB_ % 4 == 0, "half strips must be multiples of 16 bytes");
-    // block j of strip q
-    __host__ __device__ static constexpr int offD(int q, int j) { return W_D + (j / HB) * 32 * HD + q * HD + (j % HB) * BB; }
-    __host__ __device__ static constexpr int offU(int q, int j) { return W_U + (j / HB) * 32 * HD + q * HD + (j % HB) * BB; }
-    __host__ __device__ static constexpr int offR(int q, int j) { return W_R + (j / HB) * 32 * HR + q * HR + (j % HB) * B; }
+    static_assert(MB_ % 2 == 0, "strip pieces must be multiples of 16 bytes");
 };
 
 #ifndef SPINGP_HOST_EMU
@@ -72,69 +65,24 @@ SP_DEV void st_cp_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 SP_DEV void st_cp_wait_but_one() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 SP_DEV void st_cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-SP_DEV void st_tma_2d(void* dst, const void* tmap, int x, int y, void* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-        ::"r"(ss_smem(dst)), "l"(reinterpret_cast<unsigned long long>(tmap)), "r"(x), "r"(y), "r"(ss_smem(bar))
-        : "memory");
-}
 
-// The strips of lanes >= qin (the chunk across the end of the matrix and the ones past it:
-// identity padding D = I, U = 0, r = 0; or every strip when the arrays are misaligned),
-// half h of sub-tile s, element by element.
-template <class C, int B>
-SP_DEV void st_stage_ragged(const SSArgs& a, double* wm, long long wfl, int qin, int s, int h) {
-    constexpr int BB = B * B, MB = C::MB, HB = C::HB, HD = C::HD, HR = C::HR;
+// Stage blocks [j0, j0 + NB) of sub-tile s of the warp's 32 strips.  wfl = global index of the
+// warp's lane 0; strip q belongs to lane q and starts at block (wfl + q) Lc + s MB.  When the
+// whole piece lies inside the matrix (all but the last warp with data) every 16-byte piece is
+// a cp.async with compile-time piece -> (strip, offset) arithmetic and no bounds checks;
+// otherwise strip by strip: inside -> cp.async, past the end -> identity padding (D = I, U = 0,
+// r = 0), the strip across the end (or misaligned arrays) element by element.
+template <class C, int B, int NB>
+SP_DEV void st_stage(const SSArgs& a, double* wm, long long wfl, int qin, int s, int j0) {
+    constexpr int BB = B * B, MB = C::MB;
+    constexpr int nD = NB * BB / 2, nR = NB * B / 2;  // 16-byte pieces per strip
+    static_assert(NB % 2 == 0, "16-byte pieces");
     const int lane = threadIdx.x & 31;
-    const long long gb0 = wfl * a.Lc + static_cast<long long>(s) * MB + h * HB;
-    const long long nd = a.n * BB, nu = (a.n - 1) * BB, nr = a.n * B;
-    const int nq = 32 - qin;
-    double* wD = wm + C::W_D + h * 32 * HD;
-    double* wU = wm + C::W_U + h * 32 * HD;
-    double* wR = wm + C::W_R + h * 32 * HR;
-    for (int p = lane; p < nq * HD; p += 32) {
-        const int q = qin + p / HD, e = p % HD;
-        const long long gi = (gb0 + q * a.Lc) * BB + e;
-        wD[q * HD + e] = gi < nd ? a.diag[gi] : (((e % BB) % (B + 1) == 0) ? 1.0 : 0.0);
-        wU[q * HD + e] = gi < nu ? a.up[gi] : 0.0;
-    }
-    for (int p = lane; p < nq * HR; p += 32) {
-        const int q = qin + p / HR, e = p % HR;
-        const long long gi = (gb0 + q * a.Lc) * B + e;
-        wR[q * HR + e] = (gi < nr && a.rhs) ? a.rhs[gi] : 0.0;
-    }
-}
-
-// Stage half h of sub-tile s of the warp's 32 strips.  wfl = global index of the warp's lane
-// 0; strip q belongs to lane q and starts at block (wfl + q) Lc + s MB.
-//   TMA:      three 2-D tensor copies (diag, upper, rhs viewed as [chunk][Lc b²] arrays; box =
-//             32 chunks x the half's doubles) onto the mbarrier; rows past the last complete
-//             chunk are zero-filled by the hardware and then fixed up by st_stage_ragged
-//             after the wait (the caller);
-//   cp.async: consecutive lanes copy consecutive 16-byte pieces of one strip; lanes >= qin
-//             element by element here.
-template <class C, int B>
-SP_DEV void st_stage(const SSArgs& a, const void* mD, const void* mU, const void* mR, double* wm, long long wfl,
-                     int qin, int s, int h, void* bar) {
-    constexpr int BB = B * B, MB = C::MB, HB = C::HB, HD = C::HD, HR = C::HR;
-    constexpr int nD = HD / 2, nR = HR / 2;  // 16-byte pieces per strip
-    const int lane = threadIdx.x & 31;
-    double* wD = wm + C::W_D + h * 32 * HD;
-    double* wU = wm + C::W_U + h * 32 * HD;
-    double* wR = wm + C::W_R + h * 32 * HR;
-    if (a.tma) {
-        if (lane == 0) {
-            ss_fence_async();
-            ss_bar_expect(bar, 32u * (2 * HD + HR) * 8u);
-            const int blk = s * MB + h * HB, row = static_cast<int>(wfl);
-            st_tma_2d(wD, mD, blk * BB, row, bar);
-            st_tma_2d(wU, mU, blk * BB, row, bar);
-            st_tma_2d(wR, mR, blk * B, row, bar);
-        }
-        return;
-    }
-    if (qin > 0) {
-        const long long gb0 = wfl * a.Lc + static_cast<long long>(s) * MB + h * HB;  // strip 0's first block
+    const long long gb0 = wfl * a.Lc + static_cast<long long>(s) * MB + j0;  // strip 0's first block
+    double* wD = wm + C::W_D + j0 * BB;
+    double* wU = wm + C::W_U + j0 * BB;
+    double* wR = wm + C::W_R + j0 * B;
+    if (qin > 0) {  // strips [0, qin): whole chunks inside the matrix, aligned arrays
         const double* dbase = a.diag + gb0 * BB;
         const double* ubase = a.up + gb0 * BB;
         const double* rbase = a.rhs + gb0 * B;
@@ -143,62 +91,69 @@ TR_UNROLL
         for (int it = 0; it < (32 * nD + 31) / 32; ++it) {
             const int p = it * 32 + lane, q = p / nD, wi = p - q * nD;
             if (q < qin) {
-                st_cp16(wD + q * HD + 2 * wi, dbase + q * strideD + 2 * wi);
-                st_cp16(wU + q * HD + 2 * wi, ubase + q * strideD + 2 * wi);
+                st_cp16(wD + q * C::SD + 2 * wi, dbase + q * strideD + 2 * wi);
+                st_cp16(wU + q * C::SD + 2 * wi, ubase + q * strideD + 2 * wi);
             }
         }
 TR_UNROLL
         for (int it = 0; it < (32 * nR + 31) / 32; ++it) {
             const int p = it * 32 + lane, q = p / nR, wi = p - q * nR;
-            if (q < qin) st_cp16(wR + q * HR + 2 * wi, rbase + q * strideR + 2 * wi);
+            if (q < qin) st_cp16(wR + q * C::SR + 2 * wi, rbase + q * strideR + 2 * wi);
         }
     }
-    if (qin < 32) st_stage_ragged<C, B>(a, wm, wfl, qin, s, h);
+    if (qin == 32) return;
+    // the chunk across the end of the matrix and the ones past it (identity padding: D = I,
+    // U = 0, r = 0), or misaligned arrays: element by element
+    const long long nd = a.n * BB, nu = (a.n - 1) * BB, nr = a.n * B;
+    const int nq = 32 - qin;
+    for (int p = lane; p < nq * NB * BB; p += 32) {
+        const int q = qin + p / (NB * BB), e = p % (NB * BB);
+        const long long gi = (gb0 + q * a.Lc) * BB + e;
+        wD[q * C::SD + e] = gi < nd ? a.diag[gi] : (((e % BB) % (B + 1) == 0) ? 1.0 : 0.0);
+        wU[q * C::SD + e] = gi < nu ? a.up[gi] : 0.0;
+    }
+    for (int p = lane; p < nq * NB * B; p += 32) {
+        const int q = qin + p / (NB * B), e = p % (NB * B);
+        const long long gi = (gb0 + q * a.Lc) * B + e;
+        wR[q * C::SR + e] = (gi < nr && a.rhs) ? a.rhs[gi] : 0.0;
+    }
 }
 
-// Store the sub-tile's solution (the rhs slots of the 32 strips, both halves) to x.
+// Store the sub-tile's solution (the rhs slots of the 32 strips) to x.
 template <class C, int B>
 SP_DEV void st_store_x(const SSArgs& a, const double* wm, long long wfl, int s) {
-    constexpr int MB = C::MB, HB = C::HB, HR = C::HR;
-    constexpr int nR = HR / 2;  // 16-byte pieces per strip and half
+    constexpr int MB = C::MB;
+    constexpr int nR = MB * B / 2;
     const int lane = threadIdx.x & 31;
     const long long gb0 = wfl * a.Lc + static_cast<long long>(s) * MB;
     const long long last = gb0 + 31 * a.Lc + MB;
     if ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0 && last <= a.n) {
+        double* xbase = a.x + gb0 * B;
         const int strideR = static_cast<int>(a.Lc) * B;
 TR_UNROLL
-        for (int h = 0; h < 2; ++h) {
-            double* xbase = a.x + (gb0 + h * HB) * B;
-            const double* wR = wm + C::W_R + h * 32 * HR;
-TR_UNROLL
-            for (int it = 0; it < (32 * nR + 31) / 32; ++it) {
-                const int p = it * 32 + lane, q = p / nR, wi = p - q * nR;
-                if (32 * nR % 32 == 0 || p < 32 * nR) {
-                    const double* src = wR + q * HR + 2 * wi;
-                    __stcs(reinterpret_cast<double2*>(xbase + q * strideR + 2 * wi), make_double2(src[0], src[1]));
-                }
+        for (int it = 0; it < (32 * nR + 31) / 32; ++it) {
+            const int p = it * 32 + lane, q = p / nR, wi = p - q * nR;
+            if (32 * nR % 32 == 0 || p < 32 * nR) {
+                const double* src = wm + C::W_R + q * C::SR + 2 * wi;
+                __stcs(reinterpret_cast<double2*>(xbase + q * strideR + 2 * wi), make_double2(src[0], src[1]));
             }
         }
         return;
     }
     const long long nr = a.n * B;
     for (int p = lane; p < 32 * MB * B; p += 32) {
-        const int q = p / (MB * B), e = p - q * (MB * B), j = e / B;
+        const int q = p / (MB * B), e = p - q * (MB * B);
         const long long gi = (gb0 + q * a.Lc) * B + e;
-        if (gi < nr) a.x[gi] = wm[C::offR(q, j) + e % B];
+        if (gi < nr) a.x[gi] = wm[C::W_R + q * C::SR + e];
     }
 }
 
-// mD, mU, mR: 2-D tensor maps of diag / upper / rhs as [complete chunks][Lc b² (or Lc b)]
-// arrays of doubles with a 32-row x half-strip box (a.tma; otherwise unused).
 template <class C, int B>
-__global__ void __launch_bounds__(C::NT, 1)
-    k_solve_strip(SSArgs a, const __grid_constant__ CUtensorMap mD, const __grid_constant__ CUtensorMap mU,
-                  const __grid_constant__ CUtensorMap mR) {
-    extern __shared__ __align__(128) double2 st_sm2[];
+__global__ void __launch_bounds__(C::NT, 1) k_solve_strip(SSArgs a) {
+    extern __shared__ double2 st_sm2[];
     double* sm = reinterpret_cast<double*>(st_sm2);
     constexpr int BB = B * B;
-    constexpr int NR = C::NR, NF = C::NF, NCK = C::NCK, MB = C::MB, HB = C::HB;
+    constexpr int NR = C::NR, NF = C::NF, NCK = C::NCK, MB = C::MB;
     using RC = Rec<B>;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int cta = blockIdx.x;
@@ -206,39 +161,17 @@ __global__ void __launch_bounds__(C::NT, 1)
     const long long g0 = (wfl + lane) * a.Lc;  // first block of this lane's chunk
     const int nsub = a.nsub;  // Lc = nsub * MB: every sub-tile is full
     double* wm = sm + w * C::W_SIZE;
+    double* sD = wm + C::W_D + lane * C::SD;
+    double* sU = wm + C::W_U + lane * C::SD;
+    double* sR = wm + C::W_R + lane * C::SR;
     double* WR = sm + C::OFF_WR;
     double* WE = sm + C::OFF_WE;
     double* ckw = a.ckpt + gwarp * nsub * (NCK * 32) + lane;
     double* tfw = a.tfac + gwarp * (NF * 32) + lane;
     const bool want_x = a.x != nullptr;
-    // block j of this lane's strip
-    auto pD = [&](int j) { return wm + C::offD(lane, j); };
-    auto pU = [&](int j) { return wm + C::offU(lane, j); };
-    auto pR = [&](int j) { return wm + C::offR(lane, j); };
-    void* bar[2] = {wm + C::W_BAR, wm + C::W_BAR + 1};
-    unsigned ph[2] = {0u, 0u};
-    if (lane == 0) {
-        ss_bar_init(bar[0], 1);
-        ss_bar_init(bar[1], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncwarp();
     const bool empty = wfl * a.Lc >= a.n;  // a warp past the end of the matrix: neutral records
     // lanes of this warp whose whole chunk (and its last upper block) lies inside the matrix
     const int qin = a.bulk ? static_cast<int>(max(0LL, min(32LL, (a.n - 1) / a.Lc - wfl))) : 0;
-    // wait for half h of a staged sub-tile (and fix up what the TMA zero-filled)
-    auto stage_wait = [&](int s, int h, bool but_one) {
-        if (a.tma) {
-            ss_bar_wait(bar[h], ph[h]);
-            ph[h] ^= 1u;
-            if (qin < 32) st_stage_ragged<C, B>(a, wm, wfl, qin, s, h);
-        } else if (but_one) {
-            st_cp_wait_but_one();
-        } else {
-            st_cp_wait();
-        }
-        __syncwarp();
-    };
 
     // the block that couples this chunk to its left separator (the previous lane's last block)
     double Up0[BB];
@@ -264,13 +197,14 @@ TR_UNROLL
             for (int j = 0; j < B; ++j) es.W[i * B + j] = Up0[j * B + i];
         // sub-tiles are staged in halves of MB / 2 blocks, one half ahead of the elimination
         // (the half being filled was eliminated one step earlier)
-        if (!empty) st_stage<C, B>(a, &mD, &mU, &mR, wm, wfl, qin, 0, 0, bar[0]);
+        constexpr int HB = MB / 2;
+        if (!empty) st_stage<C, B, HB>(a, wm, wfl, qin, 0, 0);
         st_cp_commit();
 #pragma unroll 1
         for (int sh = 0; sh < 2 * nsub && !empty; ++sh) {
             const int s = sh >> 1, h = sh & 1;
             __syncwarp();
-            if (sh + 1 < 2 * nsub) st_stage<C, B>(a, &mD, &mU, &mR, wm, wfl, qin, (sh + 1) >> 1, (sh + 1) & 1, bar[(sh + 1) & 1]);
+            if (sh + 1 < 2 * nsub) st_stage<C, B, HB>(a, wm, wfl, qin, (sh + 1) >> 1, ((sh + 1) & 1) * HB);
             st_cp_commit();
             if (want_x && s > 0 && h == 0) {  // the state at the sub-tile's start, for sweep 2
                 double* ck = ckw + static_cast<long long>(s) * (NCK * 32);
@@ -282,17 +216,19 @@ TR_UNROLL
                 for (int i = 0; i < B; ++i) ck[(2 * BB + i) * 32] = es.rc[i];
             }
             if (sh == 6) ss_stamp(a, 7);
-            stage_wait(s, h, true);
+            st_cp_wait_but_one();
+            __syncwarp();
             if (sh == 6) ss_stamp(a, 8);
             const int nel = sh == 2 * nsub - 1 ? HB - 1 : HB;
 #pragma unroll 1
-            for (int j = 0; j < nel; ++j) ss_elim_step<B>(es, pD(h * HB + j), pU(h * HB + j), pR(h * HB + j));
+            for (int j = 0; j < nel; ++j)
+                ss_elim_step<B>(es, sD + (h * HB + j) * BB, sU + (h * HB + j) * BB, sR + (h * HB + j) * B);
             if (sh == 6) ss_stamp(a, 9);
             if (sh == 7) ss_stamp(a, 10);
         }
         // the chunk's record: its last block is the separator
-        const double* Dp = pD(MB - 1);
-        const double* rp = pR(MB - 1);
+        const double* Dp = sD + (MB - 1) * BB;
+        const double* rp = sR + (MB - 1) * B;
 TR_UNROLL
         for (int i = 0; i < BB; ++i) rec[RC::RDIAG + i] = empty ? ((i % (B + 1) == 0) ? 1.0 : 0.0) : Dp[i] - es.T[i];
 TR_UNROLL
@@ -419,11 +355,9 @@ TR_UNROLL
 #pragma unroll 1
     for (int s = nsub - 1; s >= 0 && !empty; --s) {
         double T[BB], rc[B];
-        const bool restage = s < nsub - 1;  // (the last sub-tile of sweep 1 is still staged)
-        if (restage) {
+        if (s < nsub - 1) {  // (the last sub-tile of sweep 1 is still staged)
             __syncwarp();
-            st_stage<C, B>(a, &mD, &mU, &mR, wm, wfl, qin, s, 0, bar[0]);
-            st_stage<C, B>(a, &mD, &mU, &mR, wm, wfl, qin, s, 1, bar[1]);
+            st_stage<C, B, MB>(a, wm, wfl, qin, s, 0);
         }
         if (s > 0) {
             const double* ck = ckw + static_cast<long long>(s) * (NCK * 32);
@@ -442,17 +376,15 @@ TR_UNROLL
             mtv<B>(rc, Up0, xl);
         }
         if (s == 2) ss_stamp(a, 11);
-        if (restage) {
-            stage_wait(s, 0, false);
-            if (a.tma) stage_wait(s, 1, false);
-        }
+        st_cp_wait();
+        __syncwarp();
         if (s == 2) ss_stamp(a, 12);
         const int nel = s == nsub - 1 ? MB - 1 : MB;
 #pragma unroll 1
         for (int j = 0; j < nel; ++j) {
-            double* Dp = pD(j);
-            double* Up = pU(j);
-            double* rp = pR(j);
+            double* Dp = sD + j * BB;
+            double* Up = sU + j * BB;
+            double* rp = sR + j * B;
             double S[BB], L[BB], U[BB], r[B], z[B], X[BB];
 TR_UNROLL
             for (int i = 0; i < BB; ++i) S[i] = Dp[i] - T[i];
@@ -473,16 +405,14 @@ TR_UNROLL
 TR_UNROLL
             for (int i = 0; i < B; ++i) rp[i] = z[i];
         }
-        if (s == nsub - 1) {
-            double* rp = pR(MB - 1);
+        if (s == nsub - 1)
 TR_UNROLL
-            for (int i = 0; i < B; ++i) rp[i] = xn[i];  // the separator's own x
-        }
+            for (int i = 0; i < B; ++i) sR[(MB - 1) * B + i] = xn[i];  // the separator's own x
 #pragma unroll 1
         for (int j = nel - 1; j >= 0; --j) {
-            const double* Lq = pD(j);
-            const double* Xq = pU(j);
-            double* zq = pR(j);
+            const double* Lq = sD + j * BB;
+            const double* Xq = sU + j * BB;
+            double* zq = sR + j * B;
             double L[BB], av[B], t1[B], xj[B];
 TR_UNROLL
             for (int i = 0; i < BB; ++i) L[i] = Lq[i];
