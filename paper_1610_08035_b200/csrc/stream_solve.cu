@@ -173,6 +173,9 @@ bool st_launch(spingp_ctx* ctx, int64_t n, const double* diag, const double* upp
     a.nsub = nsub;
     auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
     a.bulk = (rhs && aligned(diag) && aligned(upper) && aligned(rhs)) ? 1 : 0;
+    a.l2mode = stream_l2mode();
+    if (const char* e = std::getenv("SPINGP_SS_L2KEEP")) a.l2keep = std::atoi(e);
+    else a.l2keep = 3;
     a.crec = ctx->ws.take<double>(NR * G);
     a.xsep = ctx->ws.take<double>(G * B);
     a.ckpt = ctx->ws.take<double>(GW * nsub * NCK * 32);

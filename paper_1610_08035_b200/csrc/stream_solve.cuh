@@ -97,6 +97,7 @@ struct SSArgs {
     int Tmax;         // max tiles per warp
     int bulk;         // 1: pointers are 16-byte aligned (bulk copies), 0: plain loads
     int l2mode;       // sweep-1 loads: 0 normal, 1 evict_last (tiles re-read by sweep 2)
+    int l2keep;       // strip kernel, l2mode 1: sub-tiles (from the end) loaded evict_last in sweep 1
     double* crec;     // [NR][G] CTA records, component-major
     double* xsep;     // [G][B] solution at every CTA's last block
     double* ckpt;     // [G * NW][Tmax][NK] carry checkpoints (S_P, W_P, r_P) per tile

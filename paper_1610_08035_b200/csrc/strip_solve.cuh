@@ -57,9 +57,10 @@ struct STCfg {
 };
 
 #ifndef SPINGP_HOST_EMU
-SP_DEV void st_cp16(double* dst, const double* src) {
+SP_DEV void st_cp16(double* dst, const double* src, unsigned long long policy) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "l"(policy)
+                 : "memory");
 }
 SP_DEV void st_cp_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -73,7 +74,7 @@ SP_DEV void st_cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory
 // otherwise strip by strip: inside -> cp.async, past the end -> identity padding (D = I, U = 0,
 // r = 0), the strip across the end (or misaligned arrays) element by element.
 template <class C, int B, int NB>
-SP_DEV void st_stage(const SSArgs& a, double* wm, long long wfl, int qin, int s, int j0) {
+SP_DEV void st_stage(const SSArgs& a, double* wm, long long wfl, int qin, int s, int j0, unsigned long long policy) {
     constexpr int BB = B * B, MB = C::MB;
     constexpr int nD = NB * BB / 2, nR = NB * B / 2;  // 16-byte pieces per strip
     static_assert(NB % 2 == 0, "16-byte pieces");
@@ -91,21 +92,23 @@ TR_UNROLL
         for (int it = 0; it < (32 * nD + 31) / 32; ++it) {
             const int p = it * 32 + lane, q = p / nD, wi = p - q * nD;
             if (q < qin) {
-                st_cp16(wD + q * C::SD + 2 * wi, dbase + q * strideD + 2 * wi);
-                st_cp16(wU + q * C::SD + 2 * wi, ubase + q * strideD + 2 * wi);
+                st_cp16(wD + q * C::SD + 2 * wi, dbase + q * strideD + 2 * wi, policy);
+                st_cp16(wU + q * C::SD + 2 * wi, ubase + q * strideD + 2 * wi, policy);
             }
         }
 TR_UNROLL
         for (int it = 0; it < (32 * nR + 31) / 32; ++it) {
             const int p = it * 32 + lane, q = p / nR, wi = p - q * nR;
-            if (q < qin) st_cp16(wR + q * C::SR + 2 * wi, rbase + q * strideR + 2 * wi);
+            if (q < qin) st_cp16(wR + q * C::SR + 2 * wi, rbase + q * strideR + 2 * wi, policy);
         }
     }
     if (qin == 32) return;
-    // the chunk across the end of the matrix and the ones past it (identity padding: D = I,
-    // U = 0, r = 0), or misaligned arrays: element by element
+    // the chunk across the end of the matrix (identity padding past it: D = I, U = 0, r = 0),
+    // or every chunk when the arrays are misaligned: element by element.  Chunks that start
+    // past the end are never read (their lanes sit the sweeps out).
     const long long nd = a.n * BB, nu = (a.n - 1) * BB, nr = a.n * B;
-    const int nq = 32 - qin;
+    const long long own = (a.n + a.Lc - 1) / a.Lc - wfl;  // lanes of this warp that own a block
+    const int nq = static_cast<int>(max(0LL, min(32LL, own))) - qin;
     for (int p = lane; p < nq * NB * BB; p += 32) {
         const int q = qin + p / (NB * BB), e = p % (NB * BB);
         const long long gi = (gb0 + q * a.Lc) * BB + e;
@@ -170,6 +173,13 @@ __global__ void __launch_bounds__(C::NT, 1) k_solve_strip(SSArgs a) {
     double* tfw = a.tfac + gwarp * (NF * 32) + lane;
     const bool want_x = a.x != nullptr;
     const bool empty = wfl * a.Lc >= a.n;  // a warp past the end of the matrix: neutral records
+    const bool off = g0 >= a.n;            // a lane whose chunk starts past the end: likewise
+    // L2 hints (a.l2mode = 1): sweep 2 re-reads the sub-tiles in reverse order, so the last few
+    // of sweep 1 are worth keeping in L2, the first ones are not, and sweep 2's own loads are dead
+    const unsigned long long pol_n = ss_policy_normal();
+    const unsigned long long pol_first = a.l2mode ? ss_policy_first() : pol_n;
+    const unsigned long long pol_last = a.l2mode ? ss_policy_last() : pol_n;
+    const int keep_from = nsub - 1 - a.l2keep;  // sub-tiles >= this one: evict_last in sweep 1
     // lanes of this warp whose whole chunk (and its last upper block) lies inside the matrix
     const int qin = a.bulk ? static_cast<int>(max(0LL, min(32LL, (a.n - 1) / a.Lc - wfl))) : 0;
 
@@ -198,13 +208,15 @@ TR_UNROLL
         // sub-tiles are staged in halves of MB / 2 blocks, one half ahead of the elimination
         // (the half being filled was eliminated one step earlier)
         constexpr int HB = MB / 2;
-        if (!empty) st_stage<C, B, HB>(a, wm, wfl, qin, 0, 0);
+        if (!empty) st_stage<C, B, HB>(a, wm, wfl, qin, 0, 0, 0 >= keep_from ? pol_last : pol_first);
         st_cp_commit();
 #pragma unroll 1
         for (int sh = 0; sh < 2 * nsub && !empty; ++sh) {
             const int s = sh >> 1, h = sh & 1;
             __syncwarp();
-            if (sh + 1 < 2 * nsub) st_stage<C, B, HB>(a, wm, wfl, qin, (sh + 1) >> 1, ((sh + 1) & 1) * HB);
+            if (sh + 1 < 2 * nsub)
+                st_stage<C, B, HB>(a, wm, wfl, qin, (sh + 1) >> 1, ((sh + 1) & 1) * HB,
+                                   ((sh + 1) >> 1) >= keep_from ? pol_last : pol_first);
             st_cp_commit();
             if (want_x && s > 0 && h == 0) {  // the state at the sub-tile's start, for sweep 2
                 double* ck = ckw + static_cast<long long>(s) * (NCK * 32);
@@ -221,7 +233,7 @@ TR_UNROLL
             if (sh == 6) ss_stamp(a, 8);
             const int nel = sh == 2 * nsub - 1 ? HB - 1 : HB;
 #pragma unroll 1
-            for (int j = 0; j < nel; ++j)
+            for (int j = 0; j < nel && !off; ++j)
                 ss_elim_step<B>(es, sD + (h * HB + j) * BB, sU + (h * HB + j) * BB, sR + (h * HB + j) * B);
             if (sh == 6) ss_stamp(a, 9);
             if (sh == 7) ss_stamp(a, 10);
@@ -230,7 +242,7 @@ TR_UNROLL
         const double* Dp = sD + (MB - 1) * BB;
         const double* rp = sR + (MB - 1) * B;
 TR_UNROLL
-        for (int i = 0; i < BB; ++i) rec[RC::RDIAG + i] = empty ? ((i % (B + 1) == 0) ? 1.0 : 0.0) : Dp[i] - es.T[i];
+        for (int i = 0; i < BB; ++i) rec[RC::RDIAG + i] = (empty || off) ? ((i % (B + 1) == 0) ? 1.0 : 0.0) : Dp[i] - es.T[i];
 TR_UNROLL
         for (int i = 0; i < BB; ++i) rec[RC::LDIAG + i] = es.accLL[i];
 TR_UNROLL
@@ -238,7 +250,7 @@ TR_UNROLL
 TR_UNROLL
             for (int j = 0; j < B; ++j) rec[RC::LR + i * B + j] = es.W[j * B + i];
 TR_UNROLL
-        for (int i = 0; i < B; ++i) rec[RC::RRHS + i] = empty ? 0.0 : rp[i] - es.rc[i];
+        for (int i = 0; i < B; ++i) rec[RC::RRHS + i] = (empty || off) ? 0.0 : rp[i] - es.rc[i];
 TR_UNROLL
         for (int i = 0; i < B; ++i) rec[RC::LRHS + i] = es.accrL[i];
         rec[RC::LOGDET] = es.piv.logdet();
@@ -357,7 +369,7 @@ TR_UNROLL
         double T[BB], rc[B];
         if (s < nsub - 1) {  // (the last sub-tile of sweep 1 is still staged)
             __syncwarp();
-            st_stage<C, B, MB>(a, wm, wfl, qin, s, 0);
+            st_stage<C, B, MB>(a, wm, wfl, qin, s, 0, pol_first);
         }
         if (s > 0) {
             const double* ck = ckw + static_cast<long long>(s) * (NCK * 32);
@@ -379,7 +391,7 @@ TR_UNROLL
         st_cp_wait();
         __syncwarp();
         if (s == 2) ss_stamp(a, 12);
-        const int nel = s == nsub - 1 ? MB - 1 : MB;
+        const int nel = off ? 0 : (s == nsub - 1 ? MB - 1 : MB);
 #pragma unroll 1
         for (int j = 0; j < nel; ++j) {
             double* Dp = sD + j * BB;
