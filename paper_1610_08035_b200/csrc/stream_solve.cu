@@ -218,6 +218,16 @@ bool strip_enabled() {
 bool stream_solve(spingp_ctx* ctx, int64_t n, int b, const double* diag, const double* upper, const double* rhs,
                   double* x, double* logdet) {
     if (!stream_enabled() || n < 2 || !upper) return false;
+    {  // both kernels are cooperative launches (a grid-wide barrier between the sweeps)
+        static int coop_dev[64] = {};
+        int& coop = coop_dev[ctx->device & 63];
+        if (!coop) {
+            int v = 0;
+            CUDA_OK(cudaDeviceGetAttribute(&v, cudaDevAttrCooperativeLaunch, ctx->device));
+            coop = v ? 1 : -1;
+        }
+        if (coop < 0) return false;
+    }
     if (strip_enabled()) {  // one lane per long chunk (strip_solve.cuh); else contiguous tiles
         bool done = false;
         switch (b) {
