@@ -126,3 +126,20 @@ def test_stream_solve_device_pointers_any_alignment(ctx, kernel):
         ctx.btd_cr_solve_device(n, b, d.data_ptr(), u.data_ptr(), r.data_ptr(), 1, x.data_ptr(), ld.data_ptr())
         ctx.status()  # synchronises the context stream, raises on a device-side failure
         assert rel(x.cpu().numpy(), xo) < 1e-12 and abs(float(ld.item()) - ldo) <= 1e-12 * abs(ldo)
+
+
+@pytest.mark.parametrize("b", [3, 6])
+@pytest.mark.parametrize("bad", [0, 13, 14, 3333, 4800])
+def test_partitioned_kernels_report_the_failing_block(ctx, b, bad):
+    """The same contract on the partitioned kernels: cr_solve with several
+    right-hand sides and selective_inverse."""
+    n = 4801
+    diag, upper, _ = system(n, b, 31)
+    rhs = np.random.default_rng(4).standard_normal((n * b, 2))
+    diag[bad] = -np.eye(b)
+    with pytest.raises(P.NotPositiveDefinite) as e:
+        ctx.btd_cr_solve(diag, upper, rhs)
+    assert e.value.block_index() == bad
+    with pytest.raises(P.NotPositiveDefinite) as e:
+        ctx.btd_selinv(diag, upper)
+    assert e.value.block_index() == bad
