@@ -86,6 +86,11 @@ def measure(n=1_000_000, b=3, steps=20, device=0, check=True):
            "kernel": "k_solve_strip" if launches == 1 else "k_fwdL / k_tree_* / k_revL",
            "partitioned_ms": t_part, "partitioned_frac": bytes_ / (t_part * 1e-3) / 1e9 / peak,
            "data": "random SPD blocks (seeded), L2 flushed before each call"}
+    try:  # DRAM bytes per solve from the committed ncu capture (profiles/ncu_traffic.json)
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "ncu_traffic.json")) as f:
+            out["traffic"] = json.load(f).get("solve_operator", {}).get(out["kernel"])
+    except (OSError, ValueError):
+        out["traffic"] = None
     ctx.close()
     return out
 
