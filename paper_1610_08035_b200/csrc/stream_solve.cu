@@ -50,10 +50,14 @@ void ss_print_stamps(spingp_ctx* ctx, unsigned long long* d, int G) {
     CUDA_OK(cudaFree(d));
     unsigned long long t0 = ~0ULL;
     for (int g = 0; g < G; ++g) t0 = std::min(t0, h[g * 16]);
+    // 0-6: the phases common to both kernels; 7-15: one sub-tile / tile of each sweep (strip
+    // kernel: half-tile 6 of sweep 1 before / after its wait, after its elimination, after the
+    // next half; sub-tile 2 of sweep 2 before / after its wait, solved, stored.  tile kernel:
+    // tile 2 of sweep 1 start / staged / eliminated / tree up; sweep 2 factors loaded / tree
+    // down / staged / solved / stored)
     static const char* names[16] = {"start", "sweep 1 (warp 0)", "CTA record out", "top: all arrived", "top: released",
-                                    "release seen", "end (warp 0)", "s1 t2: start", "s1 t2: tile in", "s1 t2: eliminated",
-                                    "s1 t2: tree up", "s2 t2: F loaded", "s2 t2: tree down", "s2 t2: tile in",
-                                    "s2 t2: solved", "s2 t2: stored"};
+                                    "release seen", "end (warp 0)", "detail 7", "detail 8", "detail 9", "detail 10",
+                                    "detail 11", "detail 12", "detail 13", "detail 14", "detail 15"};
     for (int k = 0; k < 16; ++k) {
         std::vector<double> v;
         for (int g = 0; g < G; ++g)
