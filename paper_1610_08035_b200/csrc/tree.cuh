@@ -401,8 +401,18 @@ SP_DEV void tree_forward_rounds(double* R, int RS, const TreeArgs& a, const Tree
         const int n = tree_width(t.cnt, j);
         TreeFwdScratch<B> sc;
         tree_fwd_compute<B>(R, RS, n, threadIdx.x, sc);
-        if (!sc.ok && a.status)
-            report(a.status, tree_point(a, t, t.k0 + min(t.cnt, (2 * threadIdx.x + 1) << j) - 1), ST_NOT_PD);
+        if (!sc.ok && a.status) {
+            // the origin of the failure if the merged pivot A.RR + B.LL is finite, else the echo of
+            // an earlier one (a NaN child record): reported at a lower priority
+            const int k2 = 2 * static_cast<int>(threadIdx.x);
+            double acc = 0.0;
+TR_UNROLL
+            for (int i = 0; i < B * B; ++i)
+                acc += R[(Rec<B>::RDIAG + i) * RS + k2] + R[(Rec<B>::LDIAG + i) * RS + k2 + 1];
+            const long long idx = tree_point(a, t, t.k0 + min(t.cnt, (k2 + 1) << j) - 1);
+            if (isfinite(acc)) report(a.status, idx, ST_NOT_PD);
+            else report_echo(a.status, idx, ST_NOT_PD);
+        }
         __syncthreads();
         tree_fwd_store<B>(R, RS, n, threadIdx.x, sc);
         __syncthreads();
