@@ -1,6 +1,8 @@
 // stream_solve.cuh — cr_solve of a materialised SymBTD as
 // ONE persistent kernel in which every WARP streams its own contiguous run of blocks
-// through shared memory, tile by tile.
+// through shared memory, tile by tile.  (The tile kernel: SPINGP_SOLVE_STRIP=0 and systems
+// too short for strip_solve.cuh, which shares this file's elimination step, trees, top
+// system and barrier.)
 //
 // Why.  The solve operator is HBM-bound (SURVEY.md §8(d) figure 1: B_solve = 8(2b²+2b)
 // bytes per block row).  The thread-per-chunk kernels (btd_ops.cuh) move 2.9x that: every
@@ -16,12 +18,10 @@
 //              upper, rhs) by cp.async.bulk into the warp's own buffer.  Lane l owns
 //              blocks [l M, (l+1) M): M - 1 interior blocks, eliminated in order against
 //              the previous lane's last block (left spike) and its own last block, as
-//              engine.cuh's elim_block (same record, Rec<B>).  With KEEP the factor is
-//              written IN PLACE over the inputs as G = S^{-1}U, V = S^{-1}W, h = S^{-1}r
-//              (2b²+b doubles per block, the size of the inputs).
+//              engine.cuh's elim_block (same record, Rec<B>).  Sweep 1 only reads the tile.
 //   warp tree  the 32 lane records are merged pairwise with warp shuffles (5 rounds, no
 //              barrier, no shared memory); the merge factor of a pair is shuffled back
-//              to the lane whose record was consumed and stays in its registers.
+//              to the lane whose record was consumed, which stores it for sweep 2.
 //   carry      a warp owns a contiguous run of tiles.  The record reduced so far (left
 //              separator Z = the block before the run, right = the previous tile's last
 //              block P) is carried in lane 0, which eliminates P as one more interior
@@ -41,7 +41,8 @@
 // at b = 3, M = 5, mostly L2-resident until sweep 2 reads them back in reverse order);
 // sweep 2 re-reads what L2 lost and writes x.
 // A "group" is LPT = 32, 16 or 8 lanes of a warp with their own tile buffer and run: fewer
-// lanes per tile means a shallower tree for the same blocks per lane.
+// lanes per tile means a shallower tree for the same blocks per lane (measured slower than
+// 32 lanes: the groups of a warp drift apart; profiles/r02_stream_solve.md).
 #pragma once
 
 #include "tree.cuh"
