@@ -21,9 +21,12 @@
 #ifndef SP_SS3_LPT
 #define SP_SS3_LPT 32
 #endif
-// strip kernel, b = 3: blocks per lane and sub-tile
+// strip kernel, b = 3: blocks per lane and sub-tile, warps per CTA
 #ifndef SP_ST3_MB
 #define SP_ST3_MB 4
+#endif
+#ifndef SP_ST3_NW
+#define SP_ST3_NW 8
 #endif
 
 namespace spingp_host {
@@ -237,7 +240,7 @@ bool stream_solve(spingp_ctx* ctx, int64_t n, int b, const double* diag, const d
         switch (b) {
             case 1: done = st_launch<1, 8, 8>(ctx, n, diag, upper, rhs, x, logdet); break;
             case 2: done = st_launch<2, 8, 4>(ctx, n, diag, upper, rhs, x, logdet); break;
-            case 3: done = st_launch<3, 8, SP_ST3_MB>(ctx, n, diag, upper, rhs, x, logdet); break;
+            case 3: done = st_launch<3, SP_ST3_NW, SP_ST3_MB>(ctx, n, diag, upper, rhs, x, logdet); break;
             case 4: done = st_launch<4, 4, 4>(ctx, n, diag, upper, rhs, x, logdet); break;
             default: break;
         }
